@@ -1,0 +1,139 @@
+"""ctypes view of oracle/liboracle.so — the CPU checker (TEST INFRASTRUCTURE).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg import
+this module. The product (paper_2103_04930_b200) never does.
+"""
+import ctypes
+import pathlib
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+_LIB = None
+
+f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = ROOT / "oracle" / "liboracle.so"
+        if not path.exists():
+            raise RuntimeError(f"{path} missing: run `make -C oracle oracle`")
+        L = ctypes.CDLL(str(path))
+        u64, u32, i, d = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_double
+        L.oracle_output_elems.argtypes = [u64, d]
+        L.oracle_output_elems.restype = u64
+        L.oracle_transfer_size.argtypes = [u32, u32, u32, u32, d]
+        L.oracle_transfer_size.restype = u64
+        L.oracle_segment_means.argtypes = [f32p, u64, d, f64p, u64]
+        L.oracle_segment_means.restype = i
+        L.oracle_mockpose_forward.argtypes = [f32p, u64, d, f32p, u64]
+        L.oracle_mockpose_forward.restype = i
+        L.oracle_gen_frame.argtypes = [u64, u32, u32, u32, f32p]
+        L.oracle_synth_blobs.argtypes = [u64, u8p, ctypes.c_size_t, u8p, ctypes.c_size_t]
+        L.oracle_bf16_round.argtypes = [ctypes.c_float]
+        L.oracle_bf16_round.restype = ctypes.c_float
+        L.oracle_conv2d_nhwc.argtypes = [f32p, i, i, i, i, f32p, f32p, i, i, i, i, f32p]
+        L.oracle_maxpool2_nhwc.argtypes = [f32p, i, i, i, i, f32p]
+        L.oracle_upsample_plane.argtypes = [f32p, i, i, i, f32p]
+        L.oracle_nms_plane.argtypes = [f32p, i, i, ctypes.c_float, i, i32p, f32p, f32p]
+        L.oracle_nms_plane.restype = i
+        _LIB = L
+    return _LIB
+
+
+def output_elems(e: int, c: float) -> int:
+    return int(lib().oracle_output_elems(e, c))
+
+
+def transfer_size(n, c, h, w, divisor) -> int:
+    return int(lib().oracle_transfer_size(n, c, h, w, divisor))
+
+
+class OracleError(Exception):
+    pass
+
+
+def segment_means(data: np.ndarray, divisor: float) -> np.ndarray:
+    data = np.ascontiguousarray(data, np.float32)
+    k = output_elems(data.size, divisor)
+    out = np.zeros(max(k, 1), np.float64)
+    rc = lib().oracle_segment_means(data, data.size, divisor, out, k)
+    if rc:
+        raise OracleError({1: "empty", 2: "degenerate_output", 3: "size"}[rc])
+    return out[:k]
+
+
+def mockpose_forward(data: np.ndarray, divisor: float) -> np.ndarray:
+    data = np.ascontiguousarray(data, np.float32).ravel()
+    k = output_elems(data.size, divisor)
+    out = np.zeros(max(k, 1), np.float32)
+    rc = lib().oracle_mockpose_forward(data, data.size, divisor, out, k)
+    if rc:
+        raise OracleError({1: "empty", 2: "degenerate_output", 3: "size"}[rc])
+    return out[:k]
+
+
+def gen_frame(seed: int, index: int, width: int, height: int) -> np.ndarray:
+    out = np.empty(3 * width * height, np.float32)
+    lib().oracle_gen_frame(seed, index, width, height, out)
+    return out
+
+
+def batched_frame(width: int, height: int, batch: int, seed: int = 7, first: int = 0) -> np.ndarray:
+    """`batch` harness frames folded into channels (3*batch) — the wire's batching."""
+    return np.concatenate([gen_frame(seed, first + b, width, height) for b in range(batch)])
+
+
+def synth_blobs(seed: int, structure_bytes: int, weights_bytes: int):
+    s = np.empty(structure_bytes, np.uint8)
+    w = np.empty(weights_bytes, np.uint8)
+    lib().oracle_synth_blobs(seed, s, s.size, w, w.size)
+    return s.tobytes(), w.tobytes()
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Vectorised RNE fp32 -> bf16 -> fp32 (same rule as oracle_bf16_round)."""
+    a = np.ascontiguousarray(a, np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    r = ((u + 0x7FFF + lsb) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32).reshape(a.shape)
+
+
+def conv2d_nhwc(x: np.ndarray, w: np.ndarray, b: np.ndarray, relu: bool, round_bf16: bool) -> np.ndarray:
+    n, h, wd, cin = x.shape
+    cout, cin2, k, _ = w.shape
+    assert cin == cin2
+    out = np.empty((n, h, wd, cout), np.float32)
+    lib().oracle_conv2d_nhwc(np.ascontiguousarray(x, np.float32), n, h, wd, cin,
+                             np.ascontiguousarray(w, np.float32), np.ascontiguousarray(b, np.float32),
+                             cout, k, int(relu), int(round_bf16), out)
+    return out
+
+
+def maxpool2_nhwc(x: np.ndarray) -> np.ndarray:
+    n, h, w, c = x.shape
+    out = np.empty((n, h // 2, w // 2, c), np.float32)
+    lib().oracle_maxpool2_nhwc(np.ascontiguousarray(x, np.float32), n, h, w, c, out)
+    return out
+
+
+def upsample_plane(x: np.ndarray, scale: int) -> np.ndarray:
+    h, w = x.shape
+    out = np.empty((h * scale, w * scale), np.float32)
+    lib().oracle_upsample_plane(np.ascontiguousarray(x, np.float32), h, w, scale, out)
+    return out
+
+
+def nms_plane(x: np.ndarray, threshold: float, max_peaks: int):
+    h, w = x.shape
+    xy = np.zeros(2 * max_peaks, np.int32)
+    ref = np.zeros(2 * max_peaks, np.float32)
+    sc = np.zeros(max_peaks, np.float32)
+    n = lib().oracle_nms_plane(np.ascontiguousarray(x, np.float32), h, w, threshold, max_peaks, xy, ref, sc)
+    return xy[: 2 * n].reshape(n, 2), ref[: 2 * n].reshape(n, 2), sc[:n]
