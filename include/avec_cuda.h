@@ -1,0 +1,125 @@
+/* avec_cuda.h — C-ABI of the B200 destination-side execution library.
+ *
+ * Drop-in boundary. The reference's server reaches compute only through the
+ * C++ plugin interface accelfwd::backend::Backend
+ * (proj/include/accelfwd/backend.hpp:64-78):
+ *     ModelHandle register_model(const ModelDescriptor&);   // backend.hpp:68-71
+ *     Heatmap     forward(ModelHandle, const Frame&);       // backend.hpp:73-75
+ *     std::string_view label() const;                       // backend.hpp:77
+ * and its implementation MockPoseBackend (proj/src/backend.cpp:69-96). This
+ * header is the C form of that interface (plain pointers and sizes, no C++ or
+ * torch types), so a reference-side shim or any FFI can bind
+ * it. One context per GPU; calls on one context may come from several threads
+ * (each forward takes one of the context's execution slots).
+ *
+ * Error behaviour mirrors the reference: every function returns an AVEC_*
+ * status; the message of the calling thread's last failure is avec_last_error().
+ * The codes map 1:1 onto what the reference backend throws:
+ *   AVEC_ERR_INVALID_ARGUMENT  std::invalid_argument (backend.cpp:92-93)
+ *   AVEC_ERR_UNKNOWN_MODEL     Error{unknown_model}  (backend.cpp:89)
+ *   AVEC_ERR_INVALID_MODEL     Error{invalid_model}  (backend.cpp:70-73)
+ *   AVEC_ERR_DEGENERATE_OUTPUT Error{degenerate_output} (backend.cpp:43-47)
+ *   AVEC_ERR_CUDA / _OUT_OF_MEMORY / _UNSUPPORTED: device failures, which the
+ *   server reports as WireError::internal (server.cpp:313-318).
+ */
+#ifndef AVEC_CUDA_H
+#define AVEC_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AVEC_OK 0
+#define AVEC_ERR_INVALID_ARGUMENT 1
+#define AVEC_ERR_UNKNOWN_MODEL 2
+#define AVEC_ERR_INVALID_MODEL 3
+#define AVEC_ERR_DEGENERATE_OUTPUT 4
+#define AVEC_ERR_CUDA 5
+#define AVEC_ERR_OUT_OF_MEMORY 6
+#define AVEC_ERR_UNSUPPORTED 7
+
+#define AVEC_MODEL_MOCKPOSE 0 /* opaque structure: reference segment-mean model */
+#define AVEC_MODEL_POSENET 1  /* structure carries an "avecnet" pose-net spec */
+
+typedef struct avec_ctx avec_ctx;
+
+/* Message of this thread's most recent failure ("" if none). */
+const char* avec_last_error(void);
+/* Library version string. */
+const char* avec_version(void);
+
+int avec_device_count(int* count);
+
+/* Context on one GPU with `slots` concurrent execution slots (stream + staging
+ * + workspace each); slots <= 0 picks the default (2). */
+int avec_ctx_create(int device, int slots, avec_ctx** out);
+void avec_ctx_destroy(avec_ctx* ctx);
+/* Backend::label() (backend.hpp:77), e.g. "b200:0". */
+const char* avec_ctx_label(const avec_ctx* ctx);
+
+/* Backend::register_model (backend.hpp:68-71; MockPoseBackend::register_model,
+ * backend.cpp:69-81). Idempotent per digest; handles start at 1 and stay
+ * resident until the context is destroyed. `digest` is the 32-byte
+ * model_digest (wire.cpp:70-79) the caller already verified. Structures that
+ * are not an avecnet spec register as the reference's segment-mean model. */
+int avec_model_register(avec_ctx* ctx, const uint8_t* digest32, const char* name,
+                        size_t name_len, const uint8_t* structure, size_t structure_len,
+                        const uint8_t* weights, uint64_t weights_len, double output_divisor,
+                        uint64_t* handle_out);
+int avec_model_kind(avec_ctx* ctx, uint64_t handle, int* kind_out);
+
+/* Output element count of one forward: round(E / divisor) for both model
+ * kinds (wire.cpp:18-22); for pose nets also equal to N*C_out*(H/8)*(W/8). */
+int avec_output_elems(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                      uint32_t w, uint64_t* out_elems);
+
+/* Backend::forward (backend.hpp:73-75; MockPoseBackend::forward, backend.cpp:83-96)
+ * on HOST buffers: H2D of `in`, kernels, D2H into `out`, synchronous.
+ * Pinned buffers (avec_host_alloc) are DMA'd directly; pageable ones move
+ * through the slot's double-buffered pinned staging. `compute_s` (may be NULL)
+ * receives the device time of the whole cycle (H2D..D2H) from CUDA events —
+ * what the server ships as ForwardResult.compute_s (wire.hpp:122). */
+int avec_forward(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                 const float* in, uint64_t in_elems, float* out, uint64_t out_elems,
+                 double* compute_s);
+
+/* Same computation on device-resident buffers of this context's GPU, enqueued
+ * on `cuda_stream` (a cudaStream_t; NULL = the slot's own stream, synchronous). */
+int avec_forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                        uint32_t w, const float* d_in, float* d_out, void* cuda_stream);
+
+/* Pose-net post-processing on device buffers (north-star kernel library):
+ * bilinear x`scale` upsample of `planes` fp32 maps and 3x3 peak NMS.
+ * peaks: [planes][max_peaks][5] = (x, y, refined_x, refined_y, score). */
+int avec_upsample_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, int scale,
+                         float* d_out, void* cuda_stream);
+int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, float threshold,
+                    int max_peaks, int* d_counts, float* d_peaks, void* cuda_stream);
+
+/* Debug/parity hook: run a forward like avec_forward and copy the input and
+ * output activations of conv layer `layer` (weights-blob order) as unpadded
+ * fp32 NHWC (input channels in the layer's own — Caffe — channel order). */
+int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                          uint32_t w, const float* in, int layer, float* layer_in,
+                          uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);
+/* Number of conv layers and the shape of layer i: cin, cout, k, level (log2 stride). */
+int avec_posenet_layer_info(avec_ctx* ctx, uint64_t handle, int layer, int* cin, int* cout,
+                            int* k, int* level, int* relu);
+int avec_posenet_num_layers(avec_ctx* ctx, uint64_t handle, int* n_layers);
+
+/* Deterministic weights for a pose-net spec: Caffe-order fp32 blob
+ * (per conv: W[cout][cin][k][k] then b[cout]). `out` NULL returns the size. */
+int avec_posenet_synth_weights(const uint8_t* structure, size_t structure_len, float* out,
+                               uint64_t* out_floats);
+
+/* Pinned (page-locked, portable) host memory for zero-copy ingest/egress. */
+void* avec_host_alloc(uint64_t bytes);
+void avec_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,254 @@
+"""Python mirror of the reference plugin interface, backed by the B200 C-ABI.
+
+Reference: accelfwd::backend (proj/include/accelfwd/backend.hpp:20-99) and
+accelfwd::wire model types (proj/include/accelfwd/wire.hpp:28-87). Names,
+argument meaning and error behaviour follow the reference so tests read like
+proj/tests/test_backend.cpp:
+  * register_model is idempotent per digest, handles start at 1;
+  * forward raises AvecError(name="unknown_model") for foreign handles,
+    AvecError(name="degenerate_output") for K<1 or K>E, ValueError (the
+    reference's std::invalid_argument) when data size disagrees with dims.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import hashlib
+import struct
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclasses.dataclass(frozen=True)
+class Dims:
+    """wire::Dims (wire.hpp:28-42)."""
+    batch: int = 1
+    channels: int = 1
+    height: int = 1
+    width: int = 1
+
+    def elem_count(self) -> int:
+        return self.batch * self.channels * self.height * self.width
+
+    def valid(self) -> bool:
+        return (self.batch >= 1 and self.channels >= 1 and 1 <= self.height <= 65535
+                and 1 <= self.width <= 65535)
+
+
+def model_digest(structure: bytes, weights: bytes, output_divisor: float) -> bytes:
+    """sha256(structure || weights || divisor as 8-byte LE double) — wire.cpp:70-79."""
+    h = hashlib.sha256()
+    h.update(structure)
+    h.update(weights)
+    h.update(struct.pack("<d", output_divisor))
+    return h.digest()
+
+
+@dataclasses.dataclass
+class ModelDescriptor:
+    """wire::ModelDescriptor (wire.hpp:73-79)."""
+    name: str
+    structure: bytes
+    weights: bytes
+    output_divisor: float
+    digest: bytes
+
+
+def make_model(name: str, structure: bytes, weights: bytes, output_divisor: float) -> ModelDescriptor:
+    """wire::make_model (wire.cpp:81-92): rejects divisor <= 0."""
+    if not output_divisor > 0.0:
+        raise _lib.AvecError(3, "output divisor must be > 0")
+    return ModelDescriptor(name, bytes(structure), bytes(weights), float(output_divisor),
+                           model_digest(structure, weights, output_divisor))
+
+
+@dataclasses.dataclass
+class Frame:
+    """backend::Frame (backend.hpp:22-25): flattened, batch-major fp32."""
+    dims: Dims
+    data: np.ndarray
+
+
+@dataclasses.dataclass
+class Heatmap:
+    """backend::Heatmap (backend.hpp:27-30)."""
+    data: np.ndarray
+
+    def elem_count(self) -> int:
+        return int(self.data.size)
+
+
+@dataclasses.dataclass(frozen=True)
+class ModelHandle:
+    """backend::ModelHandle (backend.hpp:34-37): valid ids start at 1."""
+    id: int = 0
+
+
+def output_elems(input_elems: int, divisor: float) -> int:
+    """wire::output_elems (wire.cpp:18-22): round half away from zero."""
+    if not divisor > 0.0:
+        raise ValueError("output divisor must be > 0")
+    k = input_elems / divisor
+    return int(np.floor(k + 0.5)) if k >= 0 else -int(np.floor(-k + 0.5))
+
+
+def device_count() -> int:
+    L = _lib.load()
+    n = ctypes.c_int(0)
+    _lib.check(L.avec_device_count(ctypes.byref(n)))
+    return n.value
+
+
+class B200Backend:
+    """Backend implementation on one B200 (one avec_ctx)."""
+
+    def __init__(self, device: int = 0, slots: int = 2):
+        self._L = _lib.load()
+        ctx = ctypes.c_void_p()
+        _lib.check(self._L.avec_ctx_create(device, slots, ctypes.byref(ctx)))
+        self._ctx = ctx
+        self.device = device
+
+    def close(self) -> None:
+        if self._ctx:
+            self._L.avec_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def ctx(self) -> ctypes.c_void_p:
+        return self._ctx
+
+    def label(self) -> str:
+        return self._L.avec_ctx_label(self._ctx).decode()
+
+    def register_model(self, model: ModelDescriptor) -> ModelHandle:
+        h = ctypes.c_uint64(0)
+        u8 = ctypes.POINTER(ctypes.c_uint8)
+        dig = (ctypes.c_uint8 * 32).from_buffer_copy(model.digest)
+        s = (ctypes.c_uint8 * max(len(model.structure), 1)).from_buffer_copy(model.structure or b"\0")
+        w = (ctypes.c_uint8 * max(len(model.weights), 1)).from_buffer_copy(model.weights or b"\0")
+        name = model.name.encode()
+        _lib.check(self._L.avec_model_register(
+            self._ctx, ctypes.cast(dig, u8), name, len(name), ctypes.cast(s, u8), len(model.structure),
+            ctypes.cast(w, u8), len(model.weights), model.output_divisor, ctypes.byref(h)))
+        return ModelHandle(h.value)
+
+    def model_kind(self, handle: ModelHandle) -> int:
+        k = ctypes.c_int(-1)
+        _lib.check(self._L.avec_model_kind(self._ctx, handle.id, ctypes.byref(k)))
+        return k.value
+
+    def output_elems(self, handle: ModelHandle, dims: Dims) -> int:
+        k = ctypes.c_uint64(0)
+        _lib.check(self._L.avec_output_elems(self._ctx, handle.id, dims.batch, dims.channels,
+                                             dims.height, dims.width, ctypes.byref(k)))
+        return k.value
+
+    def forward(self, handle: ModelHandle, frame: Frame, out: Optional[np.ndarray] = None,
+                timing: Optional[list] = None) -> Heatmap:
+        """Backend::forward on host buffers (H2D, kernels, D2H inside)."""
+        data = np.ascontiguousarray(frame.data, dtype=np.float32).ravel()
+        d = frame.dims
+        if data.size != d.elem_count():
+            raise ValueError("frame data size disagrees with dims")
+        k = self.output_elems(handle, d)
+        if out is None:
+            out = np.empty(k, np.float32)
+        secs = ctypes.c_double(0)
+        _lib.check(self._L.avec_forward(self._ctx, handle.id, d.batch, d.channels, d.height, d.width,
+                                        data.ctypes.data, data.size, out.ctypes.data, out.size,
+                                        ctypes.byref(secs)))
+        if timing is not None:
+            timing.append(secs.value)
+        return Heatmap(out)
+
+    def forward_device(self, handle: ModelHandle, dims: Dims, d_in: int, d_out: int,
+                       stream: int = 0) -> None:
+        """Device-resident forward (pointers of this GPU), enqueued on `stream`."""
+        _lib.check(self._L.avec_forward_device(self._ctx, handle.id, dims.batch, dims.channels,
+                                               dims.height, dims.width, d_in, d_out,
+                                               ctypes.c_void_p(stream) if stream else None))
+
+    # ---- pose-net extras ----
+    def num_layers(self, handle: ModelHandle) -> int:
+        n = ctypes.c_int(0)
+        _lib.check(self._L.avec_posenet_num_layers(self._ctx, handle.id, ctypes.byref(n)))
+        return n.value
+
+    def layer_info(self, handle: ModelHandle, layer: int) -> dict:
+        vals = [ctypes.c_int(0) for _ in range(5)]
+        _lib.check(self._L.avec_posenet_layer_info(self._ctx, handle.id, layer,
+                                                   *[ctypes.byref(v) for v in vals]))
+        return dict(zip(["cin", "cout", "k", "level", "relu"], [v.value for v in vals]))
+
+    def layer_io(self, handle: ModelHandle, frame: Frame, layer: int):
+        info = self.layer_info(handle, layer)
+        d = frame.dims
+        n_img = d.batch * d.channels // 3
+        hl, wl = d.height >> info["level"], d.width >> info["level"]
+        lin = np.empty((n_img, hl, wl, info["cin"]), np.float32)
+        lout = np.empty((n_img, hl, wl, info["cout"]), np.float32)
+        data = np.ascontiguousarray(frame.data, np.float32).ravel()
+        _lib.check(self._L.avec_posenet_layer_io(self._ctx, handle.id, d.batch, d.channels, d.height,
+                                                 d.width, data.ctypes.data, layer, lin.ctypes.data,
+                                                 lin.size, lout.ctypes.data, lout.size))
+        return lin, lout
+
+    def upsample_device(self, d_in: int, planes: int, h: int, w: int, scale: int, d_out: int,
+                        stream: int = 0) -> None:
+        _lib.check(self._L.avec_upsample_device(self._ctx, d_in, planes, h, w, scale, d_out,
+                                                ctypes.c_void_p(stream) if stream else None))
+
+    def nms_device(self, d_in: int, planes: int, h: int, w: int, threshold: float, max_peaks: int,
+                   d_counts: int, d_peaks: int, stream: int = 0) -> None:
+        _lib.check(self._L.avec_nms_device(self._ctx, d_in, planes, h, w, threshold, max_peaks,
+                                           d_counts, d_peaks,
+                                           ctypes.c_void_p(stream) if stream else None))
+
+
+def synth_posenet_weights(structure: bytes) -> np.ndarray:
+    """The engine's deterministic init for a spec (Caffe-order fp32 blob)."""
+    L = _lib.load()
+    n = ctypes.c_uint64(0)
+    u8 = ctypes.POINTER(ctypes.c_uint8)
+    s = (ctypes.c_uint8 * len(structure)).from_buffer_copy(structure)
+    _lib.check(L.avec_posenet_synth_weights(ctypes.cast(s, u8), len(structure), None, ctypes.byref(n)))
+    out = np.empty(n.value, np.float32)
+    _lib.check(L.avec_posenet_synth_weights(ctypes.cast(s, u8), len(structure),
+                                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                            ctypes.byref(n)))
+    return out
+
+
+class PinnedBuffer:
+    """Page-locked host buffer from avec_host_alloc, viewed as a numpy array."""
+
+    def __init__(self, n: int, dtype=np.float32):
+        self._L = _lib.load()
+        nbytes = int(n) * np.dtype(dtype).itemsize
+        self.ptr = self._L.avec_host_alloc(max(nbytes, 1))
+        if not self.ptr:
+            raise MemoryError(self._L.avec_last_error().decode())
+        buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(n))
+
+    def free(self):
+        if self.ptr:
+            self.array = None
+            self._L.avec_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

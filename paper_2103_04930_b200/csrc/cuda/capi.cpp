@@ -1,0 +1,237 @@
+// extern "C" boundary of libavec_cuda.so (include/avec_cuda.h). No exception
+// crosses it: every entry point converts avec::Error / std::exception into an
+// AVEC_* code plus a thread-local message.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "engine_impl.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return AVEC_OK;
+  } catch (const avec::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return AVEC_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return AVEC_ERR_CUDA;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) avec::fail(AVEC_ERR_INVALID_ARGUMENT, std::string(what) + " is NULL");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* avec_last_error(void) { return g_last_error.c_str(); }
+
+const char* avec_version(void) { return "avec-b200 0.1 (sm_100a)"; }
+
+int avec_device_count(int* count) {
+  return guarded([&] {
+    need(count, "count");
+    avec::check_cuda(cudaGetDeviceCount(count), "cudaGetDeviceCount");
+  });
+}
+
+int avec_ctx_create(int device, int slots, avec_ctx** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = nullptr;
+    auto* ctx = new avec_ctx();
+    try {
+      avec::ctx_init(ctx, device, slots);
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+void avec_ctx_destroy(avec_ctx* ctx) {
+  if (!ctx) return;
+  try {
+    avec::ctx_shutdown(ctx);
+  } catch (...) {
+  }
+  delete ctx;
+}
+
+const char* avec_ctx_label(const avec_ctx* ctx) { return ctx ? ctx->label.c_str() : ""; }
+
+int avec_model_register(avec_ctx* ctx, const uint8_t* digest32, const char* name, size_t name_len,
+                        const uint8_t* structure, size_t structure_len, const uint8_t* weights,
+                        uint64_t weights_len, double output_divisor, uint64_t* handle_out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(digest32, "digest");
+    need(handle_out, "handle_out");
+    if (weights_len && !weights) avec::fail(AVEC_ERR_INVALID_ARGUMENT, "weights is NULL");
+    *handle_out = avec::model_register(ctx, digest32, std::string(name ? name : "", name ? name_len : 0),
+                                       structure, structure_len, weights, weights_len,
+                                       output_divisor);
+  });
+}
+
+int avec_model_kind(avec_ctx* ctx, uint64_t handle, int* kind_out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(kind_out, "kind_out");
+    *kind_out = avec::model_lookup(ctx, handle).kind;
+  });
+}
+
+int avec_output_elems(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                      uint32_t w, uint64_t* out_elems) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out_elems, "out_elems");
+    *out_elems = avec::output_elems_for(avec::model_lookup(ctx, handle), n, c, h, w);
+  });
+}
+
+int avec_forward(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                 const float* in, uint64_t in_elems, float* out, uint64_t out_elems,
+                 double* compute_s) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(in, "in");
+    need(out, "out");
+    const double s = avec::forward_host(ctx, handle, n, c, h, w, in, in_elems, out, out_elems);
+    if (compute_s) *compute_s = s;
+  });
+}
+
+int avec_forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                        uint32_t w, const float* d_in, float* d_out, void* cuda_stream) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(d_in, "d_in");
+    need(d_out, "d_out");
+    avec::forward_device(ctx, handle, n, c, h, w, d_in, d_out,
+                         static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int avec_upsample_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, int scale,
+                         float* d_out, void* cuda_stream) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(d_in, "d_in");
+    need(d_out, "d_out");
+    if (planes < 1 || h < 1 || w < 1 || scale < 1) avec::fail(AVEC_ERR_INVALID_ARGUMENT, "bad upsample shape");
+    avec::check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    avec::launch_upsample(d_in, planes, h, w, scale, d_out, st);
+    if (!st) avec::check_cuda(cudaStreamSynchronize(st), "upsample sync");
+  });
+}
+
+int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, float threshold,
+                    int max_peaks, int* d_counts, float* d_peaks, void* cuda_stream) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(d_in, "d_in");
+    need(d_counts, "d_counts");
+    need(d_peaks, "d_peaks");
+    if (planes < 1 || h < 1 || w < 1 || max_peaks < 1) avec::fail(AVEC_ERR_INVALID_ARGUMENT, "bad nms shape");
+    avec::check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+    std::lock_guard<std::mutex> lk(ctx->post_m);
+    const size_t need_bytes = avec::nms_scratch_bytes(planes, h, w);
+    ctx->scratch.ensure(need_bytes, ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    avec::launch_nms(d_in, planes, h, w, threshold, max_peaks, d_counts, d_peaks, ctx->scratch.p,
+                     ctx->scratch.bytes, st);
+    // scratch is shared per context: drain before releasing it
+    avec::check_cuda(cudaStreamSynchronize(st), "nms sync");
+  });
+}
+
+int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                          uint32_t w, const float* in, int layer, float* layer_in,
+                          uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(in, "in");
+    need(layer_in, "layer_in");
+    need(layer_out, "layer_out");
+    avec::posenet_layer_io(ctx, handle, n, c, h, w, in, layer, layer_in, layer_in_elems, layer_out,
+                           layer_out_elems);
+  });
+}
+
+int avec_posenet_num_layers(avec_ctx* ctx, uint64_t handle, int* n_layers) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(n_layers, "n_layers");
+    auto m = avec::model_lookup(ctx, handle);
+    if (m.kind != AVEC_MODEL_POSENET) avec::fail(AVEC_ERR_INVALID_ARGUMENT, "not a pose net");
+    *n_layers = int(m.net->fam.convs.size());
+  });
+}
+
+int avec_posenet_layer_info(avec_ctx* ctx, uint64_t handle, int layer, int* cin, int* cout, int* k,
+                            int* level, int* relu) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    auto m = avec::model_lookup(ctx, handle);
+    if (m.kind != AVEC_MODEL_POSENET) avec::fail(AVEC_ERR_INVALID_ARGUMENT, "not a pose net");
+    if (layer < 0 || layer >= int(m.net->fam.convs.size()))
+      avec::fail(AVEC_ERR_INVALID_ARGUMENT, "layer index");
+    const auto& d = m.net->fam.convs[layer];
+    if (cin) *cin = d.cin;
+    if (cout) *cout = d.cout;
+    if (k) *k = d.k;
+    if (level) *level = d.level;
+    if (relu) *relu = d.relu;
+  });
+}
+
+int avec_posenet_synth_weights(const uint8_t* structure, size_t structure_len, float* out,
+                               uint64_t* out_floats) {
+  return guarded([&] {
+    need(structure, "structure");
+    need(out_floats, "out_floats");
+    auto fam = avec::parse_avecnet(structure, structure_len);
+    const uint64_t n = fam.weight_floats();
+    if (out) {
+      if (*out_floats < n) avec::fail(AVEC_ERR_INVALID_ARGUMENT, "output too small");
+      avec::synth_weights(fam, out);
+    }
+    *out_floats = n;
+  });
+}
+
+void* avec_host_alloc(uint64_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    g_last_error = "cudaHostAlloc failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void avec_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,767 @@
+// B200 engine: device handle table, execution slots with pinned double-buffered
+// staging, the segment-mean (reference MockPose) path and the pose-net plan
+// executor (tcgen05 convolutions captured into a CUDA graph per shape).
+//
+// Reference counterparts: MockPoseBackend::register_model / forward
+// (proj/src/backend.cpp:69-96) and the dispatch call site in
+// Server::dispatch_loop (proj/src/server.cpp:84-111).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "engine_impl.hpp"
+
+namespace avec {
+
+// ------------------------------------------------------------------ memory
+DevMem::~DevMem() { reset(); }
+void DevMem::reset() {
+  if (p) {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (device >= 0 && cur != device) cudaSetDevice(device);
+    cudaFree(p);
+    if (device >= 0 && cur != device) cudaSetDevice(cur);
+  }
+  p = nullptr;
+  bytes = 0;
+}
+void DevMem::ensure(size_t n, int dev) {
+  if (n <= bytes && p) return;
+  reset();
+  check_cuda(cudaMalloc(&p, n), "cudaMalloc");
+  bytes = n;
+  device = dev;
+}
+
+PinnedMem::~PinnedMem() {
+  if (p) cudaFreeHost(p);
+}
+void PinnedMem::ensure(size_t n) {
+  if (n <= bytes && p) return;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  check_cuda(cudaHostAlloc(&p, n, cudaHostAllocPortable), "cudaHostAlloc");
+  bytes = n;
+}
+
+Plan::~Plan() {
+  if (graph) cudaGraphExecDestroy(graph);
+}
+
+namespace {
+
+constexpr size_t kStageChunk = size_t(8) << 20;  // pinned staging chunk (bytes)
+
+uint16_t bf16_bits(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return uint16_t((u >> 16) | ((u & 0xffff) ? 0x40 : 0));
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+float bf16_value(float x) {
+  uint32_t u = uint32_t(bf16_bits(x)) << 16;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+// ---- TMA descriptors (driver entry point, no -lcuda link) ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    check_cuda(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000,
+                                                cudaEnableDefault, &q),
+               "cuTensorMapEncodeTiled entry point");
+    if (!f || q != cudaDriverEntryPointSuccess) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled missing");
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// 2D bf16 [rows][cols] row-major, box {64 cols, box_rows}, 128-byte swizzle
+CUtensorMap make_map_2d(const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// internal concat layout of a stage input: [trunk 128][L1 38][L2 19][pad]
+// vs Caffe's concat order [L1, L2, trunk] (prototxt concat_stageN)
+int concat_internal_channel(const PoseFamily& f, int caffe_ci) {
+  const int branches = f.paf_channels + f.heat_channels;
+  return caffe_ci < branches ? caffe_ci + f.trunk_channels : caffe_ci - branches;
+}
+
+bool is_stage_input_layer(const ConvDef& d, const PoseFamily& f) {
+  return d.cin == f.paf_channels + f.heat_channels + f.trunk_channels;
+}
+
+// ------------------------------------------------------------------ slots
+struct SlotLease {
+  avec_ctx* ctx;
+  int idx;
+  explicit SlotLease(avec_ctx* c) : ctx(c), idx(-1) {
+    std::unique_lock<std::mutex> lk(ctx->slot_m);
+    ctx->slot_cv.wait(lk, [&] {
+      for (size_t i = 0; i < ctx->slot_busy.size(); ++i)
+        if (!ctx->slot_busy[i]) return true;
+      return false;
+    });
+    for (size_t i = 0; i < ctx->slot_busy.size(); ++i)
+      if (!ctx->slot_busy[i]) {
+        idx = int(i);
+        ctx->slot_busy[i] = true;
+        break;
+      }
+  }
+  ~SlotLease() {
+    {
+      std::lock_guard<std::mutex> lk(ctx->slot_m);
+      ctx->slot_busy[idx] = false;
+    }
+    ctx->slot_cv.notify_one();
+  }
+  Slot* slot() const { return ctx->slots[idx].get(); }
+};
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// H2D through the slot's two pinned chunks: the CPU fills chunk i+1 while the
+// copy engine drains chunk i.
+void stage_h2d(Slot* s, void* d_dst, const void* h_src, size_t bytes) {
+  if (is_pinned(h_src)) {
+    check_cuda(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, s->stream), "H2D");
+    return;
+  }
+  size_t off = 0;
+  int i = 0;
+  while (off < bytes) {
+    const size_t len = std::min(kStageChunk, bytes - off);
+    const int b = i & 1;
+    check_cuda(cudaEventSynchronize(s->stage_ev[b]), "stage wait");
+    std::memcpy(s->stage[b].p, static_cast<const char*>(h_src) + off, len);
+    check_cuda(cudaMemcpyAsync(static_cast<char*>(d_dst) + off, s->stage[b].p, len,
+                               cudaMemcpyHostToDevice, s->stream),
+               "H2D chunk");
+    check_cuda(cudaEventRecord(s->stage_ev[b], s->stream), "stage record");
+    off += len;
+    ++i;
+  }
+}
+
+// D2H mirror: chunk i+1 is in flight while the CPU copies chunk i out.
+void stage_d2h(Slot* s, void* h_dst, const void* d_src, size_t bytes) {
+  if (is_pinned(h_dst)) {
+    check_cuda(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, s->stream), "D2H");
+    check_cuda(cudaEventRecord(s->ev1, s->stream), "ev1");
+    check_cuda(cudaStreamSynchronize(s->stream), "D2H sync");
+    return;
+  }
+  const size_t n = (bytes + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](size_t i) {
+    const size_t off = i * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    check_cuda(cudaMemcpyAsync(s->stage[i & 1].p, static_cast<const char*>(d_src) + off, len,
+                               cudaMemcpyDeviceToHost, s->stream),
+               "D2H chunk");
+    check_cuda(cudaEventRecord(s->stage_ev[i & 1], s->stream), "stage record");
+  };
+  if (n) issue(0);
+  for (size_t i = 0; i < n; ++i) {
+    if (i + 1 < n) issue(i + 1);
+    if (i + 1 == n) check_cuda(cudaEventRecord(s->ev1, s->stream), "ev1");
+    check_cuda(cudaEventSynchronize(s->stage_ev[i & 1]), "stage wait");
+    const size_t off = i * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    std::memcpy(static_cast<char*>(h_dst) + off, s->stage[i & 1].p, len);
+  }
+  check_cuda(cudaStreamSynchronize(s->stream), "D2H sync");
+}
+
+// ------------------------------------------------------------------ pose net
+std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float* weights) {
+  auto net = std::make_shared<PoseNet>();
+  net->fam = std::move(fam);
+  const PoseFamily& f = net->fam;
+  // layout: conv1_1 fp32 [27][64] + bias, then per tc layer bf16 W + fp32 bias
+  std::vector<size_t> w_off(f.convs.size()), b_off(f.convs.size());
+  size_t total = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = total;
+    total += (bytes + 1023) / 1024 * 1024;
+    return o;
+  };
+  net->layers.resize(f.convs.size());
+  for (size_t i = 0; i < f.convs.size(); ++i) {
+    ConvLayerDev& L = net->layers[i];
+    L.def = f.convs[i];
+    if (i == 0) {
+      w_off[i] = take(27 * 64 * 4);
+      b_off[i] = take(64 * 4);
+      continue;
+    }
+    L.cin_pad = round_up(L.def.cin, 64);
+    L.cout_pad = round_up(L.def.cout, 128);
+    w_off[i] = take(size_t(L.cout_pad) * L.def.k * L.def.k * L.cin_pad * 2);
+    b_off[i] = take(size_t(L.cout_pad) * 4);
+  }
+  std::vector<uint8_t> host(total, 0);
+  const float* src = weights;
+  for (size_t i = 0; i < f.convs.size(); ++i) {
+    ConvLayerDev& L = net->layers[i];
+    const ConvDef& d = L.def;
+    const int k = d.k;
+    if (i == 0) {
+      if (d.cin != 3 || d.cout != 64 || k != 3) fail(AVEC_ERR_INVALID_MODEL, "first layer must be 3->64 3x3");
+      float* w = reinterpret_cast<float*>(host.data() + w_off[i]);
+      for (int co = 0; co < 64; ++co)
+        for (int ci = 0; ci < 3; ++ci)
+          for (int r = 0; r < 3; ++r)
+            for (int s = 0; s < 3; ++s)
+              w[(ci * 9 + r * 3 + s) * 64 + co] = bf16_value(src[((co * 3 + ci) * 3 + r) * 3 + s]);
+      src += 64 * 27;
+      std::memcpy(host.data() + b_off[i], src, 64 * 4);
+      src += 64;
+      continue;
+    }
+    const bool perm = is_stage_input_layer(d, f);
+    if (perm && L.cin_pad != 192) fail(AVEC_ERR_INVALID_MODEL, "stage input must pad to 192");
+    uint16_t* w = reinterpret_cast<uint16_t*>(host.data() + w_off[i]);
+    for (int co = 0; co < d.cout; ++co)
+      for (int ci = 0; ci < d.cin; ++ci) {
+        const int cint = perm ? concat_internal_channel(f, ci) : ci;
+        for (int r = 0; r < k; ++r)
+          for (int s = 0; s < k; ++s)
+            w[(size_t(co) * k * k + r * k + s) * L.cin_pad + cint] =
+                bf16_bits(src[((size_t(co) * d.cin + ci) * k + r) * k + s]);
+      }
+    src += size_t(d.cout) * d.cin * k * k;
+    std::memcpy(host.data() + b_off[i], src, d.cout * 4);
+    src += d.cout;
+  }
+  check_cuda(cudaSetDevice(device), "cudaSetDevice");
+  net->mem.ensure(total, device);
+  check_cuda(cudaMemcpy(net->mem.p, host.data(), total, cudaMemcpyHostToDevice), "weights H2D");
+  char* base = net->mem.as<char>();
+  for (size_t i = 0; i < f.convs.size(); ++i) {
+    if (i == 0) {
+      net->first_w = reinterpret_cast<float*>(base + w_off[i]);
+      net->first_b = reinterpret_cast<float*>(base + b_off[i]);
+    } else {
+      net->layers[i].w = base + w_off[i];
+      net->layers[i].bias = reinterpret_cast<float*>(base + b_off[i]);
+    }
+  }
+  return net;
+}
+
+struct PlanBuilder {
+  Plan& plan;
+  const PoseNet& net;
+  int device;
+
+  int buffer(int level, int C) {
+    const Geometry& g = plan.geo[level];
+    auto m = std::make_unique<DevMem>();
+    const size_t bytes = size_t(plan.n) * g.Hp() * g.Wp() * C * 2;
+    m->ensure(bytes, device);
+    check_cuda(cudaMemset(m->p, 0, bytes), "zero activation buffer");  // zero border + pad channels
+    plan.bufs.push_back(std::move(m));
+    plan.buf_level.push_back(level);
+    plan.buf_c.push_back(C);
+    return int(plan.bufs.size()) - 1;
+  }
+
+  TensorView view(int buf, int c_off, int c, int perm = 0) {
+    TensorView v;
+    v.buf = buf;
+    v.level = buf >= 0 ? plan.buf_level[buf] : 3;
+    v.c_stride = buf >= 0 ? plan.buf_c[buf] : net.fam.out_channels();
+    v.c_off = c_off;
+    v.c = c;
+    v.concat_perm = perm;
+    return v;
+  }
+
+  void record_io(int layer, TensorView in, TensorView out) {
+    plan.layer_in[layer] = in;
+    plan.layer_out[layer] = out;
+  }
+
+  // one launch covering 1 or 2 conv layers (sibling branches) of equal shape
+  void conv(std::initializer_list<int> layers_il, std::initializer_list<TensorView> ins,
+            std::initializer_list<TensorView> outs) {
+    std::vector<int> layers(layers_il);
+    std::vector<TensorView> in(ins), out(outs);
+    PlanOp op;
+    op.kind = PlanOp::kConv;
+    ConvParams& p = op.cp;
+    const ConvLayerDev& L0 = net.layers[layers[0]];
+    const Geometry& gi = plan.geo[in[0].level];
+    p.k = L0.def.k;
+    p.cin_chunks = L0.cin_pad / 64;
+    p.in_c_off = in[0].c_off;
+    p.n_images = plan.n;
+    p.H = gi.H;
+    p.W = gi.W;
+    p.Hp = gi.Hp();
+    p.Wp = gi.Wp();
+    p.P = gi.P;
+    const bool to_output = out[0].buf == -1;
+    const Geometry& go = plan.geo[to_output ? 3 : out[0].level];
+    p.out_Hp = go.Hp();
+    p.out_Wp = go.Wp();
+    p.out_P = go.P;
+    p.out_nchw_f32 = to_output ? 1 : 0;
+    p.m_tiles = L0.cout_pad / 128;
+    p.tiles_per_image = (p.H * p.Wp + 511) / 512;
+    p.n_groups = int(layers.size());
+    p.total_tiles = p.n_groups * p.n_images * p.tiles_per_image * p.m_tiles;
+    for (size_t g = 0; g < layers.size(); ++g) {
+      const ConvLayerDev& L = net.layers[layers[g]];
+      if (L.def.k != p.k || L.cin_pad != L0.cin_pad || L.cout_pad != L0.cout_pad ||
+          in[g].c_off != p.in_c_off || (out[g].buf == -1) != to_output)
+        fail(AVEC_ERR_INVALID_MODEL, "grouped conv layers differ in shape");
+      ConvGroupParams& gp = p.g[g];
+      gp.bias = L.bias;
+      gp.out = to_output ? plan.out.p : plan.bufs[out[g].buf]->p;
+      gp.out_c_off = out[g].c_off;
+      gp.out_c_stride = out[g].c_stride;
+      gp.cout = L.def.cout;
+      gp.relu = L.def.relu;
+      const int ib = in[g].buf;
+      const uint64_t rows = uint64_t(plan.n) * gi.Hp() * gi.Wp();
+      op.maps.act_big[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 256);
+      op.maps.act_small[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 8);
+      op.maps.wgt[g] = make_map_2d(L.w, uint64_t(L.def.k) * L.def.k * L.cin_pad, L.cout_pad, 128);
+      op.layers[g] = layers[g];
+      record_io(layers[g], in[g], out[g]);
+    }
+    plan.ops.push_back(op);
+  }
+
+  void pool(int src, int dst) {
+    PlanOp op;
+    op.kind = PlanOp::kPool;
+    op.src = src;
+    op.dst = dst;
+    op.level = plan.buf_level[src];
+    op.C = plan.buf_c[src];
+    plan.ops.push_back(op);
+  }
+};
+
+// COCO program (pose_deploy_linevec.prototxt) on padded-flat buffers
+void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
+  const PoseFamily& f = net.fam;
+  PlanBuilder b{plan, net, device};
+  const int nl = int(f.convs.size());
+  plan.layer_in.assign(nl, TensorView{});
+  plan.layer_out.assign(nl, TensorView{});
+  int li = 0;
+  // level 0
+  const int a0 = b.buffer(0, 64), b0 = b.buffer(0, 64);
+  {
+    PlanOp op;
+    op.kind = PlanOp::kFirst;
+    op.dst = a0;
+    op.layers[0] = 0;
+    plan.ops.push_back(op);
+    TensorView in;
+    in.buf = -2;
+    in.c = 3;
+    b.record_io(0, in, b.view(a0, 0, 64));
+    ++li;
+  }
+  b.conv({li++}, {b.view(a0, 0, 64)}, {b.view(b0, 0, 64)});  // conv1_2
+  const int p1 = b.buffer(1, 64), a1 = b.buffer(1, 128), b1 = b.buffer(1, 128);
+  b.pool(b0, p1);
+  b.conv({li++}, {b.view(p1, 0, 64)}, {b.view(a1, 0, 128)});   // conv2_1
+  b.conv({li++}, {b.view(a1, 0, 128)}, {b.view(b1, 0, 128)});  // conv2_2
+  const int p2 = b.buffer(2, 128), a2 = b.buffer(2, 256), b2 = b.buffer(2, 256);
+  b.pool(b1, p2);
+  b.conv({li++}, {b.view(p2, 0, 128)}, {b.view(a2, 0, 256)});  // conv3_1
+  b.conv({li++}, {b.view(a2, 0, 256)}, {b.view(b2, 0, 256)});  // conv3_2
+  b.conv({li++}, {b.view(b2, 0, 256)}, {b.view(a2, 0, 256)});  // conv3_3
+  b.conv({li++}, {b.view(a2, 0, 256)}, {b.view(b2, 0, 256)});  // conv3_4
+  const int p3 = b.buffer(3, 256), a3 = b.buffer(3, 512), b3 = b.buffer(3, 512),
+            c3 = b.buffer(3, 256), cat = b.buffer(3, 192);
+  b.pool(b2, p3);
+  b.conv({li++}, {b.view(p3, 0, 256)}, {b.view(a3, 0, 512)});  // conv4_1
+  b.conv({li++}, {b.view(a3, 0, 512)}, {b.view(b3, 0, 512)});  // conv4_2
+  b.conv({li++}, {b.view(b3, 0, 512)}, {b.view(c3, 0, 256)});  // conv4_3_CPM
+  const int T = f.trunk_channels, C1 = f.paf_channels, C2 = f.heat_channels;
+  b.conv({li++}, {b.view(c3, 0, 256)}, {b.view(cat, 0, T)});   // conv4_4_CPM -> trunk slot
+  // branch buffers
+  const int l1a = b.buffer(3, 128), l1b = b.buffer(3, 128), l2a = b.buffer(3, 128),
+            l2b = b.buffer(3, 128), l1x = b.buffer(3, 512), l2x = b.buffer(3, 512);
+  const int s1 = li;  // stage 1: L1 layers s1..s1+4, L2 layers s1+5..s1+9
+  b.conv({s1 + 0, s1 + 5}, {b.view(cat, 0, T), b.view(cat, 0, T)}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
+  b.conv({s1 + 1, s1 + 6}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)}, {b.view(l1b, 0, 128), b.view(l2b, 0, 128)});
+  b.conv({s1 + 2, s1 + 7}, {b.view(l1b, 0, 128), b.view(l2b, 0, 128)}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
+  b.conv({s1 + 3, s1 + 8}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)}, {b.view(l1x, 0, 512), b.view(l2x, 0, 512)});
+  b.conv({s1 + 4, s1 + 9}, {b.view(l1x, 0, 512), b.view(l2x, 0, 512)},
+         {b.view(cat, T, C1), b.view(cat, T + C1, C2)});
+  li += 10;
+  for (int t = 2; t <= f.stages; ++t) {
+    const int s = li;  // L1: s..s+6, L2: s+7..s+13
+    const int catc = T + C1 + C2;
+    b.conv({s + 0, s + 7}, {b.view(cat, 0, catc, 1), b.view(cat, 0, catc, 1)},
+           {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
+    int x = l1a, y = l1b, u = l2a, v = l2b;
+    for (int i = 1; i <= 5; ++i) {  // Mconv2..5 (7x7) then Mconv6 (1x1)
+      b.conv({s + i, s + 7 + i}, {b.view(x, 0, 128), b.view(u, 0, 128)}, {b.view(y, 0, 128), b.view(v, 0, 128)});
+      std::swap(x, y);
+      std::swap(u, v);
+    }
+    if (t == f.stages) {
+      // wire output: [n][heat 19 | paf 38][H/8][W/8] fp32
+      b.conv({s + 6, s + 13}, {b.view(x, 0, 128), b.view(u, 0, 128)},
+             {b.view(-1, C2, C1), b.view(-1, 0, C2)});
+    } else {
+      b.conv({s + 6, s + 13}, {b.view(x, 0, 128), b.view(u, 0, 128)},
+             {b.view(cat, T, C1), b.view(cat, T + C1, C2)});
+    }
+    li += 14;
+  }
+  if (li != nl) fail(AVEC_ERR_INVALID_MODEL, "plan/layer table mismatch");
+}
+
+void run_ops(avec_ctx* ctx, const Plan& plan, const PoseNet& net, size_t first, size_t last,
+             cudaStream_t st) {
+  for (size_t i = first; i < last; ++i) {
+    const PlanOp& op = plan.ops[i];
+    switch (op.kind) {
+      case PlanOp::kFirst:
+        launch_conv_first(plan.in.as<float>(), plan.n, plan.H, plan.W, net.first_w, net.first_b,
+                          plan.bufs[op.dst]->p, plan.geo[0].P, st);
+        break;
+      case PlanOp::kConv:
+        launch_conv_tc(op.maps, op.cp, ctx->sms, st);
+        break;
+      case PlanOp::kPool: {
+        const Geometry& g = plan.geo[op.level];
+        launch_maxpool2(plan.bufs[op.src]->p, plan.n, g.H, g.W, g.P, op.C, plan.bufs[op.dst]->p,
+                        plan.geo[op.level + 1].P, st);
+        break;
+      }
+    }
+  }
+}
+
+Plan* get_plan(avec_ctx* ctx, Slot* slot, const Model& m, int n_img, int H, int W) {
+  auto key = std::make_tuple(m.id, n_img, H, W);
+  auto it = slot->plans.find(key);
+  if (it != slot->plans.end()) return it->second.get();
+  auto plan = std::make_unique<Plan>();
+  plan->n = n_img;
+  plan->H = H;
+  plan->W = W;
+  for (int l = 0; l < 4; ++l) plan->geo[l] = Geometry{H >> l, W >> l, l == 3 ? 3 : 1};
+  plan->in_elems = uint64_t(n_img) * 3 * H * W;
+  plan->out_elems = uint64_t(n_img) * m.net->fam.out_channels() * (H / 8) * (W / 8);
+  plan->in.ensure(plan->in_elems * 4, ctx->device);
+  plan->out.ensure(plan->out_elems * 4, ctx->device);
+  build_coco_plan(*plan, *m.net, ctx->device);
+  // capture the whole op sequence once; replays cost one launch
+  cudaGraph_t g = nullptr;
+  check_cuda(cudaStreamBeginCapture(slot->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+  try {
+    run_ops(ctx, *plan, *m.net, 0, plan->ops.size(), slot->stream);
+  } catch (...) {
+    cudaStreamEndCapture(slot->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  check_cuda(cudaStreamEndCapture(slot->stream, &g), "end capture");
+  cudaError_t e = cudaGraphInstantiate(&plan->graph, g, 0);
+  cudaGraphDestroy(g);
+  check_cuda(e, "graph instantiate");
+  Plan* raw = plan.get();
+  slot->plans.emplace(key, std::move(plan));
+  return raw;
+}
+
+void posenet_shape(const Model& m, uint32_t n, uint32_t c, uint32_t h, uint32_t w, int& n_img) {
+  const uint64_t chans = uint64_t(n) * c;
+  if (chans % 3 != 0)
+    fail(AVEC_ERR_INVALID_ARGUMENT, "pose net needs 3 channels per frame, got " + std::to_string(chans));
+  if (h % 8 || w % 8)
+    fail(AVEC_ERR_INVALID_ARGUMENT, "pose net needs height and width divisible by 8");
+  n_img = int(chans / 3);
+  const uint64_t E = chans * h * w;
+  const uint64_t K = uint64_t(n_img) * m.net->fam.out_channels() * (h / 8) * (w / 8);
+  const uint64_t law = uint64_t(std::llround(double(E) / m.divisor));
+  if (law != K)
+    fail(AVEC_ERR_INVALID_ARGUMENT, "output divisor " + std::to_string(m.divisor) +
+                                        " gives " + std::to_string(law) + " outputs, the net yields " +
+                                        std::to_string(K));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+void ctx_init(avec_ctx* ctx, int device, int slots) {
+  int count = 0;
+  check_cuda(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  if (device < 0 || device >= count)
+    fail(AVEC_ERR_INVALID_ARGUMENT, "no CUDA device " + std::to_string(device));
+  check_cuda(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop;
+  check_cuda(cudaGetDeviceProperties(&prop, device), "device properties");
+  if (prop.major != 10)
+    fail(AVEC_ERR_UNSUPPORTED, std::string("needs an sm_100 (B200) device, found ") + prop.name);
+  ctx->device = device;
+  ctx->sms = prop.multiProcessorCount;
+  ctx->label = "b200:" + std::to_string(device);
+  conv_configure();
+  if (slots <= 0) slots = 2;
+  for (int i = 0; i < slots; ++i) {
+    auto s = std::make_unique<Slot>();
+    s->index = i;
+    check_cuda(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
+    check_cuda(cudaEventCreate(&s->ev0), "event");
+    check_cuda(cudaEventCreate(&s->ev1), "event");
+    for (int b = 0; b < 2; ++b) {
+      check_cuda(cudaEventCreateWithFlags(&s->stage_ev[b], cudaEventDisableTiming), "event");
+      s->stage[b].ensure(kStageChunk);
+    }
+    ctx->slots.push_back(std::move(s));
+    ctx->slot_busy.push_back(false);
+  }
+}
+
+void ctx_shutdown(avec_ctx* ctx) {
+  cudaSetDevice(ctx->device);
+  for (auto& s : ctx->slots) {
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    s->plans.clear();
+    if (s->stream) cudaStreamDestroy(s->stream);
+    cudaEventDestroy(s->ev0);
+    cudaEventDestroy(s->ev1);
+    cudaEventDestroy(s->stage_ev[0]);
+    cudaEventDestroy(s->stage_ev[1]);
+  }
+  ctx->slots.clear();
+  ctx->models.clear();
+}
+
+uint64_t model_register(avec_ctx* ctx, const uint8_t* digest, const std::string& name,
+                        const uint8_t* structure, size_t structure_len, const uint8_t* weights,
+                        uint64_t weights_len, double divisor) {
+  // backend.cpp:70-73: divisor positive and finite, structure non-empty
+  if (!(divisor > 0.0) || !std::isfinite(divisor))
+    fail(AVEC_ERR_INVALID_MODEL, "output divisor must be positive and finite");
+  if (structure_len == 0 || !structure) fail(AVEC_ERR_INVALID_MODEL, "model structure is empty");
+  std::array<uint8_t, 32> key;
+  std::memcpy(key.data(), digest, 32);
+  {
+    std::lock_guard<std::mutex> lk(ctx->model_m);
+    auto it = ctx->id_by_digest.find(key);
+    if (it != ctx->id_by_digest.end()) return it->second;  // idempotent per digest
+  }
+  Model m;
+  m.divisor = divisor;
+  m.name = name;
+  if (is_avecnet(structure, structure_len)) {
+    PoseFamily fam = parse_avecnet(structure, structure_len);
+    const uint64_t nf = fam.weight_floats();
+    std::vector<float> synth;
+    const float* w = nullptr;
+    if (weights_len == 0) {
+      synth.resize(nf);
+      synth_weights(fam, synth.data());
+      w = synth.data();
+    } else if (weights_len == nf * 4) {
+      w = reinterpret_cast<const float*>(weights);
+    } else {
+      fail(AVEC_ERR_INVALID_MODEL, "pose-net weights must be " + std::to_string(nf * 4) +
+                                       " bytes (Caffe-order fp32), got " + std::to_string(weights_len));
+    }
+    m.kind = AVEC_MODEL_POSENET;
+    m.net = upload_posenet(ctx->device, std::move(fam), w);
+  }
+  std::lock_guard<std::mutex> lk(ctx->model_m);
+  auto it = ctx->id_by_digest.find(key);
+  if (it != ctx->id_by_digest.end()) return it->second;
+  m.id = ctx->next_id++;
+  ctx->id_by_digest.emplace(key, m.id);
+  ctx->models.emplace(m.id, m);
+  return m.id;
+}
+
+Model model_lookup(avec_ctx* ctx, uint64_t handle) {
+  std::lock_guard<std::mutex> lk(ctx->model_m);
+  auto it = ctx->models.find(handle);
+  if (it == ctx->models.end())
+    fail(AVEC_ERR_UNKNOWN_MODEL, "handle was never issued by this backend");
+  return it->second;
+}
+
+uint64_t output_elems_for(const Model& m, uint32_t n, uint32_t c, uint32_t h, uint32_t w) {
+  const uint64_t E = uint64_t(n) * c * h * w;
+  if (E == 0) fail(AVEC_ERR_INVALID_ARGUMENT, "empty input");
+  if (m.kind == AVEC_MODEL_POSENET) {
+    int n_img = 0;
+    posenet_shape(m, n, c, h, w, n_img);
+    return uint64_t(n_img) * m.net->fam.out_channels() * (h / 8) * (w / 8);
+  }
+  // backend.cpp:42-47
+  const uint64_t K = uint64_t(std::llround(double(E) / m.divisor));
+  if (K < 1) fail(AVEC_ERR_DEGENERATE_OUTPUT, "model yields zero output elements");
+  if (K > E) fail(AVEC_ERR_DEGENERATE_OUTPUT, "model yields more output elements than inputs");
+  return K;
+}
+
+double forward_host(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                    const float* in, uint64_t in_elems, float* out, uint64_t out_elems) {
+  const Model m = model_lookup(ctx, handle);
+  const uint64_t E = uint64_t(n) * c * h * w;
+  if (in_elems != E) fail(AVEC_ERR_INVALID_ARGUMENT, "frame data size disagrees with dims");
+  const uint64_t K = output_elems_for(m, n, c, h, w);
+  if (out_elems != K)
+    fail(AVEC_ERR_INVALID_ARGUMENT, "output buffer holds " + std::to_string(out_elems) +
+                                        " elements, forward yields " + std::to_string(K));
+  check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+  SlotLease lease(ctx);
+  Slot* s = lease.slot();
+  if (m.kind == AVEC_MODEL_POSENET) {
+    int n_img = 0;
+    posenet_shape(m, n, c, h, w, n_img);
+    Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
+    check_cuda(cudaEventRecord(s->ev0, s->stream), "ev0");
+    stage_h2d(s, plan->in.p, in, E * 4);
+    check_cuda(cudaGraphLaunch(plan->graph, s->stream), "graph launch");
+    stage_d2h(s, out, plan->out.p, K * 4);
+  } else {
+    s->d_in.ensure(E * 4, ctx->device);
+    s->d_out.ensure(K * 4, ctx->device);
+    check_cuda(cudaEventRecord(s->ev0, s->stream), "ev0");
+    stage_h2d(s, s->d_in.p, in, E * 4);
+    launch_segment_means(s->d_in.as<float>(), s->d_out.as<float>(), E, K, s->stream);
+    check_cuda(cudaGetLastError(), "segment-mean launch");
+    stage_d2h(s, out, s->d_out.p, K * 4);
+  }
+  float ms = 0.f;
+  check_cuda(cudaEventElapsedTime(&ms, s->ev0, s->ev1), "event time");
+  return double(ms) * 1e-3;
+}
+
+void forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                    const float* d_in, float* d_out, cudaStream_t stream) {
+  const Model m = model_lookup(ctx, handle);
+  const uint64_t E = uint64_t(n) * c * h * w;
+  const uint64_t K = output_elems_for(m, n, c, h, w);
+  check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+  SlotLease lease(ctx);
+  Slot* s = lease.slot();
+  cudaStream_t st = stream ? stream : s->stream;
+  if (m.kind == AVEC_MODEL_POSENET) {
+    int n_img = 0;
+    posenet_shape(m, n, c, h, w, n_img);
+    Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
+    // the captured graph reads/writes the plan's own buffers
+    check_cuda(cudaMemcpyAsync(plan->in.p, d_in, E * 4, cudaMemcpyDeviceToDevice, st), "D2D in");
+    check_cuda(cudaGraphLaunch(plan->graph, st), "graph launch");
+    check_cuda(cudaMemcpyAsync(d_out, plan->out.p, K * 4, cudaMemcpyDeviceToDevice, st), "D2D out");
+  } else {
+    launch_segment_means(d_in, d_out, E, K, st);
+  }
+  // plan buffers belong to the slot: drain before the lease is released
+  check_cuda(cudaStreamSynchronize(st), "forward sync");
+}
+
+void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                      uint32_t w, const float* in, int layer, float* layer_in,
+                      uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems) {
+  const Model m = model_lookup(ctx, handle);
+  if (m.kind != AVEC_MODEL_POSENET) fail(AVEC_ERR_INVALID_ARGUMENT, "not a pose net");
+  int n_img = 0;
+  posenet_shape(m, n, c, h, w, n_img);
+  const PoseFamily& f = m.net->fam;
+  if (layer < 0 || layer >= int(f.convs.size())) fail(AVEC_ERR_INVALID_ARGUMENT, "layer index");
+  const ConvDef& d = f.convs[layer];
+  const int Hl = int(h) >> d.level, Wl = int(w) >> d.level;
+  const uint64_t need_in = uint64_t(n_img) * Hl * Wl * d.cin;
+  const uint64_t need_out = uint64_t(n_img) * Hl * Wl * d.cout;
+  if (layer_in_elems != need_in || layer_out_elems != need_out)
+    fail(AVEC_ERR_INVALID_ARGUMENT, "layer buffers have the wrong size");
+  check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+  SlotLease lease(ctx);
+  Slot* s = lease.slot();
+  Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
+  const uint64_t E = uint64_t(n) * c * h * w;
+  check_cuda(cudaMemcpy(plan->in.p, in, E * 4, cudaMemcpyHostToDevice), "H2D");
+  size_t last = 0;
+  for (size_t i = 0; i < plan->ops.size(); ++i)
+    if (plan->ops[i].layers[0] == layer || plan->ops[i].layers[1] == layer) last = i + 1;
+  run_ops(ctx, *plan, *m.net, 0, last, s->stream);
+  check_cuda(cudaStreamSynchronize(s->stream), "layer io sync");
+  auto fetch = [&](const TensorView& v, int cdim, float* dst) {
+    const Geometry& g = plan->geo[d.level];
+    if (v.buf == -2) {  // network input as the first layer sees it: bf16(x - 0.5), NHWC
+      for (int b = 0; b < n_img; ++b)
+        for (int y = 0; y < Hl; ++y)
+          for (int x = 0; x < Wl; ++x)
+            for (int ch = 0; ch < 3; ++ch)
+              dst[((size_t(b) * Hl + y) * Wl + x) * 3 + ch] =
+                  bf16_value(in[((size_t(b) * 3 + ch) * Hl + y) * Wl + x] - 0.5f);
+      return;
+    }
+    if (v.buf == -1) {  // fp32 NCHW plan output -> NHWC channel range
+      std::vector<float> all(plan->out_elems);
+      check_cuda(cudaMemcpy(all.data(), plan->out.p, all.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+      const int C = f.out_channels();
+      for (int b = 0; b < n_img; ++b)
+        for (int ch = 0; ch < cdim; ++ch)
+          for (int y = 0; y < Hl; ++y)
+            for (int x = 0; x < Wl; ++x)
+              dst[((size_t(b) * Hl + y) * Wl + x) * cdim + ch] =
+                  all[((size_t(b) * C + v.c_off + ch) * Hl + y) * Wl + x];
+      return;
+    }
+    const int grab = v.concat_perm ? v.c_stride : v.c;
+    const int off = v.concat_perm ? 0 : v.c_off;
+    DevMem tmp;
+    tmp.ensure(size_t(n_img) * Hl * Wl * grab * 4, ctx->device);
+    launch_unpad_to_f32(plan->bufs[v.buf]->p, n_img, Hl, Wl, g.P, v.c_stride, off, grab,
+                        tmp.as<float>(), s->stream);
+    std::vector<float> hostv(size_t(n_img) * Hl * Wl * grab);
+    check_cuda(cudaMemcpyAsync(hostv.data(), tmp.p, hostv.size() * 4, cudaMemcpyDeviceToHost, s->stream), "D2H");
+    check_cuda(cudaStreamSynchronize(s->stream), "sync");
+    for (size_t p = 0; p < size_t(n_img) * Hl * Wl; ++p)
+      for (int ch = 0; ch < cdim; ++ch) {
+        const int src_ch = v.concat_perm ? concat_internal_channel(f, ch) : ch;
+        dst[p * cdim + ch] = hostv[p * grab + src_ch];
+      }
+  };
+  fetch(plan->layer_in[layer], d.cin, layer_in);
+  fetch(plan->layer_out[layer], d.cout, layer_out);
+}
+
+}  // namespace avec

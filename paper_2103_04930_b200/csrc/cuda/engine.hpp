@@ -1,0 +1,57 @@
+// Internal interfaces of the B200 engine behind the C-ABI (include/avec_cuda.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../../include/avec_cuda.h"
+
+namespace avec {
+
+// error carrying an AVEC_* status code; converted to a return code at the ABI
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(e == cudaErrorMemoryAllocation ? AVEC_ERR_OUT_OF_MEMORY : AVEC_ERR_CUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- kernels (one .cu each) ----
+void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K,
+                          cudaStream_t stream);
+
+// input fp32 NCHW frames -> (x - 0.5) -> bf16 -> conv 3x3 (3 -> 64) + bias + ReLU
+// -> bf16 padded-flat NHWC [n][H+2P][W+2P][64]
+void launch_conv_first(const float* d_in, int n, int H, int W, const float* w_fp32_27x64,
+                       const float* bias64, void* d_out, int P, cudaStream_t stream);
+
+// 2x2/2 max pool, padded-flat NHWC bf16 -> padded-flat NHWC bf16
+void launch_maxpool2(const void* d_in, int n, int H, int W, int P_in, int C, void* d_out,
+                     int P_out, cudaStream_t stream);
+
+// gather an unpadded fp32 NHWC copy of channels [c_off, c_off+c) of a padded buffer
+void launch_unpad_to_f32(const void* d_in, int n, int H, int W, int P, int C_stride, int c_off,
+                         int c, float* d_out, cudaStream_t stream);
+
+// bilinear x`scale` upsample of fp32 planes [planes][h][w] -> [planes][h*s][w*s]
+void launch_upsample(const float* d_in, int planes, int h, int w, int scale, float* d_out,
+                     cudaStream_t stream);
+
+// 3x3 NMS on fp32 planes [planes][H][W]; per plane up to max_peaks peaks in
+// raster order as (x, y, refined_x, refined_y, score) and a count
+void launch_nms(const float* d_in, int planes, int H, int W, float threshold, int max_peaks,
+                int* d_counts, float* d_peaks, void* d_scratch, size_t scratch_bytes,
+                cudaStream_t stream);
+size_t nms_scratch_bytes(int planes, int H, int W);
+
+}  // namespace avec

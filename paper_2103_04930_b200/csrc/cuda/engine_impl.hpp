@@ -1,0 +1,151 @@
+// Engine state behind avec_ctx: device handle table, execution slots,
+// pinned staging, pose-net plans. Internal to libavec_cuda.so.
+#pragma once
+
+#include <array>
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "conv_tc.cuh"
+#include "engine.hpp"
+#include "netspec.hpp"
+
+namespace avec {
+
+// owning device allocation (freed on the device it came from)
+struct DevMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  ~DevMem();
+  void reset();
+  // grow-only; contents are not preserved
+  void ensure(size_t n, int dev);
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  PinnedMem() = default;
+  PinnedMem(const PinnedMem&) = delete;
+  PinnedMem& operator=(const PinnedMem&) = delete;
+  ~PinnedMem();
+  void ensure(size_t n);
+};
+
+// one conv layer resident on the device (bf16 packed for the TMA/UMMA path)
+struct ConvLayerDev {
+  ConvDef def;
+  int cin_pad = 0, cout_pad = 0;
+  void* w = nullptr;      // bf16 [cout_pad][k*k][cin_pad]
+  float* bias = nullptr;  // [cout_pad]
+};
+
+struct PoseNet {
+  PoseFamily fam;
+  std::vector<ConvLayerDev> layers;
+  DevMem mem;                  // all weights of this device
+  float* first_w = nullptr;    // conv1_1 as fp32 [27][64] (bf16-representable values)
+  float* first_b = nullptr;
+};
+
+struct Geometry {
+  int H = 0, W = 0, P = 0;
+  int Hp() const { return H + 2 * P; }
+  int Wp() const { return W + 2 * P; }
+};
+
+// a channel range of a plan buffer (or the fp32 NCHW output when buf < 0)
+struct TensorView {
+  int buf = -1;  // index into Plan::bufs; -1 = plan output (fp32 NCHW), -2 = plan input
+  int level = 0;
+  int c_stride = 0, c_off = 0, c = 0;
+  int concat_perm = 0;  // 1: channels are the internal concat layout of a stage input
+};
+
+struct PlanOp {
+  enum Kind { kFirst, kConv, kPool } kind = kConv;
+  ConvParams cp{};
+  ConvMaps maps{};
+  int layers[2] = {-1, -1};
+  int src = -1, dst = -1, level = 0, C = 0;  // pool: src/dst buffers
+};
+
+struct Plan {
+  int n = 0, H = 0, W = 0;
+  Geometry geo[4];
+  std::vector<std::unique_ptr<DevMem>> bufs;
+  std::vector<int> buf_level, buf_c;
+  std::vector<PlanOp> ops;
+  std::vector<TensorView> layer_in, layer_out;
+  DevMem in, out;  // fp32 NCHW frames in, fp32 NCHW net output
+  uint64_t in_elems = 0, out_elems = 0;
+  cudaGraphExec_t graph = nullptr;
+  ~Plan();
+};
+
+struct Slot {
+  int index = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  PinnedMem stage[2];
+  DevMem d_in, d_out;  // segment-mean path
+  std::map<std::tuple<uint64_t, int, int, int>, std::unique_ptr<Plan>> plans;
+};
+
+struct Model {
+  uint64_t id = 0;
+  int kind = AVEC_MODEL_MOCKPOSE;
+  double divisor = 1.0;
+  std::string name;
+  std::shared_ptr<PoseNet> net;
+};
+
+}  // namespace avec
+
+struct avec_ctx {
+  int device = 0;
+  int sms = 148;
+  std::string label;
+  std::vector<std::unique_ptr<avec::Slot>> slots;
+  std::vector<bool> slot_busy;
+  std::mutex slot_m;
+  std::condition_variable slot_cv;
+  std::mutex model_m;
+  std::map<std::array<uint8_t, 32>, uint64_t> id_by_digest;
+  std::map<uint64_t, avec::Model> models;
+  uint64_t next_id = 1;
+  avec::DevMem scratch;  // post-processing scratch (guarded by post_m)
+  std::mutex post_m;
+};
+
+namespace avec {
+
+// engine entry points used by capi.cpp
+void ctx_init(avec_ctx* ctx, int device, int slots);
+void ctx_shutdown(avec_ctx* ctx);
+uint64_t model_register(avec_ctx* ctx, const uint8_t* digest, const std::string& name,
+                        const uint8_t* structure, size_t structure_len, const uint8_t* weights,
+                        uint64_t weights_len, double divisor);
+Model model_lookup(avec_ctx* ctx, uint64_t handle);
+uint64_t output_elems_for(const Model& m, uint32_t n, uint32_t c, uint32_t h, uint32_t w);
+double forward_host(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                    const float* in, uint64_t in_elems, float* out, uint64_t out_elems);
+void forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                    const float* d_in, float* d_out, cudaStream_t stream);
+void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                      uint32_t w, const float* in, int layer, float* layer_in,
+                      uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);
+
+}  // namespace avec
