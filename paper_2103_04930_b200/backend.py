@@ -203,6 +203,22 @@ class B200Backend:
                                                  lin.size, lout.ctypes.data, lout.size))
         return lin, lout
 
+    def profile(self, handle: ModelHandle, dims: Dims, d_in: int, reps: int = 3) -> list:
+        """Per-launch device timings of the pose-net plan (see avec_posenet_profile)."""
+        n = ctypes.c_int(0)
+        cap = 256
+        kind = np.zeros(cap, np.int32)
+        flops = np.zeros(cap, np.float64)
+        nbytes = np.zeros(cap, np.float64)
+        ms = np.zeros(cap, np.float32)
+        _lib.check(self._L.avec_posenet_profile(
+            self._ctx, handle.id, dims.batch, dims.channels, dims.height, dims.width, d_in, reps, cap,
+            ctypes.byref(n), kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), flops.ctypes.data,
+            nbytes.ctypes.data, ms.ctypes.data))
+        names = {0: "conv_first", 1: "conv_tc", 2: "maxpool"}
+        return [dict(kind=names[int(kind[i])], flops=float(flops[i]), bytes=float(nbytes[i]),
+                     ms=float(ms[i])) for i in range(n.value)]
+
     def upsample_device(self, d_in: int, planes: int, h: int, w: int, scale: int, d_out: int,
                         stream: int = 0) -> None:
         _lib.check(self._L.avec_upsample_device(self._ctx, d_in, planes, h, w, scale, d_out,

@@ -178,6 +178,24 @@ int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c
   });
 }
 
+int avec_posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                         uint32_t w, const float* d_in, int reps, int max_ops, int* n_ops,
+                         int* op_kind, double* op_flops, double* op_bytes, float* op_ms) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(d_in, "d_in");
+    need(n_ops, "n_ops");
+    auto prof = avec::posenet_profile(ctx, handle, n, c, h, w, d_in, reps < 1 ? 1 : reps);
+    *n_ops = int(prof.size());
+    for (int i = 0; i < int(prof.size()) && i < max_ops; ++i) {
+      if (op_kind) op_kind[i] = prof[i].kind;
+      if (op_flops) op_flops[i] = prof[i].flops;
+      if (op_bytes) op_bytes[i] = prof[i].bytes;
+      if (op_ms) op_ms[i] = prof[i].ms;
+    }
+  });
+}
+
 int avec_posenet_num_layers(avec_ctx* ctx, uint64_t handle, int* n_layers) {
   return guarded([&] {
     need(ctx, "ctx");

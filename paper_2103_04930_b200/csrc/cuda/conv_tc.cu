@@ -11,25 +11,33 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kTileM = 128;            // output channels per tile (MMA M)
-constexpr int kSubN = 256;             // pixels per MMA (MMA N)
-constexpr int kSubs = 2;               // MMAs per tile sharing one weight k-block
-constexpr int kTileN = kSubN * kSubs;  // pixels per tile
-constexpr int kWinRows = kTileN + 8;   // window rows (covers k-1 <= 7 extra rows)
-constexpr int kWinBytes = kWinRows * 128;
-constexpr int kWinStages = 2;
+constexpr int kTileM = 128;   // output channels per tile (MMA M)
+constexpr int kSubN = 256;    // pixels per MMA (MMA N)
 constexpr int kWgtBytes = kTileM * 128;  // 128 rows x 64 bf16
-constexpr int kWgtStages = 5;
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
+constexpr int kChunk = 32;                      // epilogue pixels per TMEM load / TMA store
+constexpr int kStageBytes = 2 * kChunk * 128;   // two 64-channel halves of 32 rows x 128 B
+constexpr int kEpiThreads = 128;
+constexpr int kEpiBar = 1;                      // named barrier id for the 4 epilogue warps
 
-struct SmemLayout {
+template <int SUBS>
+struct Cfg {
+  static constexpr int kTileN = kSubN * SUBS;
+  static constexpr int kWinRows = kTileN + 8;   // + (k-1) <= 7 halo rows, 8-aligned
+  static constexpr int kWinBytes = kWinRows * 128;
+  static constexpr int kWinStages = 2;
+  static constexpr int kAccStages = 2 / SUBS;   // TMEM holds 512 fp32 columns
+  static constexpr int kWgtStages = SUBS == 2 ? 4 : 8;
   static constexpr int win = 0;
   static constexpr int wgt = win + kWinStages * kWinBytes;
-  static constexpr int bars = wgt + kWgtStages * kWgtBytes;
+  static constexpr int stg = wgt + kWgtStages * kWgtBytes;
+  static constexpr int bars = stg + 2 * kStageBytes;
   static constexpr int total = bars + 256;
+  static_assert(kWinBytes % 1024 == 0 && wgt % 1024 == 0 && stg % 1024 == 0,
+                "SW128 operands need 1024 B alignment");
+  static_assert(total + 1024 <= 232448, "smem budget");
 };
-static_assert(SmemLayout::wgt % 1024 == 0, "SW128 operands need 1024 B alignment");
 
 struct TileCoord {
   int g, n, pt, mt;
@@ -47,21 +55,29 @@ __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t) {
   return c;
 }
 
+__device__ __forceinline__ float activate(uint32_t bits, float bias, int relu) {
+  float x = __uint_as_float(bits) + bias;
+  return relu ? fmaxf(x, 0.f) : x;
+}
+
+template <int SUBS>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p) {
+  using C = Cfg<SUBS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* win = smem + SmemLayout::win;
-  uint8_t* wgt = smem + SmemLayout::wgt;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
+  uint8_t* win = smem + C::win;
+  uint8_t* wgt = smem + C::wgt;
+  uint8_t* stg = smem + C::stg;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::bars);
   uint64_t* win_full = bars;
-  uint64_t* win_empty = bars + kWinStages;
-  uint64_t* w_full = bars + 2 * kWinStages;
-  uint64_t* w_empty = w_full + kWgtStages;
-  uint64_t* acc_full = w_empty + kWgtStages;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* win_empty = win_full + C::kWinStages;
+  uint64_t* w_full = win_empty + C::kWinStages;
+  uint64_t* w_empty = w_full + C::kWgtStages;
+  uint64_t* acc_full = w_empty + C::kWgtStages;
+  uint64_t* acc_empty = acc_full + C::kAccStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::kAccStages);
 
   const uint32_t warp = warp_id();
   if (warp == 0 && elect_one()) {
@@ -69,17 +85,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch(&maps.act_big[g]);
       tma_prefetch(&maps.act_small[g]);
       tma_prefetch(&maps.wgt[g]);
+      if (p.out_mode == kOutTmaBf16) tma_prefetch(&maps.out[g]);
     }
-    for (int i = 0; i < kWinStages; ++i) {
+    for (int i = 0; i < C::kWinStages; ++i) {
       mbar_init(&win_full[i], 1);
       mbar_init(&win_empty[i], 1);
     }
-    for (int i = 0; i < kWgtStages; ++i) {
+    for (int i = 0; i < C::kWgtStages; ++i) {
       mbar_init(&w_full[i], 1);
       mbar_init(&w_empty[i], 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 128);
+    for (int i = 0; i < C::kAccStages; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kEpiThreads);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -87,11 +106,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch: everything above overlapped the previous
+  // layer's tail; from here on we read its output and overwrite buffers it
+  // may still read, so wait for it to complete, then let the next layer launch.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int k = p.k;
   const int pad = k / 2;
-  const int kblocks_per_tile = p.cin_chunks * k * k;
-  (void)kblocks_per_tile;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -99,28 +121,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t keep = policy_evict_last();
       int ws = 0, wst = 0;
       uint32_t wph = 0, wtph = 0;
-      const uint32_t win_tx = (k > 1 ? kWinRows : kTileN) * 128;
+      const uint32_t win_tx = (C::kTileN + (k > 1 ? 8 : 0)) * 128;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
         const TileCoord tc = decode_tile(p, t);
-        const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + tc.pt * kTileN;
+        const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + tc.pt * C::kTileN;
         for (int c = 0; c < p.cin_chunks; ++c) {
           const int ch = p.in_c_off + c * 64;
           for (int r = 0; r < k; ++r) {
             mbar_wait(&win_empty[ws], wph ^ 1);
             mbar_arrive_expect_tx(&win_full[ws], win_tx);
-            uint8_t* wbuf = win + ws * kWinBytes;
+            uint8_t* wbuf = win + ws * C::kWinBytes;
             const int wr = row0 + r * p.Wp;
-            tma_load_2d(wbuf, &maps.act_big[tc.g], &win_full[ws], ch, wr);
-            tma_load_2d(wbuf + 256 * 128, &maps.act_big[tc.g], &win_full[ws], ch, wr + 256);
+#pragma unroll
+            for (int b = 0; b < SUBS; ++b)
+              tma_load_2d(wbuf + b * kSubN * 128, &maps.act_big[tc.g], &win_full[ws], ch, wr + b * kSubN);
             if (k > 1)
-              tma_load_2d(wbuf + 512 * 128, &maps.act_small[tc.g], &win_full[ws], ch, wr + 512);
-            if (++ws == kWinStages) { ws = 0; wph ^= 1; }
+              tma_load_2d(wbuf + C::kTileN * 128, &maps.act_small[tc.g], &win_full[ws], ch,
+                          wr + C::kTileN);
+            if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
             for (int s = 0; s < k; ++s) {
               mbar_wait(&w_empty[wst], wtph ^ 1);
               mbar_arrive_expect_tx(&w_full[wst], kWgtBytes);
               tma_load_2d_hint(wgt + wst * kWgtBytes, &maps.wgt[tc.g], &w_full[wst],
                                ((r * k + s) * p.cin_chunks + c) * 64, tc.mt * kTileM, keep);
-              if (++wst == kWgtStages) { wst = 0; wtph ^= 1; }
+              if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
             }
           }
         }
@@ -130,91 +154,122 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
       const uint32_t idesc = idesc_bf16_f32(kTileM, kSubN);
-      int ws = 0, wst = 0;
+      int ws = 0, wst = 0, acc = 0;
       uint32_t wph = 0, wtph = 0, aph = 0;
       const uint32_t win_base = smem_u32(win), wgt_base = smem_u32(wgt);
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-        mbar_wait(acc_empty, aph ^ 1);
+        mbar_wait(&acc_empty[acc], aph ^ 1);
         tc_fence_after();
+        const uint32_t d0 = tmem + acc * C::kTileN;
         bool first = true;
         for (int c = 0; c < p.cin_chunks; ++c) {
           for (int r = 0; r < k; ++r) {
             mbar_wait(&win_full[ws], wph);
             tc_fence_after();
-            const uint32_t wb = win_base + ws * kWinBytes;
+            const uint32_t wb = win_base + ws * C::kWinBytes;
             for (int s = 0; s < k; ++s) {
               mbar_wait(&w_full[wst], wtph);
               tc_fence_after();
               const uint32_t ab = wgt_base + wst * kWgtBytes;
 #pragma unroll
-              for (int sub = 0; sub < kSubs; ++sub) {
+              for (int sub = 0; sub < SUBS; ++sub) {
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                   const uint64_t ad = desc_sw128(ab + kk * 32);
                   const uint64_t bd = desc_sw128(wb + (sub * kSubN + s) * 128 + kk * 32);
-                  mma_bf16_ss(tmem + sub * kSubN, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+                  mma_bf16_ss(d0 + sub * kSubN, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
                 }
               }
               first = false;
               mma_commit(&w_empty[wst]);
-              if (++wst == kWgtStages) { wst = 0; wtph ^= 1; }
+              if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
             }
             mma_commit(&win_empty[ws]);
-            if (++ws == kWinStages) { ws = 0; wph ^= 1; }
+            if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
           }
         }
-        mma_commit(acc_full);
-        aph ^= 1;
+        mma_commit(&acc_full[acc]);
+        if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
     const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may touch
-    const int co_local = quad * 32 + lane_id();
+    const uint32_t lane = lane_id();
+    const int co_local = quad * 32 + lane;
+    const bool leader = threadIdx.x == 64;
+    int acc = 0, stg_i = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       const TileCoord tc = decode_tile(p, t);
       const ConvGroupParams& g = p.g[tc.g];
       const int co = tc.mt * kTileM + co_local;
-      const bool live = co < g.cout;
+      const int cout_m = min(kTileM, g.cout - tc.mt * kTileM);  // channels of this m-tile
+      const bool live = co_local < cout_m;
       const float bias = live ? g.bias[co] : 0.f;
-      mbar_wait(acc_full, aph);
+      mbar_wait(&acc_full[acc], aph);
       tc_fence_after();
-      for (int sub = 0; sub < kSubs; ++sub) {
-        const int o0 = tc.pt * kTileN + sub * kSubN;
-        int h = o0 / p.Wp;
-        int w = o0 - h * p.Wp;
-        for (int col = 0; col < kSubN; col += 16) {
-          uint32_t v[16];
-          tmem_ld16(tmem + ((quad * 32) << 16) + sub * kSubN + col, v);
+      for (int sub = 0; sub < SUBS; ++sub) {
+        for (int ch = 0; ch < kSubN / kChunk; ++ch) {
+          const int o0 = tc.pt * C::kTileN + sub * kSubN + ch * kChunk;
+          uint32_t v[32];
+          tmem_ld32(tmem + ((quad * 32) << 16) + acc * C::kTileN + sub * kSubN + ch * kChunk, v);
           tmem_ld_wait();
+          // pixel (o0 + lane) validity, shared by the warp as a bit mask
+          const int pos = o0 + int(lane);
+          const int hh = pos / p.Wp;
+          const int ww = pos - hh * p.Wp;
+          const uint32_t mask = __ballot_sync(0xffffffffu, hh < p.H && ww < p.W);
+          if (p.out_mode == kOutTmaBf16) {
+            uint8_t* buf = stg + (stg_i & 1) * kStageBytes;
+            if (leader) bulk_wait_read<1>();  // the store that last used `buf` has read it
+            named_bar_sync(kEpiBar, kEpiThreads);
+            if (live) {
+              uint8_t* half = buf + (co_local >> 6) * (kChunk * 128);
+              const uint32_t cb = (co_local & 63) * 2;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (live && h < p.H && w < p.W) {
-              float x = __uint_as_float(v[j]) + bias;
-              if (g.relu) x = fmaxf(x, 0.f);
-              if (p.out_nchw_f32) {
-                float* dst = static_cast<float*>(g.out) +
-                             ((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) * p.H + h) *
-                                 p.W + w;
-                *dst = x;
-              } else {
-                __nv_bfloat16* dst =
-                    static_cast<__nv_bfloat16*>(g.out) +
-                    (static_cast<size_t>(tc.n * p.out_Hp + h + p.out_P) * p.out_Wp + w + p.out_P) *
-                        g.out_c_stride +
-                    g.out_c_off + co;
-                *dst = __float2bfloat16_rn(x);
+              for (int j = 0; j < kChunk; ++j) {
+                const float x = (mask >> j) & 1u ? activate(v[j], bias, g.relu) : 0.f;
+                *reinterpret_cast<__nv_bfloat16*>(half + j * 128 + ((((cb >> 4) ^ (j & 7)) << 4) | (cb & 15))) =
+                    __float2bfloat16_rn(x);
               }
             }
-            if (++w == p.Wp) { w = 0; ++h; }
+            fence_proxy_async_smem();
+            named_bar_sync(kEpiBar, kEpiThreads);
+            if (leader) {
+              const int row = p.P * p.Wp + p.P + o0;
+              const int c0 = g.out_c_off + tc.mt * kTileM;
+              tma_store_3d(&maps.out[tc.g], buf, c0, row, tc.n);
+              if (cout_m > 64) tma_store_3d(&maps.out[tc.g], buf + kChunk * 128, c0 + 64, row, tc.n);
+              bulk_commit();
+            }
+            ++stg_i;
+          } else if (live && mask) {
+            int h = o0 / p.Wp;
+            int w = o0 - h * p.Wp;
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+              if ((mask >> j) & 1u) {
+                const float x = activate(v[j], bias, g.relu);
+                if (p.out_mode == kOutNchwF32) {
+                  static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
+                                                  p.H + h) * p.W + w] = x;
+                } else {
+                  static_cast<__nv_bfloat16*>(g.out)[(static_cast<size_t>(tc.n * p.Hp + h + p.P) * p.Wp + w + p.P) *
+                                                         g.out_c_stride + g.out_c_off + co] =
+                      __float2bfloat16_rn(x);
+                }
+              }
+              if (++w == p.Wp) { w = 0; ++h; }
+            }
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(acc_empty);
-      aph ^= 1;
+      mbar_arrive(&acc_empty[acc]);
+      if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
     }
+    if (leader) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -224,20 +279,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+template <int SUBS>
+constexpr size_t smem_bytes() {
+  return Cfg<SUBS>::total + 1024;
+}
+
 }  // namespace
 
-size_t conv_smem_bytes() { return SmemLayout::total + 1024; }
-
 void conv_configure() {
-  check_cuda(cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(conv_smem_bytes())),
+  check_cuda(cudaFuncSetAttribute(conv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem_bytes<1>())),
+             "conv smem attribute");
+  check_cuda(cudaFuncSetAttribute(conv_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem_bytes<2>())),
              "conv smem attribute");
 }
 
 void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
   const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
-  conv_tc_kernel<<<grid, kThreads, conv_smem_bytes(), stream>>>(maps, p);
-  check_cuda(cudaGetLastError(), "conv_tc launch");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = p.subs == 1 ? smem_bytes<1>() : smem_bytes<2>();
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (p.subs == 1)
+    check_cuda(cudaLaunchKernelEx(&cfg, conv_tc_kernel<1>, maps, p), "conv_tc launch");
+  else
+    check_cuda(cudaLaunchKernelEx(&cfg, conv_tc_kernel<2>, maps, p), "conv_tc launch");
 }
 
 }  // namespace avec

@@ -9,21 +9,37 @@
 //   out[o][co] = sum_{r,s,ci} act[base_n + o + r*Wp + s][ci] * W[co][r][s][ci]
 //
 // for o over the image's output positions laid out on the padded width (the
-// Wp-W columns per row that fall in the border are computed and discarded).
+// Wp-W columns per row that fall in the border are computed, then written as
+// ZERO, which keeps the output's border valid padding for the next layer).
 //
 // GEMM mapping (swap-AB): M = 128 output channels (weights are operand A),
-// N = 256 pixels per MMA (activations are operand B), K = 64 channels of one
-// tap per k-block. A CTA tile is 128 Cout x 512 pixels (two N=256 MMAs that
-// share every weight k-block); both accumulators fill the 512 TMEM columns.
+// N = 256 pixels per MMA (activations are operand B; N=256 keeps the SS-mode
+// smem operand traffic under the measured 128 B/clk, see tests/native/tc_probe.cu),
+// K = 64 channels of one tap per k-block.
+//
+// Two tile shapes (template SUBS):
+//  * SUBS = 2: 128 Cout x 512 pixels; both N=256 MMAs share every weight
+//    k-block (halves L2 weight traffic); accumulators fill all 512 TMEM
+//    columns. Used for large-K layers (7x7 stages) where the mainloop dwarfs
+//    the epilogue.
+//  * SUBS = 1: 128 x 256 with TWO accumulator stages in TMEM, so the epilogue
+//    of tile i overlaps the mainloop of tile i+1. Used for the small-K,
+//    high-resolution VGG layers where the epilogue is a large share.
 //
 // Activation reuse: for each (channel chunk, filter row r) the producer loads
-// ONE window of 512 + k - 1 rows; the k taps s = 0..k-1 are MMA descriptors
-// offset by s rows into that window (validated by tests/native/tc_probe.cu), so
-// a 7x7 conv reads its input 7x, not 49x, from L2.
+// ONE window of 256*SUBS + 8 rows; the k taps s = 0..k-1 are MMA descriptors
+// offset by s rows into that window (the hardware swizzles on absolute smem
+// address bits, validated by tests/native/tc_probe.cu), so a 7x7 conv reads
+// its input 7x, not 49x, from L2.
+//
+// Epilogue: TMEM -> registers (bias, ReLU, zero outside the image, bf16) ->
+// 128B-swizzled smem staging -> TMA bulk-tensor store of [32 px][64 ch] boxes
+// into the output's 3D view [N][Hp*Wp][C] (rows past the image are clipped by
+// the tensor bounds). Outputs that are not 64-channel slabs (the 38/19-channel
+// branch heads) and the fp32 NCHW network output use a direct-store path.
 //
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA
-// issuer, warps 2-5 epilogue (TMEM -> bias/ReLU -> bf16 NHWC or fp32 NCHW).
-// Persistent: grid = min(tiles, SMs); tiles strided by gridDim.x.
+// issuer, warps 2-5 epilogue. Persistent: grid = min(tiles, SMs).
 #pragma once
 
 #include <cuda.h>
@@ -35,9 +51,15 @@ namespace avec {
 
 constexpr int kConvMaxGroups = 2;
 
+enum ConvOutMode : int {
+  kOutTmaBf16 = 0,   // bf16 padded-flat NHWC via TMA store (64-channel slabs)
+  kOutDirectBf16 = 1,  // bf16 padded-flat NHWC, per-element stores
+  kOutNchwF32 = 2,   // fp32 NCHW [n][c][H][W] (network output)
+};
+
 struct ConvGroupParams {
   const float* bias;   // [m_tiles * 128], zero padded
-  void* out;           // bf16 padded-flat NHWC buffer, or fp32 NCHW output
+  void* out;           // destination base
   int out_c_off;       // channel offset inside the destination
   int out_c_stride;    // channels of the destination buffer (NHWC) / total channels (NCHW)
   int cout;            // real output channels written
@@ -50,25 +72,25 @@ struct ConvParams {
   int in_c_off;        // first input channel inside the source buffer
   int n_images;
   int H, W;            // output = input spatial size
-  int Hp, Wp, P;       // input buffer geometry
-  int out_Hp, out_Wp, out_P;  // output buffer geometry (NHWC mode)
-  int out_nchw_f32;    // 1: write fp32 NCHW [n][c][H][W] (final outputs)
+  int Hp, Wp, P;       // buffer geometry (input and output share it)
+  int out_mode;        // ConvOutMode
+  int subs;            // 1 or 2 (tile width 256 * subs pixels)
   int m_tiles;         // ceil(cout / 128)
-  int tiles_per_image; // ceil(H*Wp / 512)
+  int tiles_per_image; // ceil(H*Wp / (256*subs))
   int n_groups;
   int total_tiles;
   ConvGroupParams g[kConvMaxGroups];
 };
 
 struct ConvMaps {
-  CUtensorMap act_big[kConvMaxGroups];    // box {64 ch, 256 rows}
-  CUtensorMap act_small[kConvMaxGroups];  // box {64 ch, 8 rows}
-  CUtensorMap wgt[kConvMaxGroups];        // box {64, 128 rows}
+  CUtensorMap act_big[kConvMaxGroups];    // 2D [rows][C_in], box {64 ch, 256 rows}
+  CUtensorMap act_small[kConvMaxGroups];  // 2D, box {64 ch, 8 rows}
+  CUtensorMap wgt[kConvMaxGroups];        // 2D [cout_pad][k*k*cin_pad], box {64, 128 rows}
+  CUtensorMap out[kConvMaxGroups];        // 3D [N][Hp*Wp][C_out], box {64 ch, 32 rows, 1}
 };
 
 // host side
-size_t conv_smem_bytes();
-// per device, before the first launch (sets the dynamic smem limit)
+// per device, before the first launch (sets the dynamic smem limits)
 void conv_configure();
 void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
 

@@ -103,6 +103,21 @@ CUtensorMap make_map_2d(const void* base, uint64_t cols, uint64_t rows, uint32_t
   return m;
 }
 
+// 3D bf16 [n][rows][cols] (the padded-flat buffer seen per image), box {64, 32, 1}
+CUtensorMap make_map_3d_store(const void* base, uint64_t cols, uint64_t rows, uint64_t n) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {cols, rows, n};
+  cuuint64_t strides[2] = {cols * 2, rows * cols * 2};
+  cuuint32_t box[3] = {64, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled (store) failed: " + std::to_string(int(r)));
+  return m;
+}
+
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 // internal concat layout of a stage input: [trunk 128][L1 38][L2 19][pad]
@@ -142,6 +157,14 @@ struct SlotLease {
     ctx->slot_cv.notify_one();
   }
   Slot* slot() const { return ctx->slots[idx].get(); }
+  // order this use of the slot after its previous asynchronous forward
+  void after_pending(cudaStream_t st) const {
+    Slot* s = slot();
+    if (!s->pending) return;
+    if (st) check_cuda(cudaStreamWaitEvent(st, s->done, 0), "wait slot");
+    else check_cuda(cudaEventSynchronize(s->done), "wait slot");
+    s->pending = false;
+  }
 };
 
 bool is_pinned(const void* p) {
@@ -208,7 +231,7 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
   auto net = std::make_shared<PoseNet>();
   net->fam = std::move(fam);
   const PoseFamily& f = net->fam;
-  // layout: conv1_1 fp32 [27][64] + bias, then per tc layer bf16 W + fp32 bias
+  // per layer: bf16 W [cout_pad][k*k][cin_pad] + fp32 bias, 1 KB aligned
   std::vector<size_t> w_off(f.convs.size()), b_off(f.convs.size());
   size_t total = 0;
   auto take = [&](size_t bytes) {
@@ -220,14 +243,11 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
   for (size_t i = 0; i < f.convs.size(); ++i) {
     ConvLayerDev& L = net->layers[i];
     L.def = f.convs[i];
-    if (i == 0) {
-      w_off[i] = take(27 * 64 * 4);
-      b_off[i] = take(64 * 4);
-      continue;
-    }
-    L.cin_pad = round_up(L.def.cin, 64);
+    // the 3-channel first layer runs as a 1x1 conv over its 64-channel im2col
+    L.exec_k = i == 0 ? 1 : L.def.k;
+    L.cin_pad = i == 0 ? 64 : round_up(L.def.cin, 64);
     L.cout_pad = round_up(L.def.cout, 128);
-    w_off[i] = take(size_t(L.cout_pad) * L.def.k * L.def.k * L.cin_pad * 2);
+    w_off[i] = take(size_t(L.cout_pad) * L.exec_k * L.exec_k * L.cin_pad * 2);
     b_off[i] = take(size_t(L.cout_pad) * 4);
   }
   std::vector<uint8_t> host(total, 0);
@@ -237,16 +257,14 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
     const ConvDef& d = L.def;
     const int k = d.k;
     if (i == 0) {
-      if (d.cin != 3 || d.cout != 64 || k != 3) fail(AVEC_ERR_INVALID_MODEL, "first layer must be 3->64 3x3");
-      float* w = reinterpret_cast<float*>(host.data() + w_off[i]);
-      for (int co = 0; co < 64; ++co)
-        for (int ci = 0; ci < 3; ++ci)
-          for (int r = 0; r < 3; ++r)
-            for (int s = 0; s < 3; ++s)
-              w[(ci * 9 + r * 3 + s) * 64 + co] = bf16_value(src[((co * 3 + ci) * 3 + r) * 3 + s]);
-      src += 64 * 27;
-      std::memcpy(host.data() + b_off[i], src, 64 * 4);
-      src += 64;
+      if (d.cin != 3 || k != 3) fail(AVEC_ERR_INVALID_MODEL, "first layer must be 3x3 over 3 channels");
+      uint16_t* w = reinterpret_cast<uint16_t*>(host.data() + w_off[i]);
+      for (int co = 0; co < d.cout; ++co)
+        for (int t = 0; t < 27; ++t)  // t = ci*9 + r*3 + s, the im2col channel order
+          w[size_t(co) * 64 + t] = bf16_bits(src[size_t(co) * 27 + t]);
+      src += size_t(d.cout) * 27;
+      std::memcpy(host.data() + b_off[i], src, d.cout * 4);
+      src += d.cout;
       continue;
     }
     const bool perm = is_stage_input_layer(d, f);
@@ -269,13 +287,8 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
   check_cuda(cudaMemcpy(net->mem.p, host.data(), total, cudaMemcpyHostToDevice), "weights H2D");
   char* base = net->mem.as<char>();
   for (size_t i = 0; i < f.convs.size(); ++i) {
-    if (i == 0) {
-      net->first_w = reinterpret_cast<float*>(base + w_off[i]);
-      net->first_b = reinterpret_cast<float*>(base + b_off[i]);
-    } else {
-      net->layers[i].w = base + w_off[i];
-      net->layers[i].bias = reinterpret_cast<float*>(base + b_off[i]);
-    }
+    net->layers[i].w = base + w_off[i];
+    net->layers[i].bias = reinterpret_cast<float*>(base + b_off[i]);
   }
   return net;
 }
@@ -323,7 +336,7 @@ struct PlanBuilder {
     ConvParams& p = op.cp;
     const ConvLayerDev& L0 = net.layers[layers[0]];
     const Geometry& gi = plan.geo[in[0].level];
-    p.k = L0.def.k;
+    p.k = L0.exec_k;
     p.cin_chunks = L0.cin_pad / 64;
     p.in_c_off = in[0].c_off;
     p.n_images = plan.n;
@@ -333,20 +346,29 @@ struct PlanBuilder {
     p.Wp = gi.Wp();
     p.P = gi.P;
     const bool to_output = out[0].buf == -1;
-    const Geometry& go = plan.geo[to_output ? 3 : out[0].level];
-    p.out_Hp = go.Hp();
-    p.out_Wp = go.Wp();
-    p.out_P = go.P;
-    p.out_nchw_f32 = to_output ? 1 : 0;
+    // 64-channel slabs at 8-aligned offsets go out through TMA stores
+    bool slab = !to_output;
+    for (size_t g = 0; g < layers.size(); ++g)
+      slab = slab && net.layers[layers[g]].def.cout % 64 == 0 && out[g].c_off % 8 == 0 &&
+             out[g].level == in[g].level;
+    p.out_mode = to_output ? kOutNchwF32 : slab ? kOutTmaBf16 : kOutDirectBf16;
+    // wide tiles (weights shared by 512 pixels) for the long-K 7x7 layers;
+    // 256-pixel tiles with a double-buffered accumulator elsewhere
+    p.subs = L0.exec_k == 7 ? 2 : 1;
     p.m_tiles = L0.cout_pad / 128;
-    p.tiles_per_image = (p.H * p.Wp + 511) / 512;
+    p.tiles_per_image = (p.H * p.Wp + 256 * p.subs - 1) / (256 * p.subs);
     p.n_groups = int(layers.size());
     p.total_tiles = p.n_groups * p.n_images * p.tiles_per_image * p.m_tiles;
     for (size_t g = 0; g < layers.size(); ++g) {
       const ConvLayerDev& L = net.layers[layers[g]];
-      if (L.def.k != p.k || L.cin_pad != L0.cin_pad || L.cout_pad != L0.cout_pad ||
+      if (L.exec_k != p.k || L.cin_pad != L0.cin_pad || L.cout_pad != L0.cout_pad ||
           in[g].c_off != p.in_c_off || (out[g].buf == -1) != to_output)
         fail(AVEC_ERR_INVALID_MODEL, "grouped conv layers differ in shape");
+      if (p.out_mode == kOutTmaBf16) {
+        const int ob = out[g].buf;
+        op.maps.out[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob], uint64_t(gi.Hp()) * gi.Wp(),
+                                           plan.n);
+      }
       ConvGroupParams& gp = p.g[g];
       gp.bias = L.bias;
       gp.out = to_output ? plan.out.p : plan.bufs[out[g].buf]->p;
@@ -358,7 +380,7 @@ struct PlanBuilder {
       const uint64_t rows = uint64_t(plan.n) * gi.Hp() * gi.Wp();
       op.maps.act_big[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 256);
       op.maps.act_small[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 8);
-      op.maps.wgt[g] = make_map_2d(L.w, uint64_t(L.def.k) * L.def.k * L.cin_pad, L.cout_pad, 128);
+      op.maps.wgt[g] = make_map_2d(L.w, uint64_t(L.exec_k) * L.exec_k * L.cin_pad, L.cout_pad, 128);
       op.layers[g] = layers[g];
       record_io(layers[g], in[g], out[g]);
     }
@@ -385,18 +407,17 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
   plan.layer_out.assign(nl, TensorView{});
   int li = 0;
   // level 0
-  const int a0 = b.buffer(0, 64), b0 = b.buffer(0, 64);
+  const int a0 = b.buffer(0, 64), b0 = b.buffer(0, 64), i2c = b.buffer(0, 64);
   {
-    PlanOp op;
+    PlanOp op;  // frames -> normalised bf16 im2col of the 3x3x3 taps
     op.kind = PlanOp::kFirst;
-    op.dst = a0;
-    op.layers[0] = 0;
+    op.dst = i2c;
     plan.ops.push_back(op);
+    b.conv({li++}, {b.view(i2c, 0, 64)}, {b.view(a0, 0, 64)});  // conv1_1 as 1x1 over the im2col
     TensorView in;
     in.buf = -2;
     in.c = 3;
-    b.record_io(0, in, b.view(a0, 0, 64));
-    ++li;
+    plan.layer_in[0] = in;  // parity hook shows the layer its real 3-channel input
   }
   b.conv({li++}, {b.view(a0, 0, 64)}, {b.view(b0, 0, 64)});  // conv1_2
   const int p1 = b.buffer(1, 64), a1 = b.buffer(1, 128), b1 = b.buffer(1, 128);
@@ -458,8 +479,8 @@ void run_ops(avec_ctx* ctx, const Plan& plan, const PoseNet& net, size_t first, 
     const PlanOp& op = plan.ops[i];
     switch (op.kind) {
       case PlanOp::kFirst:
-        launch_conv_first(plan.in.as<float>(), plan.n, plan.H, plan.W, net.first_w, net.first_b,
-                          plan.bufs[op.dst]->p, plan.geo[0].P, st);
+        launch_im2col_first(plan.in.as<float>(), plan.n, plan.H, plan.W, plan.bufs[op.dst]->p,
+                            plan.geo[0].P, st);
         break;
       case PlanOp::kConv:
         launch_conv_tc(op.maps, op.cp, ctx->sms, st);
@@ -547,6 +568,7 @@ void ctx_init(avec_ctx* ctx, int device, int slots) {
     check_cuda(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
     check_cuda(cudaEventCreate(&s->ev0), "event");
     check_cuda(cudaEventCreate(&s->ev1), "event");
+    check_cuda(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming), "event");
     for (int b = 0; b < 2; ++b) {
       check_cuda(cudaEventCreateWithFlags(&s->stage_ev[b], cudaEventDisableTiming), "event");
       s->stage[b].ensure(kStageChunk);
@@ -564,6 +586,7 @@ void ctx_shutdown(avec_ctx* ctx) {
     if (s->stream) cudaStreamDestroy(s->stream);
     cudaEventDestroy(s->ev0);
     cudaEventDestroy(s->ev1);
+    cudaEventDestroy(s->done);
     cudaEventDestroy(s->stage_ev[0]);
     cudaEventDestroy(s->stage_ev[1]);
   }
@@ -650,6 +673,7 @@ double forward_host(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint
   check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
   SlotLease lease(ctx);
   Slot* s = lease.slot();
+  lease.after_pending(s->stream);
   if (m.kind == AVEC_MODEL_POSENET) {
     int n_img = 0;
     posenet_shape(m, n, c, h, w, n_img);
@@ -681,6 +705,7 @@ void forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint
   SlotLease lease(ctx);
   Slot* s = lease.slot();
   cudaStream_t st = stream ? stream : s->stream;
+  lease.after_pending(st);
   if (m.kind == AVEC_MODEL_POSENET) {
     int n_img = 0;
     posenet_shape(m, n, c, h, w, n_img);
@@ -692,8 +717,78 @@ void forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint
   } else {
     launch_segment_means(d_in, d_out, E, K, st);
   }
-  // plan buffers belong to the slot: drain before the lease is released
-  check_cuda(cudaStreamSynchronize(st), "forward sync");
+  if (stream) {
+    // asynchronous: the slot's plan buffers stay busy until `done` fires
+    check_cuda(cudaEventRecord(s->done, st), "done event");
+    s->pending = true;
+  } else {
+    check_cuda(cudaStreamSynchronize(st), "forward sync");
+  }
+}
+
+std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c,
+                                       uint32_t h, uint32_t w, const float* d_in, int reps) {
+  const Model m = model_lookup(ctx, handle);
+  if (m.kind != AVEC_MODEL_POSENET) fail(AVEC_ERR_INVALID_ARGUMENT, "not a pose net");
+  int n_img = 0;
+  posenet_shape(m, n, c, h, w, n_img);
+  check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+  SlotLease lease(ctx);
+  Slot* s = lease.slot();
+  lease.after_pending(s->stream);
+  Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
+  const uint64_t E = uint64_t(n) * c * h * w;
+  check_cuda(cudaMemcpyAsync(plan->in.p, d_in, E * 4, cudaMemcpyDeviceToDevice, s->stream), "D2D");
+  check_cuda(cudaGraphLaunch(plan->graph, s->stream), "warm graph");
+  const size_t nops = plan->ops.size();
+  std::vector<cudaEvent_t> ev(nops + 1);
+  for (auto& e : ev) check_cuda(cudaEventCreate(&e), "event");
+  std::vector<OpProfile> prof(nops);
+  for (int r = 0; r < reps; ++r) {
+    for (size_t i = 0; i < nops; ++i) {
+      check_cuda(cudaEventRecord(ev[i], s->stream), "event");
+      run_ops(ctx, *plan, *m.net, i, i + 1, s->stream);
+    }
+    check_cuda(cudaEventRecord(ev[nops], s->stream), "event");
+    check_cuda(cudaEventSynchronize(ev[nops]), "event sync");
+    for (size_t i = 0; i < nops; ++i) {
+      float ms = 0;
+      check_cuda(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]), "elapsed");
+      prof[i].ms += ms / float(reps);
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  const PoseFamily& f = m.net->fam;
+  for (size_t i = 0; i < nops; ++i) {
+    const PlanOp& op = plan->ops[i];
+    OpProfile& p = prof[i];
+    p.layers[0] = op.layers[0];
+    p.layers[1] = op.layers[1];
+    p.flops = 0;
+    p.bytes = 0;
+    if (op.kind == PlanOp::kPool) {
+      const Geometry& g = plan->geo[op.level];
+      p.kind = 2;
+      p.bytes = double(n_img) * g.H * g.W * op.C * 2 * 1.25;  // read 4, write 1 bf16 per window
+      continue;
+    }
+    if (op.kind == PlanOp::kFirst) {  // im2col: 3 fp32 in + 64 bf16 out per pixel
+      p.kind = 0;
+      p.bytes = double(n_img) * h * w * (12.0 + 128.0);
+      continue;
+    }
+    p.kind = 1;
+    for (int g = 0; g < 2; ++g) {
+      if (op.layers[g] < 0) continue;
+      const ConvDef& d = f.convs[op.layers[g]];
+      const double px = double(n_img) * (h >> d.level) * (w >> d.level);
+      p.flops += 2.0 * px * d.cin * d.cout * d.k * d.k;
+      const double in_b = op.kind == PlanOp::kFirst ? 4.0 : 2.0;  // fp32 frame or bf16 act
+      const bool final_out = plan->layer_out[op.layers[g]].buf == -1;
+      p.bytes += px * (d.cin * in_b + d.cout * (final_out ? 4.0 : 2.0));
+    }
+  }
+  return prof;
 }
 
 void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,

@@ -30,10 +30,10 @@ inline void check_cuda(cudaError_t e, const char* what) {
 void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K,
                           cudaStream_t stream);
 
-// input fp32 NCHW frames -> (x - 0.5) -> bf16 -> conv 3x3 (3 -> 64) + bias + ReLU
-// -> bf16 padded-flat NHWC [n][H+2P][W+2P][64]
-void launch_conv_first(const float* d_in, int n, int H, int W, const float* w_fp32_27x64,
-                       const float* bias64, void* d_out, int P, cudaStream_t stream);
+// input fp32 NCHW frames -> (x - 0.5) -> bf16 -> im2col of the 3x3x3 first-layer
+// taps into 64-channel rows of a padded-flat NHWC buffer [n][H+2P][W+2P][64]
+void launch_im2col_first(const float* d_in, int n, int H, int W, void* d_out, int P,
+                         cudaStream_t stream);
 
 // 2x2/2 max pool, padded-flat NHWC bf16 -> padded-flat NHWC bf16
 void launch_maxpool2(const void* d_in, int n, int H, int W, int P_in, int C, void* d_out,

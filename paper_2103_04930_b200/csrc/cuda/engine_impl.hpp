@@ -46,6 +46,7 @@ struct PinnedMem {
 // one conv layer resident on the device (bf16 packed for the TMA/UMMA path)
 struct ConvLayerDev {
   ConvDef def;
+  int exec_k = 0;  // filter size as executed (the first layer runs 1x1 over its im2col)
   int cin_pad = 0, cout_pad = 0;
   void* w = nullptr;      // bf16 [cout_pad][k*k][cin_pad]
   float* bias = nullptr;  // [cout_pad]
@@ -54,9 +55,7 @@ struct ConvLayerDev {
 struct PoseNet {
   PoseFamily fam;
   std::vector<ConvLayerDev> layers;
-  DevMem mem;                  // all weights of this device
-  float* first_w = nullptr;    // conv1_1 as fp32 [27][64] (bf16-representable values)
-  float* first_b = nullptr;
+  DevMem mem;  // all weights of this device
 };
 
 struct Geometry {
@@ -98,6 +97,8 @@ struct Slot {
   int index = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t done = nullptr;  // last enqueued async work on a caller stream
+  bool pending = false;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   PinnedMem stage[2];
   DevMem d_in, d_out;  // segment-mean path
@@ -144,6 +145,15 @@ double forward_host(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint
                     const float* in, uint64_t in_elems, float* out, uint64_t out_elems);
 void forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                     const float* d_in, float* d_out, cudaStream_t stream);
+struct OpProfile {
+  int kind;        // 0 first conv (CUDA cores), 1 tcgen05 conv, 2 max-pool
+  double flops;    // algorithmic 2*MACs of the launch
+  double bytes;    // algorithmic bytes (inputs read once + outputs written once)
+  float ms;        // CUDA-event duration on the launching stream
+  int layers[2];
+};
+std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c,
+                                       uint32_t h, uint32_t w, const float* d_in, int reps);
 void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                       uint32_t w, const float* in, int layer, float* layer_in,
                       uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);

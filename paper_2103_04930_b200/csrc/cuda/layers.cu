@@ -9,27 +9,25 @@ namespace avec {
 
 namespace {
 
-// conv1_1: 3 input channels make a K=27 GEMM — too thin for the tensor cores,
-// so it runs on the FP32 pipes, fused with the wire-format conversion:
-// fp32 NCHW frame -> (x - 0.5) -> bf16 (the net's input precision) -> 3x3 conv
-// -> +bias -> ReLU -> bf16 NHWC (64 ch, one 128-byte row per pixel).
-__global__ void __launch_bounds__(128) conv_first_kernel(const float* __restrict__ in, int n,
-                                                         int H, int W,
-                                                         const float* __restrict__ w27x64,
-                                                         const float* __restrict__ bias,
-                                                         __nv_bfloat16* __restrict__ out, int P) {
-  __shared__ float sw[27 * 64];
-  __shared__ float sb[64];
-  for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) sw[i] = w27x64[i];
-  if (threadIdx.x < 64) sb[threadIdx.x] = bias[threadIdx.x];
-  __syncthreads();
+// conv1_1 has 3 input channels (K = 27), too thin to feed the tensor cores
+// directly. This streaming kernel fuses the wire-format conversion with an
+// im2col: fp32 NCHW frame -> (x - 0.5) -> bf16 (the net's input precision) ->
+// one 64-channel row per pixel holding the 27 taps (ci*9 + r*3 + s) and 37
+// zeros, in the level-0 padded-flat layout. conv1_1 then runs as a 1x1
+// tcgen05 conv over those 64 channels (weights packed to match).
+// HBM-bound: 12 B read + 128 B written per pixel.
+__global__ void __launch_bounds__(128) im2col_first_kernel(const float* __restrict__ in, int n,
+                                                           int H, int W,
+                                                           __nv_bfloat16* __restrict__ out, int P) {
   const long long pix = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long total = static_cast<long long>(n) * H * W;
   if (pix >= total) return;
   const int x = static_cast<int>(pix % W);
   const int y = static_cast<int>((pix / W) % H);
   const int b = static_cast<int>(pix / (static_cast<long long>(W) * H));
-  float xin[27];
+  uint32_t packed[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) packed[i] = 0;
 #pragma unroll
   for (int ci = 0; ci < 3; ++ci) {
     const float* plane = in + (static_cast<size_t>(b) * 3 + ci) * H * W;
@@ -39,34 +37,18 @@ __global__ void __launch_bounds__(128) conv_first_kernel(const float* __restrict
       for (int s = 0; s < 3; ++s) {
         const int yy = y + r - 1, xx = x + s - 1;
         float v = 0.f;
-        if (yy >= 0 && yy < H && xx >= 0 && xx < W)
-          v = __bfloat162float(__float2bfloat16_rn(__ldg(plane + yy * W + xx) - 0.5f));
-        xin[ci * 9 + r * 3 + s] = v;
+        if (yy >= 0 && yy < H && xx >= 0 && xx < W) v = __ldg(plane + yy * W + xx) - 0.5f;
+        const int t = ci * 9 + r * 3 + s;
+        const uint32_t bits = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+        packed[t >> 1] |= (t & 1) ? (bits << 16) : bits;
       }
     }
   }
-  __nv_bfloat16* dst =
-      out + ((static_cast<size_t>(b) * (H + 2 * P) + y + P) * (W + 2 * P) + x + P) * 64;
+  uint4* dst = reinterpret_cast<uint4*>(
+      out + ((static_cast<size_t>(b) * (H + 2 * P) + y + P) * (W + 2 * P) + x + P) * 64);
 #pragma unroll
-  for (int c8 = 0; c8 < 8; ++c8) {
-    float acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-#pragma unroll
-    for (int t = 0; t < 27; ++t) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = fmaf(xin[t], sw[t * 64 + c8 * 8 + j], acc[j]);
-    }
-    uint32_t packed[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float a = fmaxf(acc[2 * j] + sb[c8 * 8 + 2 * j], 0.f);
-      float c = fmaxf(acc[2 * j + 1] + sb[c8 * 8 + 2 * j + 1], 0.f);
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(a, c);
-      packed[j] = *reinterpret_cast<uint32_t*>(&h2);
-    }
-    reinterpret_cast<uint4*>(dst)[c8] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-  }
+  for (int q = 0; q < 8; ++q)
+    dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
 }
 
 __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n, int H, int W,
@@ -121,12 +103,12 @@ unsigned blocks_for(long long total, int threads) {
 
 }  // namespace
 
-void launch_conv_first(const float* d_in, int n, int H, int W, const float* w_fp32_27x64,
-                       const float* bias64, void* d_out, int P, cudaStream_t stream) {
+void launch_im2col_first(const float* d_in, int n, int H, int W, void* d_out, int P,
+                         cudaStream_t stream) {
   const long long total = static_cast<long long>(n) * H * W;
-  conv_first_kernel<<<blocks_for(total, 128), 128, 0, stream>>>(
-      d_in, n, H, W, w_fp32_27x64, bias64, static_cast<__nv_bfloat16*>(d_out), P);
-  check_cuda(cudaGetLastError(), "conv_first launch");
+  im2col_first_kernel<<<blocks_for(total, 128), 128, 0, stream>>>(
+      d_in, n, H, W, static_cast<__nv_bfloat16*>(d_out), P);
+  check_cuda(cudaGetLastError(), "im2col_first launch");
 }
 
 void launch_maxpool2(const void* d_in, int n, int H, int W, int P_in, int C, void* d_out,
