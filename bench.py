@@ -171,15 +171,17 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     n_rot = 4
     host_frames = [O.batched_frame(W, H, BATCH, seed=7, first=(rank * n_rot + i) * BATCH) for i in range(n_rot)]
     d_in = [torch.from_numpy(f).to(f"cuda:{dev}") for f in host_frames]
-    d_out = torch.empty(K, dtype=torch.float32, device=f"cuda:{dev}")
-    stream = torch.cuda.Stream(device=dev)
+    d_out = [torch.empty(K, dtype=torch.float32, device=f"cuda:{dev}") for _ in range(2)]
+    # two cycles in flight, like the server's two execution slots
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
 
     if world > 1:
         dist.barrier()
 
     # ---------------- device-resident throughput (value) ----------------
     def step(i):
-        be.forward_device(h, dims, d_in[i % n_rot].data_ptr(), d_out.data_ptr(), stream.cuda_stream)
+        be.forward_device(h, dims, d_in[i % n_rot].data_ptr(), d_out[i % 2].data_ptr(),
+                          streams[i % 2].cuda_stream)
 
     for i in range(args.warmup):
         step(i)
@@ -188,11 +190,15 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event()
     with ClockSampler(dev) as clocks:
-        ev0.record(stream)
+        ev0.record(streams[0])
+        streams[1].wait_event(ev0)
         for i in range(args.steps):
             step(i)
-        ev1.record(stream)
+        ev_b.record(streams[1])
+        streams[0].wait_event(ev_b)
+        ev1.record(streams[0])
         torch.cuda.synchronize()
     dev_ms = ev0.elapsed_time(ev1)
     if world > 1:
@@ -222,21 +228,27 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
             s += float(pin_out[j].array[0])  # host read of the step's result
         checksum[j] = s
 
-    if world > 1:
-        dist.barrier()
-    n0 = (args.steps + 1) // 2
-    t0 = time.perf_counter()
-    ths = [threading.Thread(target=worker, args=(0, n0)), threading.Thread(target=worker, args=(1, args.steps - n0))]
-    for t in ths:
-        t.start()
-    for t in ths:
-        t.join()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = frames_total / e2e_s
+    def e2e_run(threads: int) -> float:
+        if world > 1:
+            dist.barrier()
+        counts = [args.steps // threads + (1 if i < args.steps % threads else 0) for i in range(threads)]
+        t0 = time.perf_counter()
+        ths = [threading.Thread(target=worker, args=(j, counts[j])) for j in range(threads)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([s], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            s = float(t.item())
+        return frames_total / s
+
+    # one client thread (synchronous cycles) and two (the server's two slots in flight)
+    e2e_by_threads = {1: e2e_run(1), 2: e2e_run(2)}
+    e2e_threads = max(e2e_by_threads, key=e2e_by_threads.get)
+    e2e = e2e_by_threads[e2e_threads]
 
     # ---------------- roofline of the dominant kernel ----------------
     prof = be.profile(h, dims, d_in[0].data_ptr(), reps=3)
@@ -292,7 +304,10 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
                        "global_batch": BATCH * world, "frame": f"{W}x{H}", "parallelism": f"frame groups x{world}",
                        "l2": "4 rotating input buffers; per-step activation working set ~1.4 GB >> 126 MB L2"},
             "e2e": {"value": round(e2e, 2), "unit": "frames/s", "h2d_bytes_per_step": E * 4,
-                    "d2h_bytes_per_step": K * 4, "api": "avec_forward (pinned host buffers, 2 slots)"},
+                    "d2h_bytes_per_step": K * 4,
+                    "api": f"avec_forward (pinned host buffers), {e2e_threads} host thread(s) over 2 slots",
+                    "by_threads": {str(k): round(v, 2) for k, v in e2e_by_threads.items()}},
+            "pdl": os.environ.get("AVEC_PDL", "0") == "1",
             "roofline": roofline, "cpu_baseline": cpu,
             "gpu_launches": args.steps * len(prof),
             "clocks": clocks.summary(),
@@ -306,8 +321,8 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

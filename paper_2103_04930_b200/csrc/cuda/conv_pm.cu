@@ -1,0 +1,340 @@
+// Pixel-major tcgen05 implicit-GEMM convolution (sm_100a) for the VGG front
+// end and the other short-K layers.
+//
+// Same padded-flat activation layout, window-reuse trick and warp roles as the
+// swap-AB kernel (conv_tc.cu), with the GEMM oriented the other way:
+//   M = 128 output pixels (activation window = operand A),
+//   N = 64/128/256 output channels (weights = operand B), K = 64 per k-block.
+// The accumulator row of a pixel sits in one TMEM lane, so each epilogue
+// thread holds 32 consecutive channels of ITS pixel per tcgen05.ld and writes
+// them as 16-byte vectors straight into the pixel's NHWC row: no transpose, no
+// shared-memory staging, no barriers. That is what the high-resolution layers
+// need — their K is short (conv1_1: 64, conv1_2: 576), so the epilogue, not
+// the MMA, bounds them.
+//
+// Tile = 128 * SUBS_M pixels x N channels; TMEM holds 2 accumulator stages
+// (2 * SUBS_M * N <= 512 columns) so the epilogue of tile i overlaps the
+// mainloop of tile i+1. Positions outside the image (padded-width columns,
+// rows past H) are written as zeros, keeping the output's border valid
+// padding; rows past the image's padded extent are not written.
+#include <cuda_bf16.h>
+
+#include "conv_tc.cuh"
+#include "engine.hpp"
+#include "ptx.cuh"
+
+namespace avec {
+
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 192;
+constexpr uint32_t kTmemCols = 512;
+
+template <int N, int SUBS_M>
+struct PmCfg {
+  static constexpr int kTileN = 128 * SUBS_M;  // pixels per tile
+  static constexpr int kWinRows = kTileN + 8;
+  static constexpr int kWinBytes = kWinRows * 128;
+  static constexpr int kWinStages = 2;
+  static constexpr int kWgtBytes = N * 128;  // N rows x 64 bf16
+  static constexpr int kAccCols = SUBS_M * N;
+  static constexpr int kAccStages = 2;
+  static_assert(kAccStages * kAccCols <= 512, "TMEM budget");
+  static constexpr int win = 0;
+  static constexpr int wgt = win + kWinStages * kWinBytes;
+  static constexpr int kWgtStages = (232448 - 1024 - 2048 - wgt) / kWgtBytes > 16
+                                        ? 16
+                                        : (232448 - 1024 - 2048 - wgt) / kWgtBytes;
+  static constexpr int bias = wgt + kWgtStages * kWgtBytes;  // N floats per acc stage
+  static constexpr int bars = bias + kAccStages * N * 4;
+  static constexpr int total = bars + 256;
+  static_assert(kWinBytes % 1024 == 0 && wgt % 1024 == 0, "SW128 alignment");
+  static_assert(total + 1024 <= 232448, "smem budget");
+};
+
+struct PmTile {
+  int g, n, pt, nt;
+};
+
+__device__ __forceinline__ PmTile pm_decode(const ConvParams& p, int t) {
+  PmTile c;
+  const int per_group = p.n_images * p.tiles_per_image * p.m_tiles;
+  c.g = t / per_group;
+  int rem = t - c.g * per_group;
+  c.nt = rem % p.m_tiles;
+  rem /= p.m_tiles;
+  c.pt = rem % p.tiles_per_image;
+  c.n = rem / p.tiles_per_image;
+  return c;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int N, int SUBS_M>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_pm_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p) {
+  using C = PmCfg<N, SUBS_M>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* win = smem + C::win;
+  uint8_t* wgt = smem + C::wgt;
+  float* sbias = reinterpret_cast<float*>(smem + C::bias);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::bars);
+  uint64_t* win_full = bars;
+  uint64_t* win_empty = win_full + C::kWinStages;
+  uint64_t* w_full = win_empty + C::kWinStages;
+  uint64_t* w_empty = w_full + C::kWgtStages;
+  uint64_t* acc_full = w_empty + C::kWgtStages;
+  uint64_t* acc_empty = acc_full + C::kAccStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::kAccStages);
+
+  const uint32_t warp = warp_id();
+  if (warp == 0 && elect_one()) {
+    for (int g = 0; g < p.n_groups; ++g) {
+      tma_prefetch(C::kTileN == 256 ? &maps.act_big[g] : &maps.act_mid[g]);
+      tma_prefetch(&maps.act_small[g]);
+      tma_prefetch(&maps.wgt[g]);
+    }
+    for (int i = 0; i < C::kWinStages; ++i) {
+      mbar_init(&win_full[i], 1);
+      mbar_init(&win_empty[i], 1);
+    }
+    for (int i = 0; i < C::kWgtStages; ++i) {
+      mbar_init(&w_full[i], 1);
+      mbar_init(&w_empty[i], 1);
+    }
+    for (int i = 0; i < C::kAccStages; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see conv_tc.cu
+
+  const int k = p.k;
+  const int pad = k / 2;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      const uint64_t keep = policy_evict_last();
+      int ws = 0, wst = 0;
+      uint32_t wph = 0, wtph = 0;
+      const uint32_t win_tx = (C::kTileN + (k > 1 ? 8 : 0)) * 128;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        const PmTile tc = pm_decode(p, t);
+        const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + tc.pt * C::kTileN;
+        for (int c = 0; c < p.cin_chunks; ++c) {
+          const int ch = p.in_c_off + c * 64;
+          for (int r = 0; r < k; ++r) {
+            mbar_wait(&win_empty[ws], wph ^ 1);
+            mbar_arrive_expect_tx(&win_full[ws], win_tx);
+            uint8_t* wbuf = win + ws * C::kWinBytes;
+            const int wr = row0 + r * p.Wp;
+            // window rows: kTileN (<= 256, one box when SUBS_M == 2) + 8-row halo
+            if (C::kTileN == 256)
+              tma_load_2d(wbuf, &maps.act_big[tc.g], &win_full[ws], ch, wr);
+            else
+              tma_load_2d(wbuf, &maps.act_mid[tc.g], &win_full[ws], ch, wr);
+            if (k > 1)
+              tma_load_2d(wbuf + C::kTileN * 128, &maps.act_small[tc.g], &win_full[ws], ch,
+                          wr + C::kTileN);
+            if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
+            for (int s = 0; s < k; ++s) {
+              mbar_wait(&w_empty[wst], wtph ^ 1);
+              mbar_arrive_expect_tx(&w_full[wst], C::kWgtBytes);
+              tma_load_2d_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], &w_full[wst],
+                               ((r * k + s) * p.cin_chunks + c) * 64, tc.nt * N, keep);
+              if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc = idesc_bf16_f32(128, N);
+      int ws = 0, wst = 0, acc = 0;
+      uint32_t wph = 0, wtph = 0, aph = 0;
+      const uint32_t win_base = smem_u32(win), wgt_base = smem_u32(wgt);
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        mbar_wait(&acc_empty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + acc * C::kAccCols;
+        bool first = true;
+        for (int c = 0; c < p.cin_chunks; ++c) {
+          for (int r = 0; r < k; ++r) {
+            mbar_wait(&win_full[ws], wph);
+            tc_fence_after();
+            const uint32_t wb = win_base + ws * C::kWinBytes;
+            for (int s = 0; s < k; ++s) {
+              mbar_wait(&w_full[wst], wtph);
+              tc_fence_after();
+              const uint32_t bb = wgt_base + wst * C::kWgtBytes;
+#pragma unroll
+              for (int sub = 0; sub < SUBS_M; ++sub) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint64_t ad = desc_sw128(wb + (sub * 128 + s) * 128 + kk * 32);
+                  const uint64_t bd = desc_sw128(bb + kk * 32);
+                  mma_bf16_ss(d0 + sub * N, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+                }
+              }
+              first = false;
+              mma_commit(&w_empty[wst]);
+              if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
+            }
+            mma_commit(&win_empty[ws]);
+            if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
+          }
+        }
+        mma_commit(&acc_full[acc]);
+        if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
+      }
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t quad = warp & 3;
+    const int ep = int(threadIdx.x) - 64;  // 0..127
+    int acc = 0;
+    uint32_t aph = 0;
+    const int img_rows = p.Hp * p.Wp;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      const PmTile tc = pm_decode(p, t);
+      const ConvGroupParams& g = p.g[tc.g];
+      float* bs = sbias + acc * N;
+      // this tile's bias slice (the acc stage's previous tile finished reading it)
+      for (int i = ep; i < N; i += 128) {
+        const int co = tc.nt * N + i;
+        bs[i] = co < g.cout ? g.bias[co] : 0.f;
+      }
+      named_bar_sync(1, 128);
+      mbar_wait(&acc_full[acc], aph);
+      tc_fence_after();
+      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.out);
+      for (int sub = 0; sub < SUBS_M; ++sub) {
+        const int o = tc.pt * C::kTileN + sub * 128 + int(quad) * 32 + int(lane_id());
+        const int hh = o / p.Wp;
+        const int ww = o - hh * p.Wp;
+        const bool valid = hh < p.H && ww < p.W;
+        const int row_in_img = p.P * p.Wp + p.P + o;  // output row of this pixel
+        const bool store = row_in_img < img_rows;
+        uint4* dst = reinterpret_cast<uint4*>(
+            out + (static_cast<size_t>(tc.n) * img_rows + row_in_img) * g.out_c_stride + g.out_c_off +
+            tc.nt * N);
+        const int c_left = g.cout - tc.nt * N;  // live channels of this tile
+#pragma unroll
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem + ((quad * 32) << 16) + acc * C::kAccCols + sub * N + c0, v);
+          tmem_ld_wait();
+          if (p.out_mode != kOutTmaBf16) {
+            // thin heads (38/19 channels into the stage concat) and the fp32
+            // NCHW network output: per-channel stores of valid pixels only;
+            // lanes are consecutive pixels, so NCHW stores coalesce along W
+            if (valid && c0 < c_left) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (c0 + j < c_left) {
+                  float a = __uint_as_float(v[j]) + bs[c0 + j];
+                  if (g.relu) a = fmaxf(a, 0.f);
+                  const int co = tc.nt * N + c0 + j;
+                  if (p.out_mode == kOutNchwF32)
+                    static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
+                                                    p.H + hh) * p.W + ww] = a;
+                  else
+                    out[(static_cast<size_t>(tc.n) * img_rows + row_in_img) * g.out_c_stride + g.out_c_off + co] =
+                        __float2bfloat16_rn(a);
+                }
+              }
+            }
+            continue;
+          }
+          if (store && c0 < c_left) {
+            uint32_t w[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float a = __uint_as_float(v[2 * j]) + bs[c0 + 2 * j];
+              float b = __uint_as_float(v[2 * j + 1]) + bs[c0 + 2 * j + 1];
+              if (g.relu) {
+                a = fmaxf(a, 0.f);
+                b = fmaxf(b, 0.f);
+              }
+              w[j] = valid ? pack_bf16(a, b) : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              dst[c0 / 8 + q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[acc]);
+      if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+template <int N, int SUBS_M>
+void launch_pm(const ConvMaps& maps, const ConvParams& p, int grid, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = PmCfg<N, SUBS_M>::total + 1024;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  check_cuda(cudaLaunchKernelEx(&cfg, conv_pm_kernel<N, SUBS_M>, maps, p), "conv_pm launch");
+}
+
+template <int N, int SUBS_M>
+void configure_pm() {
+  check_cuda(cudaFuncSetAttribute(conv_pm_kernel<N, SUBS_M>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(PmCfg<N, SUBS_M>::total + 1024)),
+             "conv_pm smem attribute");
+}
+
+}  // namespace
+
+int conv_pm_subs(int n_tile) { return n_tile == 256 ? 1 : 2; }
+
+void conv_pm_configure() {
+  configure_pm<64, 2>();
+  configure_pm<128, 2>();
+  configure_pm<256, 1>();
+}
+
+void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
+  const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
+  switch (p.pm_n) {
+    case 64: launch_pm<64, 2>(maps, p, grid, stream); break;
+    case 128: launch_pm<128, 2>(maps, p, grid, stream); break;
+    case 256: launch_pm<256, 1>(maps, p, grid, stream); break;
+    default: fail(AVEC_ERR_UNSUPPORTED, "pixel-major conv supports N tiles of 64/128/256");
+  }
+}
+
+}  // namespace avec

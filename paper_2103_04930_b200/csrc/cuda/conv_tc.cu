@@ -1,6 +1,8 @@
 // tcgen05 implicit-GEMM convolution — see conv_tc.cuh for the design.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "conv_tc.cuh"
 #include "engine.hpp"
 #include "ptx.cuh"
@@ -108,9 +110,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   // Programmatic dependent launch: everything above overlapped the previous
   // layer's tail; from here on we read its output and overwrite buffers it
-  // may still read, so wait for it to complete, then let the next layer launch.
+  // may still read, so wait for it to complete. The next layer is released
+  // only once this CTA has issued its last MMA (see below), so its CTAs do
+  // not park on SMs another stream could use.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int k = p.k;
   const int pad = k / 2;
@@ -192,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
       }
     }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else {
     // ------------------------------------------------------------ epilogue
     const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may touch
@@ -286,6 +290,16 @@ constexpr size_t smem_bytes() {
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    // Off by default: measured +1% on one stream but -22% with two slots in
+    // flight (dependents park on SMs the other stream needs). AVEC_PDL=1 enables.
+    const char* e = std::getenv("AVEC_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 void conv_configure() {
   check_cuda(cudaFuncSetAttribute(conv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem_bytes<1>())),
@@ -306,7 +320,7 @@ void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cud
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   if (p.subs == 1)
     check_cuda(cudaLaunchKernelEx(&cfg, conv_tc_kernel<1>, maps, p), "conv_tc launch");
   else

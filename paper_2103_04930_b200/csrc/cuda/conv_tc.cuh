@@ -74,9 +74,11 @@ struct ConvParams {
   int H, W;            // output = input spatial size
   int Hp, Wp, P;       // buffer geometry (input and output share it)
   int out_mode;        // ConvOutMode
-  int subs;            // 1 or 2 (tile width 256 * subs pixels)
-  int m_tiles;         // ceil(cout / 128)
-  int tiles_per_image; // ceil(H*Wp / (256*subs))
+  int subs;            // swap-AB: 1 or 2 (tile width 256 * subs pixels)
+  int pixel_major;     // 1: conv_pm.cu orientation (M = pixels, N = pm_n channels)
+  int pm_n;            // pixel-major channel tile: 64, 128 or 256
+  int m_tiles;         // channel tiles: ceil(cout / 128), or ceil(cout / pm_n)
+  int tiles_per_image; // ceil(H*Wp / pixels per tile)
   int n_groups;
   int total_tiles;
   ConvGroupParams g[kConvMaxGroups];
@@ -85,7 +87,8 @@ struct ConvParams {
 struct ConvMaps {
   CUtensorMap act_big[kConvMaxGroups];    // 2D [rows][C_in], box {64 ch, 256 rows}
   CUtensorMap act_small[kConvMaxGroups];  // 2D, box {64 ch, 8 rows}
-  CUtensorMap wgt[kConvMaxGroups];        // 2D [cout_pad][k*k*cin_pad], box {64, 128 rows}
+  CUtensorMap act_mid[kConvMaxGroups];    // 2D, box {64 ch, 128 rows}
+  CUtensorMap wgt[kConvMaxGroups];        // 2D [cout_pad][k*k*cin_pad], box {64, 128 (or pm_n) rows}
   CUtensorMap out[kConvMaxGroups];        // 3D [N][Hp*Wp][C_out], box {64 ch, 32 rows, 1}
 };
 
@@ -93,5 +96,9 @@ struct ConvMaps {
 // per device, before the first launch (sets the dynamic smem limits)
 void conv_configure();
 void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
+// pixel-major variant (conv_pm.cu)
+void conv_pm_configure();
+int conv_pm_subs(int n_tile);  // 128-pixel M sub-tiles per tile for a channel tile
+void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
 
 }  // namespace avec

@@ -142,12 +142,18 @@ struct SlotLease {
         if (!ctx->slot_busy[i]) return true;
       return false;
     });
-    for (size_t i = 0; i < ctx->slot_busy.size(); ++i)
+    // round-robin over free slots: back-to-back asynchronous calls on
+    // alternating streams land on alternating slots and overlap
+    const size_t n = ctx->slot_busy.size();
+    for (size_t k = 0; k < n; ++k) {
+      const size_t i = (ctx->next_slot + k) % n;
       if (!ctx->slot_busy[i]) {
         idx = int(i);
         ctx->slot_busy[i] = true;
+        ctx->next_slot = (i + 1) % n;
         break;
       }
+    }
   }
   ~SlotLease() {
     {
@@ -352,11 +358,22 @@ struct PlanBuilder {
       slab = slab && net.layers[layers[g]].def.cout % 64 == 0 && out[g].c_off % 8 == 0 &&
              out[g].level == in[g].level;
     p.out_mode = to_output ? kOutNchwF32 : slab ? kOutTmaBf16 : kOutDirectBf16;
-    // wide tiles (weights shared by 512 pixels) for the long-K 7x7 layers;
-    // 256-pixel tiles with a double-buffered accumulator elsewhere
-    p.subs = L0.exec_k == 7 ? 2 : 1;
-    p.m_tiles = L0.cout_pad / 128;
-    p.tiles_per_image = (p.H * p.Wp + 256 * p.subs - 1) / (256 * p.subs);
+    // Short-K layers run pixel-major (the epilogue writes pixel rows or NCHW
+    // planes directly); the long-K 7x7 stage layers run swap-AB with wide
+    // tiles that share each weight k-block across 512 pixels.
+    p.pixel_major = L0.exec_k != 7 ? 1 : 0;
+    if (p.pixel_major) {
+      const int c64 = round_up(L0.def.cout, 64);
+      p.pm_n = c64 >= 256 ? 256 : c64;
+      p.subs = conv_pm_subs(p.pm_n);
+      p.m_tiles = (L0.def.cout + p.pm_n - 1) / p.pm_n;
+      p.tiles_per_image = (p.H * p.Wp + 128 * p.subs - 1) / (128 * p.subs);
+    } else {
+      p.pm_n = 0;
+      p.subs = L0.exec_k == 7 ? 2 : 1;
+      p.m_tiles = L0.cout_pad / 128;
+      p.tiles_per_image = (p.H * p.Wp + 256 * p.subs - 1) / (256 * p.subs);
+    }
     p.n_groups = int(layers.size());
     p.total_tiles = p.n_groups * p.n_images * p.tiles_per_image * p.m_tiles;
     for (size_t g = 0; g < layers.size(); ++g) {
@@ -364,7 +381,7 @@ struct PlanBuilder {
       if (L.exec_k != p.k || L.cin_pad != L0.cin_pad || L.cout_pad != L0.cout_pad ||
           in[g].c_off != p.in_c_off || (out[g].buf == -1) != to_output)
         fail(AVEC_ERR_INVALID_MODEL, "grouped conv layers differ in shape");
-      if (p.out_mode == kOutTmaBf16) {
+      if (p.out_mode == kOutTmaBf16 && !p.pixel_major) {
         const int ob = out[g].buf;
         op.maps.out[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob], uint64_t(gi.Hp()) * gi.Wp(),
                                            plan.n);
@@ -380,7 +397,9 @@ struct PlanBuilder {
       const uint64_t rows = uint64_t(plan.n) * gi.Hp() * gi.Wp();
       op.maps.act_big[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 256);
       op.maps.act_small[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 8);
-      op.maps.wgt[g] = make_map_2d(L.w, uint64_t(L.exec_k) * L.exec_k * L.cin_pad, L.cout_pad, 128);
+      op.maps.act_mid[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 128);
+      op.maps.wgt[g] = make_map_2d(L.w, uint64_t(L.exec_k) * L.exec_k * L.cin_pad, L.cout_pad,
+                                   p.pixel_major ? uint32_t(p.pm_n) : 128u);
       op.layers[g] = layers[g];
       record_io(layers[g], in[g], out[g]);
     }
@@ -483,7 +502,10 @@ void run_ops(avec_ctx* ctx, const Plan& plan, const PoseNet& net, size_t first, 
                             plan.geo[0].P, st);
         break;
       case PlanOp::kConv:
-        launch_conv_tc(op.maps, op.cp, ctx->sms, st);
+        if (op.cp.pixel_major)
+          launch_conv_pm(op.maps, op.cp, ctx->sms, st);
+        else
+          launch_conv_tc(op.maps, op.cp, ctx->sms, st);
         break;
       case PlanOp::kPool: {
         const Geometry& g = plan.geo[op.level];
@@ -561,6 +583,7 @@ void ctx_init(avec_ctx* ctx, int device, int slots) {
   ctx->sms = prop.multiProcessorCount;
   ctx->label = "b200:" + std::to_string(device);
   conv_configure();
+  conv_pm_configure();
   if (slots <= 0) slots = 2;
   for (int i = 0; i < slots; ++i) {
     auto s = std::make_unique<Slot>();

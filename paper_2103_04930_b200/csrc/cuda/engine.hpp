@@ -26,6 +26,9 @@ inline void check_cuda(cudaError_t e, const char* what) {
          std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// programmatic dependent launch between conv layers (opt-in: env AVEC_PDL=1)
+bool pdl_enabled();
+
 // ---- kernels (one .cu each) ----
 void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K,
                           cudaStream_t stream);

@@ -121,6 +121,7 @@ struct avec_ctx {
   std::string label;
   std::vector<std::unique_ptr<avec::Slot>> slots;
   std::vector<bool> slot_busy;
+  size_t next_slot = 0;  // round-robin cursor (guarded by slot_m)
   std::mutex slot_m;
   std::condition_variable slot_cv;
   std::mutex model_m;
