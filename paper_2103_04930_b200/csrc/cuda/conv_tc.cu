@@ -30,11 +30,14 @@ struct Cfg {
   static constexpr int kWinBytes = kWinRows * 128;
   static constexpr int kWinStages = 2;
   static constexpr int kAccStages = 2 / SUBS;   // TMEM holds 512 fp32 columns
-  static constexpr int kWgtStages = SUBS == 2 ? 4 : 8;
+  // the wide tiles trade the second epilogue staging buffer for a 5th weight
+  // stage: deeper weight prefetch matters more than epilogue overlap there
+  static constexpr int kStgBufs = SUBS == 2 ? 1 : 2;
+  static constexpr int kWgtStages = SUBS == 2 ? 5 : 8;
   static constexpr int win = 0;
   static constexpr int wgt = win + kWinStages * kWinBytes;
   static constexpr int stg = wgt + kWgtStages * kWgtBytes;
-  static constexpr int bars = stg + 2 * kStageBytes;
+  static constexpr int bars = stg + kStgBufs * kStageBytes;
   static constexpr int total = bars + 256;
   static_assert(kWinBytes % 1024 == 0 && wgt % 1024 == 0 && stg % 1024 == 0,
                 "SW128 operands need 1024 B alignment");
@@ -56,6 +59,55 @@ __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t) {
   c.n = rem / p.tiles_per_image;
   return c;
 }
+
+// One unit of work: output positions [o0, o0+len) of image n, branch g, channel tile mt.
+struct Work {
+  int g, n, mt, o0, len;
+};
+
+// Iterates this CTA's work. Regular mode: fixed tiles strided by gridDim.x.
+// Balanced mode (p.balanced_units > 0): the (branch, image) segments are cut
+// into 32-position units and every CTA takes an equal contiguous run of them,
+// split at segment ends and at kMaxLen positions, so all SMs finish together
+// instead of 128 tiles leaving 20 of 148 SMs idle. Runs that end mid-chunk
+// overlap a neighbour's first chunk; both CTAs compute bit-identical values
+// for those positions, so the duplicate stores are benign.
+struct WorkIter {
+  int cur, end;
+  __device__ explicit WorkIter(const ConvParams& p) {
+    if (p.balanced_units > 0) {
+      cur = int(static_cast<long long>(blockIdx.x) * p.balanced_units / gridDim.x);
+      end = int(static_cast<long long>(blockIdx.x + 1) * p.balanced_units / gridDim.x);
+    } else {
+      cur = blockIdx.x;
+      end = p.total_tiles;
+    }
+  }
+  template <int kMaxLen>
+  __device__ bool next(const ConvParams& p, Work& w) {
+    if (cur >= end) return false;
+    if (p.balanced_units > 0) {
+      const int U = p.units_per_seg;
+      const int seg = cur / U, off = cur - seg * U;
+      const int take = min(min(end, (seg + 1) * U) - cur, kMaxLen / 32);
+      w.g = seg / p.n_images;
+      w.n = seg - w.g * p.n_images;
+      w.mt = 0;
+      w.o0 = off * 32;
+      w.len = take * 32;
+      cur += take;
+    } else {
+      const TileCoord tc = decode_tile(p, cur);
+      w.g = tc.g;
+      w.n = tc.n;
+      w.mt = tc.mt;
+      w.o0 = tc.pt * kMaxLen;
+      w.len = kMaxLen;
+      cur += gridDim.x;
+    }
+    return true;
+  }
+};
 
 __device__ __forceinline__ float activate(uint32_t bits, float bias, int relu) {
   float x = __uint_as_float(bits) + bias;
@@ -125,9 +177,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ws = 0, wst = 0;
       uint32_t wph = 0, wtph = 0;
       const uint32_t win_tx = (C::kTileN + (k > 1 ? 8 : 0)) * 128;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-        const TileCoord tc = decode_tile(p, t);
-        const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + tc.pt * C::kTileN;
+      WorkIter it(p);
+      Work tc;
+      while (it.next<C::kTileN>(p, tc)) {
+        const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + tc.o0;
         for (int c = 0; c < p.cin_chunks; ++c) {
           const int ch = p.in_c_off + c * 64;
           for (int r = 0; r < k; ++r) {
@@ -156,11 +209,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
-      const uint32_t idesc = idesc_bf16_f32(kTileM, kSubN);
       int ws = 0, wst = 0, acc = 0;
       uint32_t wph = 0, wtph = 0, aph = 0;
       const uint32_t win_base = smem_u32(win), wgt_base = smem_u32(wgt);
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      WorkIter it(p);
+      Work tc;
+      while (it.next<C::kTileN>(p, tc)) {
+        // MMA N per sub-tile: 256, or the (32-multiple) remainder of a short run
+        uint32_t idesc[SUBS];
+        int nsub = 0;
+#pragma unroll
+        for (int sub = 0; sub < SUBS; ++sub) {
+          const int n_cols = min(kSubN, tc.len - sub * kSubN);
+          idesc[sub] = n_cols > 0 ? idesc_bf16_f32(kTileM, n_cols) : 0u;
+          nsub += n_cols > 0;
+        }
         mbar_wait(&acc_empty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem + acc * C::kTileN;
@@ -176,11 +239,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t ab = wgt_base + wst * kWgtBytes;
 #pragma unroll
               for (int sub = 0; sub < SUBS; ++sub) {
+                if (sub < nsub) {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                  const uint64_t ad = desc_sw128(ab + kk * 32);
-                  const uint64_t bd = desc_sw128(wb + (sub * kSubN + s) * 128 + kk * 32);
-                  mma_bf16_ss(d0 + sub * kSubN, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+                  for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t ad = desc_sw128(ab + kk * 32);
+                    const uint64_t bd = desc_sw128(wb + (sub * kSubN + s) * 128 + kk * 32);
+                    mma_bf16_ss(d0 + sub * kSubN, ad, bd, idesc[sub], (first && kk == 0) ? 0u : 1u);
+                  }
                 }
               }
               first = false;
@@ -204,8 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = threadIdx.x == 64;
     int acc = 0, stg_i = 0;
     uint32_t aph = 0;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-      const TileCoord tc = decode_tile(p, t);
+    WorkIter it(p);
+    Work tc;
+    while (it.next<C::kTileN>(p, tc)) {
       const ConvGroupParams& g = p.g[tc.g];
       const int co = tc.mt * kTileM + co_local;
       const int cout_m = min(kTileM, g.cout - tc.mt * kTileM);  // channels of this m-tile
@@ -215,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       for (int sub = 0; sub < SUBS; ++sub) {
         for (int ch = 0; ch < kSubN / kChunk; ++ch) {
-          const int o0 = tc.pt * C::kTileN + sub * kSubN + ch * kChunk;
+          if (sub * kSubN + ch * kChunk >= tc.len) break;  // uniform across the epilogue warps
+          const int o0 = tc.o0 + sub * kSubN + ch * kChunk;
           uint32_t v[32];
           tmem_ld32(tmem + ((quad * 32) << 16) + acc * C::kTileN + sub * kSubN + ch * kChunk, v);
           tmem_ld_wait();
@@ -225,8 +292,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ww = pos - hh * p.Wp;
           const uint32_t mask = __ballot_sync(0xffffffffu, hh < p.H && ww < p.W);
           if (p.out_mode == kOutTmaBf16) {
-            uint8_t* buf = stg + (stg_i & 1) * kStageBytes;
-            if (leader) bulk_wait_read<1>();  // the store that last used `buf` has read it
+            uint8_t* buf = stg + (stg_i % C::kStgBufs) * kStageBytes;
+            // the store that last used `buf` must have read it
+            if (leader) {
+              if (C::kStgBufs == 2) bulk_wait_read<1>();
+              else bulk_wait_read<0>();
+            }
             named_bar_sync(kEpiBar, kEpiThreads);
             if (live) {
               uint8_t* half = buf + (co_local >> 6) * (kChunk * 128);
@@ -310,7 +381,8 @@ void conv_configure() {
 }
 
 void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
-  const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
+  const int work = p.balanced_units > 0 ? p.balanced_units : p.total_tiles;
+  const int grid = work < sm_count ? work : sm_count;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);

@@ -81,6 +81,10 @@ struct ConvParams {
   int tiles_per_image; // ceil(H*Wp / pixels per tile)
   int n_groups;
   int total_tiles;
+  // swap-AB balanced partition (0 = regular tiles): 32-position units over the
+  // n_groups * n_images segments of units_per_seg units each
+  int balanced_units;
+  int units_per_seg;
   ConvGroupParams g[kConvMaxGroups];
 };
 

@@ -376,6 +376,19 @@ struct PlanBuilder {
     }
     p.n_groups = int(layers.size());
     p.total_tiles = p.n_groups * p.n_images * p.tiles_per_image * p.m_tiles;
+    p.units_per_seg = (p.H * p.Wp + 31) / 32;
+    // balanced persistent partition for the wide-tile swap-AB launches
+    // Opt-in (AVEC_BALANCED=1): measured slower on C2 (95.6 vs 82.7 us per 7x7
+    // pair) because the runs that span two segments re-stream the weights twice
+    // and set the kernel's critical path; kept for shapes whose regular tile
+    // count leaves many SMs idle.
+    static const bool balanced_on = [] {
+      const char* e = std::getenv("AVEC_BALANCED");
+      return e && e[0] == '1';
+    }();
+    p.balanced_units = (balanced_on && !p.pixel_major && p.subs == 2 && p.m_tiles == 1)
+                           ? p.n_groups * p.n_images * p.units_per_seg
+                           : 0;
     for (size_t g = 0; g < layers.size(); ++g) {
       const ConvLayerDev& L = net.layers[layers[g]];
       if (L.exec_k != p.k || L.cin_pad != L0.cin_pad || L.cout_pad != L0.cout_pad ||

@@ -111,7 +111,7 @@ __global__ void probe_mma(const __grid_constant__ CUtensorMap mapA,
 }
 
 // issue-rate probe: one CTA per SM, thread 0 streams MMAs on resident smem
-__global__ void probe_rate(int N, int iters, unsigned long long* cycles) {
+__global__ void probe_rate(int N, int iters, unsigned long long* cycles, int b_row_off = 0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar_mma;
@@ -130,7 +130,7 @@ __global__ void probe_rate(int N, int iters, unsigned long long* cycles) {
   tc_fence_after();
   if (threadIdx.x == 0) {
     const uint32_t idesc = idesc_bf16_f32(128, N);
-    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 16384);
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 16384) + b_row_off * 128;
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -145,6 +145,48 @@ __global__ void probe_rate(int N, int iters, unsigned long long* cycles) {
   tc_fence_before();
   __syncthreads();
   if (warp_id() == 0) tmem_dealloc<256>(tmem_base);
+}
+
+// per "k-block": 7 taps x 2 subs x 4 k-slices, A from a 16 KB weight tile,
+// B from a 520-row window at row offset s (+256 for sub 1), like conv_tc_kernel<2>
+__global__ void probe_conv_pattern(int kblocks, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar_mma;
+  __shared__ uint32_t tmem_base;
+  for (int i = threadIdx.x; i < (16384 + 66560) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp_id() == 0) tmem_alloc<512>(&tmem_base);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_mma, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16_f32(128, 256);
+    const uint32_t a0 = smem_u32(smem), w0 = smem_u32(smem + 16384);
+    long long t0 = clock64();
+    for (int kb = 0; kb < kblocks; ++kb) {
+      for (int s = 0; s < 7; ++s) {
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16_ss(tmem_base + sub * 256, desc_sw128(a0 + kk * 32),
+                        desc_sw128(w0 + (sub * 256 + s) * 128 + kk * 32), idesc, 1);
+      }
+    }
+    mma_commit(&bar_mma);
+    mbar_wait(&bar_mma, 0);
+    long long t1 = clock64();
+    cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc<512>(tmem_base);
 }
 
 int main() {
@@ -211,8 +253,9 @@ int main() {
   unsigned long long* dc;
   CK(cudaMalloc(&dc, sms * 8));
   std::vector<unsigned long long> hc(sms);
-  for (int ni = 0; ni < 3; ++ni) {
-    int N = Ns[ni], iters = 4096;
+  const int Nr[9] = {64, 96, 128, 160, 176, 192, 208, 224, 256};
+  for (int ni = 0; ni < 9; ++ni) {
+    int N = Nr[ni], iters = 4096;
     probe_rate<<<sms, 128, smem>>>(N, 16, dc);  // warm
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
@@ -231,6 +274,29 @@ int main() {
     double flops = 2.0 * 128 * N * 16 * 4.0 * iters * sms;
     std::printf("%s{\"N\": %d, \"cycles_per_mma\": %.2f, \"ideal_cycles\": %.1f, \"tflops\": %.1f}",
                 ni ? ", " : "", N, cyc / (4.0 * iters), 128.0 * N / 256.0, flops / (ms * 1e-3) / 1e12);
+  }
+  // operand B read at a row offset that is not a multiple of the 8-row swizzle atom
+  std::printf("], \"rate_offset\": [");
+  const int offs[5] = {0, 1, 3, 7, 8};
+  for (int oi = 0; oi < 5; ++oi) {
+    probe_rate<<<sms, 128, smem>>>(256, 4096, dc, offs[oi]);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(hc.data(), dc, sms * 8, cudaMemcpyDeviceToHost));
+    double cyc = 0;
+    for (int i = 0; i < sms; ++i) cyc += double(hc[i]);
+    std::printf("%s{\"N\": 256, \"b_row_off\": %d, \"cycles_per_mma\": %.2f}", oi ? ", " : "", offs[oi],
+                cyc / sms / (4.0 * 4096));
+  }
+  // the conv kernel's exact operand pattern (weights A, 520-row window B, two subs, 7 taps)
+  std::printf("], \"rate_conv_pattern\": [");
+  for (int rep = 0; rep < 2; ++rep) {
+    CK(cudaFuncSetAttribute(probe_conv_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + 16384 + 66560));
+    probe_conv_pattern<<<sms, 128, 1024 + 16384 + 66560>>>(512, dc);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(hc.data(), dc, sms * 8, cudaMemcpyDeviceToHost));
+    double cyc = 0;
+    for (int i = 0; i < sms; ++i) cyc += double(hc[i]);
+    std::printf("%s{\"cycles_per_mma_N256\": %.2f}", rep ? ", " : "", cyc / sms / (512.0 * 7 * 2 * 4));
   }
   std::printf("], \"sms\": %d}\n", sms);
   return 0;
