@@ -17,14 +17,14 @@ CUDA_SRCS := $(wildcard $(CUDA_DIR)/*.cu) $(wildcard $(CUDA_DIR)/*.cpp)
 CUDA_HDRS := $(wildcard $(CUDA_DIR)/*.hpp) $(wildcard $(CUDA_DIR)/*.cuh) include/avec_cuda.h
 CUDA_OBJS := $(patsubst $(CUDA_DIR)/%,build/obj/cuda/%.o,$(CUDA_SRCS))
 
-HOST_SRCS := $(filter-out $(HOST_DIR)/server_main.cpp,$(wildcard $(HOST_DIR)/*.cpp))
+HOST_SRCS := $(filter-out $(HOST_DIR)/%_main.cpp,$(wildcard $(HOST_DIR)/*.cpp))
 HOST_HDRS := $(wildcard $(HOST_DIR)/*.hpp) include/avec_cuda.h
 HOST_OBJS := $(patsubst $(HOST_DIR)/%.cpp,build/obj/host/%.o,$(HOST_SRCS))
 
 .PHONY: all product oracle probe clean
 all: product oracle probe
 
-product: $(LIB)/libavec_cuda.so $(LIB)/libavec_host.so $(BIN)/avec-server
+product: $(LIB)/libavec_cuda.so $(LIB)/libavec_host.so $(BIN)/avec-server $(BIN)/avec-loadgen
 
 build/obj/cuda/%.cu.o: $(CUDA_DIR)/%.cu $(CUDA_HDRS)
 	@mkdir -p $(dir $@)
@@ -48,6 +48,16 @@ $(LIB)/libavec_host.so: $(HOST_OBJS) $(LIB)/libavec_cuda.so
 $(BIN)/avec-server: $(HOST_DIR)/server_main.cpp $(LIB)/libavec_host.so
 	@mkdir -p $(BIN)
 	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIB) -lavec_host -lavec_cuda -Wl,-rpath,'$$ORIGIN/../lib' -lpthread
+
+$(BIN)/avec-loadgen: $(HOST_DIR)/loadgen_main.cpp $(LIB)/libavec_host.so
+	@mkdir -p $(BIN)
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIB) -lavec_host -lavec_cuda -Wl,-rpath,'$$ORIGIN/../lib' -lpthread
+
+# test-only: the same server over a CPU stub backend (tests/native), for
+# protocol tests without a GPU
+build/avec_stub_server: tests/native/stub_server.cpp $(LIB)/libavec_host.so
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -I$(HOST_DIR) -o $@ $< -L$(LIB) -lavec_host -lavec_cuda -Wl,-rpath,'$$ORIGIN/../$(LIB)' -lpthread
 
 oracle:
 	$(MAKE) -C oracle oracle

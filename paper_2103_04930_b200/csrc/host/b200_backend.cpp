@@ -1,0 +1,170 @@
+#include "b200_backend.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+#include <thread>
+
+#include "avec_cuda.h"
+
+namespace avec::backend {
+
+namespace {
+
+[[noreturn]] void rethrow(int rc) {
+  const std::string msg = avec_last_error();
+  switch (rc) {
+    case AVEC_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case AVEC_ERR_UNKNOWN_MODEL: throw Error(ErrorCode::unknown_model, msg);
+    case AVEC_ERR_INVALID_MODEL: throw Error(ErrorCode::invalid_model, msg);
+    case AVEC_ERR_DEGENERATE_OUTPUT: throw Error(ErrorCode::degenerate_output, msg);
+    default: throw Error(ErrorCode::internal, msg);
+  }
+}
+
+void check(int rc) {
+  if (rc != AVEC_OK) rethrow(rc);
+}
+
+}  // namespace
+
+B200Backend::B200Backend(std::vector<int> devices, int slots_per_device, Policy policy)
+    : slots_(slots_per_device < 1 ? 2 : slots_per_device), policy_(policy) {
+  if (devices.empty()) {
+    int n = 0;
+    check(avec_device_count(&n));
+    for (int i = 0; i < n; ++i) devices.push_back(i);
+  }
+  if (devices.empty()) throw Error(ErrorCode::internal, "no CUDA device visible");
+  try {
+    for (int d : devices) {
+      avec_ctx* c = nullptr;
+      check(avec_ctx_create(d, slots_, &c));
+      ctx_.push_back(c);
+    }
+  } catch (...) {
+    for (auto* c : ctx_) avec_ctx_destroy(c);
+    throw;
+  }
+  devices_ = devices;
+  inflight_.reset(new std::atomic<int>[ctx_.size()]);
+  for (size_t i = 0; i < ctx_.size(); ++i) inflight_[i] = 0;
+  label_ = ctx_.size() == 1 ? std::string(avec_ctx_label(ctx_[0]))
+                            : "b200x" + std::to_string(ctx_.size()) +
+                                  (policy_ == Policy::split ? ":split" : ":affinity");
+}
+
+B200Backend::~B200Backend() {
+  for (auto* c : ctx_) avec_ctx_destroy(c);
+}
+
+ModelHandle B200Backend::register_model(const wire::ModelDescriptor& m) {
+  // reference backend.cpp:70-73 validation happens in the engine, per device
+  std::lock_guard<std::mutex> lk(m_);
+  auto it = id_by_digest_.find(m.digest);
+  if (it != id_by_digest_.end()) return {it->second};
+  Entry e;
+  for (auto* c : ctx_) {
+    std::uint64_t h = 0;
+    const int rc = avec_model_register(c, m.digest.data(), m.name.data(), m.name.size(),
+                                       m.structure.data(), m.structure.size(), m.weights.data(),
+                                       m.weights.size(), m.output_divisor, &h);
+    if (rc != AVEC_OK) rethrow(rc);
+    e.per_device.push_back(h);
+  }
+  check(avec_model_kind(ctx_[0], e.per_device[0], &e.kind));
+  const std::uint64_t id = next_id_++;
+  id_by_digest_.emplace(m.digest, id);
+  models_.emplace(id, std::move(e));
+  return {id};
+}
+
+B200Backend::Entry B200Backend::lookup(ModelHandle h) {
+  std::lock_guard<std::mutex> lk(m_);
+  auto it = models_.find(h.id);
+  if (it == models_.end()) throw Error(ErrorCode::unknown_model, "handle was never issued by this backend");
+  return it->second;
+}
+
+std::uint64_t B200Backend::output_elems(ModelHandle model, const wire::Dims& d) {
+  const Entry e = lookup(model);
+  std::uint64_t k = 0;
+  check(avec_output_elems(ctx_[0], e.per_device[0], d.batch, d.channels, d.height, d.width, &k));
+  return k;
+}
+
+int B200Backend::concurrency() const {
+  return policy_ == Policy::split ? slots_ : int(ctx_.size()) * slots_;
+}
+
+int B200Backend::pick_device() {
+  int best = 0;
+  for (size_t i = 1; i < ctx_.size(); ++i)
+    if (inflight_[i].load() < inflight_[best].load()) best = int(i);
+  return best;
+}
+
+double B200Backend::run_on(int dev, const Entry& e, const wire::Dims& d, const float* in,
+                           std::uint64_t n_in, float* out, std::uint64_t n_out) {
+  inflight_[dev]++;
+  double s = 0;
+  const int rc = avec_forward(ctx_[dev], e.per_device[dev], d.batch, d.channels, d.height, d.width, in,
+                              n_in, out, n_out, &s);
+  inflight_[dev]--;
+  if (rc != AVEC_OK) rethrow(rc);
+  return s;
+}
+
+double B200Backend::forward_into(ModelHandle model, const wire::Dims& d, const float* in,
+                                 std::uint64_t n_in, float* out, std::uint64_t n_out) {
+  const Entry e = lookup(model);
+  const std::uint64_t frames = std::uint64_t(d.batch) * d.channels / 3;
+  const int G = int(ctx_.size());
+  if (policy_ == Policy::affinity || G == 1 || e.kind != AVEC_MODEL_POSENET || frames < 2 ||
+      std::uint64_t(d.batch) * d.channels % 3 != 0)
+    return run_on(pick_device(), e, d, in, n_in, out, n_out);
+  // split: contiguous frame groups, one per GPU, concurrently
+  const std::uint64_t per_frame_in = 3ull * d.height * d.width;
+  const std::uint64_t per_frame_out = n_out / frames;
+  const int groups = int(std::min<std::uint64_t>(frames, G));
+  std::vector<double> secs(groups, 0.0);
+  std::vector<std::exception_ptr> errs(groups);
+  std::vector<std::thread> th;
+  std::uint64_t f0 = 0;
+  for (int g = 0; g < groups; ++g) {
+    const std::uint64_t nf = frames / groups + (std::uint64_t(g) < frames % groups ? 1 : 0);
+    const wire::Dims sub{1, std::uint32_t(3 * nf), d.height, d.width};
+    th.emplace_back([&, g, f0, nf, sub] {
+      try {
+        secs[g] = run_on(g, e, sub, in + f0 * per_frame_in, nf * per_frame_in, out + f0 * per_frame_out,
+                         nf * per_frame_out);
+      } catch (...) {
+        errs[g] = std::current_exception();
+      }
+    });
+    f0 += nf;
+  }
+  for (auto& t : th) t.join();
+  for (auto& ep : errs)
+    if (ep) std::rethrow_exception(ep);
+  return *std::max_element(secs.begin(), secs.end());
+}
+
+Heatmap B200Backend::forward(ModelHandle model, const Frame& frame) {
+  if (frame.data.size() != frame.dims.elem_count())
+    throw std::invalid_argument("frame data size disagrees with dims");
+  Heatmap h;
+  h.data.resize(output_elems(model, frame.dims));
+  forward_into(model, frame.dims, frame.data.data(), frame.data.size(), h.data.data(), h.data.size());
+  return h;
+}
+
+void* B200Backend::alloc_host(std::size_t bytes) {
+  void* p = avec_host_alloc(bytes);
+  if (!p) throw std::bad_alloc();
+  return p;
+}
+
+void B200Backend::free_host(void* p) { avec_host_free(p); }
+
+}  // namespace avec::backend

@@ -1,0 +1,69 @@
+// The B200 compute plugin: accelfwd-style Backend over the C-ABI of
+// libavec_cuda.so (include/avec_cuda.h), one avec_ctx per GPU.
+//
+// Multi-GPU: frames are independent, so there is no
+// collective. Two placement policies:
+//  * affinity (default): each forward runs whole on the least-loaded GPU;
+//    sessions spread across GPUs (C4: 8 clients, one per B200);
+//  * split: a batched pose-net forward (channels = 3N) is cut into contiguous
+//    frame groups, one per GPU, run concurrently; each GPU writes its slice of
+//    the NCHW output, which is batch-major, so slices are contiguous (C5).
+#pragma once
+
+#include <atomic>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "backend.hpp"
+
+struct avec_ctx;
+
+namespace avec::backend {
+
+class B200Backend final : public Backend {
+ public:
+  enum class Policy { affinity, split };
+  // devices empty = all visible GPUs
+  explicit B200Backend(std::vector<int> devices = {}, int slots_per_device = 2,
+                       Policy policy = Policy::affinity);
+  ~B200Backend() override;
+
+  ModelHandle register_model(const wire::ModelDescriptor& model) override;
+  Heatmap forward(ModelHandle model, const Frame& frame) override;
+  std::string_view label() const override { return label_; }
+
+  bool zero_copy() const override { return true; }
+  std::uint64_t output_elems(ModelHandle model, const wire::Dims& dims) override;
+  double forward_into(ModelHandle model, const wire::Dims& dims, const float* in, std::uint64_t n_in,
+                      float* out, std::uint64_t n_out) override;
+  int concurrency() const override;
+  void* alloc_host(std::size_t bytes) override;
+  void free_host(void* p) override;
+
+  int device_count() const { return int(ctx_.size()); }
+
+ private:
+  struct Entry {
+    int kind = 0;
+    std::vector<std::uint64_t> per_device;  // handle on each context
+  };
+  Entry lookup(ModelHandle h);
+  int pick_device();
+  double run_on(int dev, const Entry& e, const wire::Dims& d, const float* in, std::uint64_t n_in,
+                float* out, std::uint64_t n_out);
+
+  std::vector<avec_ctx*> ctx_;
+  std::vector<int> devices_;
+  int slots_;
+  Policy policy_;
+  std::string label_;
+  std::unique_ptr<std::atomic<int>[]> inflight_;
+  std::mutex m_;
+  std::map<wire::Digest, std::uint64_t> id_by_digest_;
+  std::map<std::uint64_t, Entry> models_;
+  std::uint64_t next_id_ = 1;
+};
+
+}  // namespace avec::backend

@@ -1,0 +1,113 @@
+// Compute plugin contract of the destination server, mirroring
+// accelfwd::backend::Backend (proj/include/accelfwd/backend.hpp:64-78):
+// register_model (idempotent per digest, handles from 1), forward, label.
+//
+// The B200 server needs two more things from a backend, both with defaults so
+// any reference-style backend still plugs in:
+//  * forward_into: zero-copy forward from the session's pinned ingest buffer
+//    into its pinned egress buffer, returning the device-measured compute
+//    seconds shipped as ForwardResult.compute_s (wire.hpp:122);
+//  * concurrency: how many forwards may run at once (GPUs x slots), so the
+//    dispatcher can keep every device busy while preserving FIFO dispatch.
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "wire.hpp"
+
+namespace avec::backend {
+
+// reference ErrorCode values a backend raises (error.hpp:8-41)
+enum class ErrorCode { invalid_model, unknown_model, degenerate_output, internal, bad_config };
+
+struct Error : std::runtime_error {
+  ErrorCode code;
+  Error(ErrorCode c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct Frame {
+  wire::Dims dims;
+  std::vector<float> data;  // flattened, batch-major
+};
+
+struct Heatmap {
+  std::vector<float> data;
+  std::uint64_t elem_count() const { return data.size(); }
+};
+
+struct ModelHandle {
+  std::uint64_t id = 0;  // valid ids start at 1
+  bool operator==(const ModelHandle&) const = default;
+};
+
+// FIFO admission for a single accelerator (reference backend.hpp:40-62)
+class FifoGate {
+ public:
+  class Pass {
+   public:
+    explicit Pass(FifoGate* g) : g_(g) {}
+    Pass(Pass&& o) noexcept : g_(o.g_) { o.g_ = nullptr; }
+    Pass(const Pass&) = delete;
+    ~Pass() {
+      if (g_) g_->leave();
+    }
+
+   private:
+    FifoGate* g_;
+  };
+  Pass enter();
+
+ private:
+  void leave();
+  std::mutex m_;
+  std::condition_variable cv_;
+  std::uint64_t next_ = 0, serving_ = 0;
+};
+
+class Backend {
+ public:
+  virtual ~Backend() = default;
+
+  // Throws Error{invalid_model}.
+  virtual ModelHandle register_model(const wire::ModelDescriptor& model) = 0;
+  // Throws Error{unknown_model | degenerate_output | internal}, std::invalid_argument.
+  virtual Heatmap forward(ModelHandle model, const Frame& frame) = 0;
+  virtual std::string_view label() const = 0;
+
+  // ---- B200 server extensions (defaults go through forward()) ----
+  virtual bool zero_copy() const { return false; }
+  virtual std::uint64_t output_elems(ModelHandle, const wire::Dims&) {
+    throw Error(ErrorCode::internal, "output_elems unsupported by this backend");
+  }
+  virtual double forward_into(ModelHandle, const wire::Dims&, const float*, std::uint64_t, float*,
+                              std::uint64_t) {
+    throw Error(ErrorCode::internal, "forward_into unsupported by this backend");
+  }
+  virtual int concurrency() const { return 1; }
+  // host memory for ingest/egress staging (pinned when the backend can)
+  virtual void* alloc_host(std::size_t bytes);
+  virtual void free_host(void* p);
+};
+
+// Emulation presets of the reference (backend.cpp:108-134) and the delay
+// wrapper (backend.cpp:138-174): each forward takes at least the preset's
+// per-frame time; the first registration per digest pays its load time.
+struct BackendProfile {
+  double per_frame_compute_s = 0;
+  double model_load_s = 0;
+  std::string label = "none";
+  bool is_zero() const { return per_frame_compute_s <= 0 && model_load_s <= 0; }
+};
+BackendProfile preset_profile(std::string_view name, std::string_view kind, double scale);
+std::shared_ptr<Backend> wrap_delay(std::shared_ptr<Backend> inner, BackendProfile profile);
+
+}  // namespace avec::backend

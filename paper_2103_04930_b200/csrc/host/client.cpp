@@ -1,0 +1,70 @@
+#include "client.hpp"
+
+namespace avec::client {
+
+using namespace wire;
+
+Session Session::connect(const std::string& endpoint, double timeout_s) {
+  Session s(net::connect_tcp(endpoint, timeout_s));
+  s.handshake();
+  return s;
+}
+
+Session::Session(std::unique_ptr<net::Stream> stream)
+    : ch_(std::make_unique<net::Channel>(std::move(stream))) {}
+
+namespace {
+[[noreturn]] void remote(const ErrorMsg& e) {
+  throw RemoteError(e.code, std::string("destination reported ") + wire_error_name(e.code) + ": " + e.message);
+}
+}  // namespace
+
+void Session::handshake(std::uint32_t version) {
+  ch_->send(Hello{version});
+  Message m = ch_->recv();
+  if (const auto* ack = std::get_if<HelloAck>(&m)) {
+    if (ack->version != version) throw std::runtime_error("destination speaks another protocol version");
+    return;
+  }
+  if (const auto* e = std::get_if<ErrorMsg>(&m)) remote(*e);
+  throw std::runtime_error("unexpected handshake reply");
+}
+
+bool Session::ensure_model(const ModelDescriptor& model) {
+  ch_->send(ModelCheck{model.digest});
+  Message m = ch_->recv();
+  if (const auto* e = std::get_if<ErrorMsg>(&m)) remote(*e);
+  if (const auto* ack = std::get_if<ModelAck>(&m)) {
+    if (ack->digest != model.digest) throw std::runtime_error("acknowledged digest differs");
+    return true;
+  }
+  if (!std::get_if<ModelNeeded>(&m)) throw std::runtime_error("unexpected reply to ModelCheck");
+  ModelUpload up;
+  up.digest = model.digest;
+  up.output_divisor = model.output_divisor;
+  up.name = model.name;
+  up.structure = model.structure;
+  up.weights = model.weights;
+  ch_->send(Message(std::move(up)));
+  Message m2 = ch_->recv();
+  if (const auto* e = std::get_if<ErrorMsg>(&m2)) remote(*e);
+  const auto* ack = std::get_if<ModelAck>(&m2);
+  if (!ack || ack->digest != model.digest) throw std::runtime_error("upload was not acknowledged");
+  return false;
+}
+
+double Session::forward(const float* data, std::uint32_t elems, std::uint32_t width,
+                        std::uint32_t height, std::vector<float>& out) {
+  const auto head = frame_data_header(elems);
+  ch_->send_parts(head.data(), head.size(), data, std::size_t(elems) * 4);
+  ch_->send(Resolution{width, height});
+  ch_->send(FrameSize{elems});
+  Message m = ch_->recv();
+  if (const auto* e = std::get_if<ErrorMsg>(&m)) remote(*e);
+  auto* fr = std::get_if<ForwardResult>(&m);
+  if (!fr) throw std::runtime_error("expected ForwardResult");
+  out = std::move(fr->data);
+  return fr->compute_s;
+}
+
+}  // namespace avec::client

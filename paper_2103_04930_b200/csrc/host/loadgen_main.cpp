@@ -1,0 +1,108 @@
+// avec-loadgen: N concurrent sessions driving an AVEC destination over TCP and
+// reporting through-the-wire frames/s (BASELINE configs C2/C4). Frames follow
+// the reference harness generator (proj/src/harness.cpp:29-42: seed_seq{lo32,
+// hi32, index} -> mt19937_64, top 24 bits / 2^24), batch folded into channels.
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "client.hpp"
+
+namespace {
+
+std::vector<float> gen_batch(std::uint64_t seed, std::uint32_t first, std::uint32_t batch, std::uint32_t w,
+                             std::uint32_t h) {
+  std::vector<float> out;
+  out.reserve(std::size_t(batch) * 3 * w * h);
+  for (std::uint32_t b = 0; b < batch; ++b) {
+    std::seed_seq seq{std::uint32_t(seed), std::uint32_t(seed >> 32), first + b};
+    std::mt19937_64 rng(seq);
+    for (std::size_t i = 0; i < std::size_t(3) * w * h; ++i)
+      out.push_back(float(double(rng() >> 40) * (1.0 / 16777216.0)));
+  }
+  return out;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  std::string endpoint = "127.0.0.1:7000", model = "posenet";
+  unsigned clients = 1, steps = 20, warmup = 3, batch = 8, width = 656, height = 368;
+  for (int i = 1; i + 1 < argc; i += 2) {
+    std::string a = argv[i], v = argv[i + 1];
+    if (a == "--endpoint") endpoint = v;
+    else if (a == "--clients") clients = std::stoul(v);
+    else if (a == "--steps") steps = std::stoul(v);
+    else if (a == "--warmup") warmup = std::stoul(v);
+    else if (a == "--batch") batch = std::stoul(v);
+    else if (a == "--width") width = std::stoul(v);
+    else if (a == "--height") height = std::stoul(v);
+    else if (a == "--model") model = v;
+    else {
+      std::fprintf(stderr, "unknown option %s\n", a.c_str());
+      return 2;
+    }
+  }
+  using namespace avec;
+  wire::ModelDescriptor md;
+  if (model == "posenet") {
+    std::string s = "avecnet 1\nfamily openpose_coco\ninit he_uniform 1\n";
+    md = wire::make_model("openpose_coco", {s.begin(), s.end()}, {}, 192.0 / 57.0);
+  } else {
+    std::vector<std::uint8_t> s(4096, 7);
+    md = wire::make_model("mockpose", s, {}, 192.0 / 57.0);
+  }
+  std::vector<std::vector<float>> frames;
+  for (unsigned c = 0; c < clients; ++c) frames.push_back(gen_batch(7, c * batch, batch, width, height));
+  const std::uint32_t elems = std::uint32_t(frames[0].size());
+
+  std::atomic<int> ready{0};
+  std::atomic<bool> go{false};
+  std::vector<double> busy(clients, 0.0), compute(clients, 0.0);
+  std::vector<std::string> errs(clients);
+  std::vector<std::thread> th;
+  for (unsigned c = 0; c < clients; ++c) {
+    th.emplace_back([&, c] {
+      try {
+        auto s = client::Session::connect(endpoint, 10.0);
+        s.ensure_model(md);
+        std::vector<float> out;
+        for (unsigned i = 0; i < warmup; ++i) s.forward(frames[c].data(), elems, width, height, out);
+        ready++;
+        while (!go) std::this_thread::yield();
+        const auto t0 = std::chrono::steady_clock::now();
+        for (unsigned i = 0; i < steps; ++i)
+          compute[c] += s.forward(frames[c].data(), elems, width, height, out);
+        busy[c] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        s.close();
+      } catch (const std::exception& e) {
+        errs[c] = e.what();
+        ready++;
+      }
+    });
+  }
+  while (ready < int(clients)) std::this_thread::yield();
+  const auto t0 = std::chrono::steady_clock::now();
+  go = true;
+  for (auto& t : th) t.join();
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  for (auto& e : errs)
+    if (!e.empty()) {
+      std::printf("{\"ok\": false, \"error\": \"%s\"}\n", e.c_str());
+      return 1;
+    }
+  double cs = 0;
+  for (double v : compute) cs += v;
+  const double frames_total = double(steps) * batch * clients;
+  std::printf("{\"ok\": true, \"clients\": %u, \"steps\": %u, \"batch\": %u, \"frames\": %.0f, \"wall_s\": %.6f, "
+              "\"fps\": %.3f, \"ms_per_cycle\": %.4f, \"server_compute_ms\": %.4f, \"model\": \"%s\"}\n",
+              clients, steps, batch, frames_total, wall, frames_total / wall, 1e3 * wall / steps,
+              1e3 * cs / (double(steps) * clients), model.c_str());
+  return 0;
+}
