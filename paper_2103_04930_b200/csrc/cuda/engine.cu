@@ -813,7 +813,7 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
       p.bytes = double(n_img) * h * w * (12.0 + 128.0);
       continue;
     }
-    p.kind = 1;
+    p.kind = op.cp.pixel_major ? 1 : 3;
     for (int g = 0; g < 2; ++g) {
       if (op.layers[g] < 0) continue;
       const ConvDef& d = f.convs[op.layers[g]];

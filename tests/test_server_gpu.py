@@ -115,6 +115,22 @@ def test_loadgen_posenet_throughput(server):
     assert out["ok"] and out["fps"] > 50
 
 
+def test_reference_server_with_b200_plugin():
+    """Plugin-level drop-in: the reference's OWN Server (built from its sources)
+    with the B200 engine behind accelfwd::backend::Backend via the C-ABI shim
+    (oracle/ref_drivers/b200_shim.hpp = INTEGRATION.md), driven by the
+    reference client: results bit-identical to its local MockPose."""
+    exe = ROOT / "oracle" / "_ref" / "ref_b200_server"
+    srv = W.ServerProc([str(exe)])
+    try:
+        assert "(backend b200:0)" in srv.banner
+        rc, out = ref_client(srv.endpoint, "--width", "656", "--height", "368", "--batch", "2",
+                             "--frames", "3", "--check-mockpose")
+        assert rc == 0 and out["mismatches"] == 0 and out["byte_account_bad"] == 0
+    finally:
+        srv.stop()
+
+
 def test_split_policy_server(tmp_path):
     srv = W.ServerProc([str(SERVER), "--policy", "split", "--slots", "1"])
     try:
