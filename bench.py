@@ -150,6 +150,34 @@ def cpu_posenet_oracle_sample() -> dict:
             "cores": O.lib().oracle_threads(), "seconds": dt}
 
 
+def wire_run(device: int, steps: int, clients: int) -> dict:
+    """C2 cycles through bin/avec-server (one GPU) from `clients` concurrent
+    native sessions over TCP loopback (BASELINE "through AVEC server")."""
+    server = ROOT / "paper_2103_04930_b200" / "bin" / "avec-server"
+    loadgen = ROOT / "paper_2103_04930_b200" / "bin" / "avec-loadgen"
+    p = subprocess.Popen([str(server), "--devices", str(device), "--slots", "2"], stdout=subprocess.PIPE,
+                         stderr=subprocess.PIPE, text=True)
+    try:
+        line = p.stdout.readline()
+        if not line.startswith("listening on"):
+            return {"ok": False, "error": "server did not start: " + line + p.stderr.read()[-300:]}
+        ep = line.split()[2]
+        r = subprocess.run([str(loadgen), "--endpoint", ep, "--clients", str(clients), "--steps", str(steps),
+                            "--warmup", "3", "--batch", str(BATCH), "--width", str(W), "--height", str(H)],
+                           capture_output=True, text=True, timeout=900)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        out["transport"] = "TCP loopback, native client (bin/avec-loadgen), avec-server --slots 2"
+        return out
+    except Exception as e:  # noqa: BLE001
+        return {"ok": False, "error": str(e)}
+    finally:
+        p.terminate()
+        try:
+            p.wait(timeout=60)
+        except subprocess.TimeoutExpired:
+            p.kill()
+
+
 def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     import numpy as np
     import torch
@@ -250,6 +278,13 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     e2e_threads = max(e2e_by_threads, key=e2e_by_threads.get)
     e2e = e2e_by_threads[e2e_threads]
 
+    # ---------------- through the wire: avec-server + native clients over TCP ----------------
+    wire = wire_run(dev, steps=max(10, args.steps // 8), clients=2)
+    if world > 1:
+        t = torch.tensor([wire.get("fps", 0.0)], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        wire["fps_all_ranks"] = float(t.item())
+
     # ---------------- roofline of the dominant kernel ----------------
     prof = be.profile(h, dims, d_in[0].data_ptr(), reps=3)
     peaks = load_peaks()
@@ -314,6 +349,7 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
                     "d2h_bytes_per_step": K * 4,
                     "api": f"avec_forward (pinned host buffers), {e2e_threads} host thread(s) over 2 slots",
                     "by_threads": {str(k): round(v, 2) for k, v in e2e_by_threads.items()}},
+            "wire": wire,
             "pdl": os.environ.get("AVEC_PDL", "0") == "1",
             "roofline": roofline, "cpu_baseline": cpu,
             "gpu_launches": args.steps * len(prof),

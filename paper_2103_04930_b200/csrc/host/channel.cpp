@@ -1,6 +1,7 @@
 #include "channel.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 namespace avec::net {
@@ -95,6 +96,40 @@ wire::Message Channel::recv(FrameSink* sink) {
       }
     }
     // inconsistent counts: buffer the whole frame and let the decoder reject it
+  }
+
+  // streamed ForwardResult (client side): preamble, then floats into the sink
+  if (sink && tag == std::uint8_t(wire::Tag::forward_result) && len >= 13) {
+    if (!fill(17)) eof();
+    double compute_s;
+    std::uint32_t count;
+    std::memcpy(&compute_s, data() + 5, 8);
+    std::memcpy(&count, data() + 13, 4);
+    if (count >= 1 && std::uint64_t(len) == 13 + 4 * std::uint64_t(count) && std::isfinite(compute_s) &&
+        compute_s >= 0) {
+      if (float* dst = sink->result_buffer(count)) {
+        head_ += 17;
+        const std::size_t want = 4 * std::size_t(count);
+        const std::size_t have = std::min(avail(), want);
+        std::memcpy(dst, data(), have);
+        head_ += have;
+        std::size_t done = have;
+        auto* out = reinterpret_cast<std::uint8_t*>(dst);
+        while (done < want) {
+          const std::size_t got = stream_->read_some(out + done, want - done);
+          if (got == 0) {
+            poisoned_ = true;
+            throw NetError(NetError::disconnected, "peer closed the connection");
+          }
+          done += got;
+          received_ += got;
+        }
+        wire::ForwardResult fr;
+        fr.compute_s = compute_s;
+        fr.elem_count = count;  // payload is in the sink; fr.data stays empty
+        return fr;
+      }
+    }
   }
 
   if (!fill(wire::kHeaderBytes + std::size_t(len))) eof();

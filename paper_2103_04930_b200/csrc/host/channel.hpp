@@ -31,6 +31,8 @@ class FrameSink {
   // destination for `elems` floats of an incoming FrameData (valid until the
   // next call); nullptr makes the channel buffer the message instead
   virtual float* frame_buffer(std::uint32_t elems) = 0;
+  // same for an incoming ForwardResult (clients); default: buffer it
+  virtual float* result_buffer(std::uint32_t /*elems*/) { return nullptr; }
 };
 
 class Channel {

@@ -53,17 +53,31 @@ bool Session::ensure_model(const ModelDescriptor& model) {
   return false;
 }
 
+namespace {
+// receive the ForwardResult floats straight into the caller's vector
+struct VectorSink final : net::FrameSink {
+  std::vector<float>& v;
+  explicit VectorSink(std::vector<float>& out) : v(out) {}
+  float* frame_buffer(std::uint32_t) override { return nullptr; }
+  float* result_buffer(std::uint32_t elems) override {
+    if (v.size() != elems) v.resize(elems);
+    return v.data();
+  }
+};
+}  // namespace
+
 double Session::forward(const float* data, std::uint32_t elems, std::uint32_t width,
                         std::uint32_t height, std::vector<float>& out) {
   const auto head = frame_data_header(elems);
   ch_->send_parts(head.data(), head.size(), data, std::size_t(elems) * 4);
   ch_->send(Resolution{width, height});
   ch_->send(FrameSize{elems});
-  Message m = ch_->recv();
+  VectorSink sink(out);
+  Message m = ch_->recv(&sink);
   if (const auto* e = std::get_if<ErrorMsg>(&m)) remote(*e);
   auto* fr = std::get_if<ForwardResult>(&m);
   if (!fr) throw std::runtime_error("expected ForwardResult");
-  out = std::move(fr->data);
+  if (!fr->data.empty()) out = std::move(fr->data);  // not streamed (small replies)
   return fr->compute_s;
 }
 

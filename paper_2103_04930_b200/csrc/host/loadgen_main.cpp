@@ -34,6 +34,7 @@ std::vector<float> gen_batch(std::uint64_t seed, std::uint32_t first, std::uint3
 int main(int argc, char** argv) {
   std::string endpoint = "127.0.0.1:7000", model = "posenet";
   unsigned clients = 1, steps = 20, warmup = 3, batch = 8, width = 656, height = 368;
+  unsigned long elems_override = 0;  // raw FrameData size (memcpy sweep), Resolution = width x (E/width)
   for (int i = 1; i + 1 < argc; i += 2) {
     std::string a = argv[i], v = argv[i + 1];
     if (a == "--endpoint") endpoint = v;
@@ -44,6 +45,7 @@ int main(int argc, char** argv) {
     else if (a == "--width") width = std::stoul(v);
     else if (a == "--height") height = std::stoul(v);
     else if (a == "--model") model = v;
+    else if (a == "--elems") elems_override = std::stoul(v);
     else {
       std::fprintf(stderr, "unknown option %s\n", a.c_str());
       return 2;
@@ -55,11 +57,27 @@ int main(int argc, char** argv) {
     std::string s = "avecnet 1\nfamily openpose_coco\ninit he_uniform 1\n";
     md = wire::make_model("openpose_coco", {s.begin(), s.end()}, {}, 192.0 / 57.0);
   } else {
+    // the reference's model: opaque structure -> segment means; "mockpose-c1"
+    // (divisor 1) returns as many floats as it receives (memcpy sweep, C3)
     std::vector<std::uint8_t> s(4096, 7);
-    md = wire::make_model("mockpose", s, {}, 192.0 / 57.0);
+    md = wire::make_model("mockpose", s, {}, model == "mockpose-c1" ? 1.0 : 192.0 / 57.0);
   }
   std::vector<std::vector<float>> frames;
-  for (unsigned c = 0; c < clients; ++c) frames.push_back(gen_batch(7, c * batch, batch, width, height));
+  if (elems_override) {
+    height = std::uint32_t(elems_override / width);
+    if (std::uint64_t(width) * height != elems_override) {
+      std::printf("{\"ok\": false, \"error\": \"--elems must be a multiple of --width\"}\n");
+      return 2;
+    }
+    batch = 1;
+    for (unsigned c = 0; c < clients; ++c) {
+      std::vector<float> f(elems_override);
+      for (std::size_t i = 0; i < f.size(); ++i) f[i] = float(i % 1021) * 0.5f;
+      frames.push_back(std::move(f));
+    }
+  } else {
+    for (unsigned c = 0; c < clients; ++c) frames.push_back(gen_batch(7, c * batch, batch, width, height));
+  }
   const std::uint32_t elems = std::uint32_t(frames[0].size());
 
   std::atomic<int> ready{0};
