@@ -38,12 +38,13 @@ int oracle_threads(void);
 /* bf16 round-to-nearest-even of an fp32 value, returned as fp32 */
 float oracle_bf16_round(float x);
 /* One conv layer on NHWC fp32 activations (values already bf16-representable),
- * weights in wire order W[cout][cin][kh][kw] fp32, bias[cout].
+ * weights in wire order W[cout][cin][kh][kw] fp32, bias[cout]; act 0 none,
+ * 1 ReLU, 2 PReLU with per-channel `slope` (may be NULL otherwise).
  * Output NHWC fp32 with `out_round_bf16` choosing bf16 RNE rounding.
  * Accumulates each output in double. */
 void oracle_conv2d_nhwc(const float* in, int n, int h, int w, int cin,
                         const float* weight, const float* bias, int cout, int k,
-                        int relu, int out_round_bf16, float* out);
+                        int act, const float* slope, int out_round_bf16, float* out);
 void oracle_maxpool2_nhwc(const float* in, int n, int h, int w, int c, float* out);
 
 /* ---- post-processing oracle ---- */

@@ -44,8 +44,9 @@ float oracle_bf16_round(float x) {
 
 typedef struct {
   const float* in; const double* wt; const float* bias; float* out;
-  int n, h, w, cin, cout, k, relu, rnd;
-  int next_row; /* guarded by atomic fetch-add */
+  int n, h, w, cin, cout, k, act, rnd;
+  const float* slope; /* PReLU slopes when act == 2 */
+  int next_row;       /* guarded by atomic fetch-add */
 } conv_job;
 
 static void* conv_worker(void* arg) {
@@ -76,7 +77,8 @@ static void* conv_worker(void* arg) {
       float* o = j->out + (((size_t)b * h + y) * w + x) * cout;
       for (int co = 0; co < cout; ++co) {
         float v = (float)(acc[co] + (double)j->bias[co]);
-        if (j->relu && v < 0.f) v = 0.f;
+        if (j->act == 1 && v < 0.f) v = 0.f;             /* Caffe ReLU */
+        if (j->act == 2 && v < 0.f) v = v * j->slope[co];  /* Caffe PReLU, channel-wise */
         o[co] = j->rnd ? oracle_bf16_round(v) : v;
       }
     }
@@ -87,7 +89,7 @@ static void* conv_worker(void* arg) {
 
 void oracle_conv2d_nhwc(const float* in, int n, int h, int w, int cin,
                         const float* weight, const float* bias, int cout, int k,
-                        int relu, int out_round_bf16, float* out) {
+                        int act, const float* slope, int out_round_bf16, float* out) {
   /* repack W[co][ci][r][s] -> Wt[r][s][ci][co] so the inner loop runs over co */
   double* wt = (double*)malloc(sizeof(double) * (size_t)k * k * cin * cout);
   for (int co = 0; co < cout; ++co)
@@ -96,7 +98,7 @@ void oracle_conv2d_nhwc(const float* in, int n, int h, int w, int cin,
         for (int s = 0; s < k; ++s)
           wt[(((size_t)r * k + s) * cin + ci) * cout + co] =
               (double)weight[(((size_t)co * cin + ci) * k + r) * k + s];
-  conv_job j = {in, wt, bias, out, n, h, w, cin, cout, k, relu, out_round_bf16, 0};
+  conv_job j = {in, wt, bias, out, n, h, w, cin, cout, k, act, out_round_bf16, slope, 0};
   int nt = oracle_threads();
   pthread_t th[64];
   for (int t = 0; t < nt; ++t) pthread_create(&th[t], NULL, conv_worker, &j);

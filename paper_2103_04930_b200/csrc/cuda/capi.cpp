@@ -219,7 +219,7 @@ int avec_posenet_layer_info(avec_ctx* ctx, uint64_t handle, int layer, int* cin,
     if (cout) *cout = d.cout;
     if (k) *k = d.k;
     if (level) *level = d.level;
-    if (relu) *relu = d.relu;
+    if (relu) *relu = d.act;
   });
 }
 

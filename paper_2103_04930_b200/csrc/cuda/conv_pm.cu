@@ -44,11 +44,11 @@ struct PmCfg {
   static_assert(kAccStages * kAccCols <= 512, "TMEM budget");
   static constexpr int win = 0;
   static constexpr int wgt = win + kWinStages * kWinBytes;
-  static constexpr int kWgtStages = (232448 - 1024 - 2048 - wgt) / kWgtBytes > 16
+  static constexpr int kWgtStages = (232448 - 1024 - 4352 - wgt) / kWgtBytes > 16
                                         ? 16
-                                        : (232448 - 1024 - 2048 - wgt) / kWgtBytes;
-  static constexpr int bias = wgt + kWgtStages * kWgtBytes;  // N floats per acc stage
-  static constexpr int bars = bias + kAccStages * N * 4;
+                                        : (232448 - 1024 - 4352 - wgt) / kWgtBytes;
+  static constexpr int bias = wgt + kWgtStages * kWgtBytes;  // N bias + N slope floats per acc stage
+  static constexpr int bars = bias + 2 * kAccStages * N * 4;
   static constexpr int total = bars + 256;
   static_assert(kWinBytes % 1024 == 0 && wgt % 1024 == 0, "SW128 alignment");
   static_assert(total + 1024 <= 232448, "smem budget");
@@ -216,10 +216,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const PmTile tc = pm_decode(p, t);
       const ConvGroupParams& g = p.g[tc.g];
       float* bs = sbias + acc * N;
-      // this tile's bias slice (the acc stage's previous tile finished reading it)
+      float* sl = sbias + (C::kAccStages + acc) * N;
+      // this tile's bias / PReLU-slope slices (the acc stage's previous tile
+      // finished reading them); ReLU is PReLU with slope 0, identity slope 1
       for (int i = ep; i < N; i += 128) {
         const int co = tc.nt * N + i;
         bs[i] = co < g.cout ? g.bias[co] : 0.f;
+        sl[i] = g.act == 2 && co < g.cout ? g.slope[co] : 1.f;  // identity unless PReLU
       }
       named_bar_sync(1, 128);
       mbar_wait(&acc_full[acc], aph);
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 32; ++j) {
                 if (c0 + j < c_left) {
                   float a = __uint_as_float(v[j]) + bs[c0 + j];
-                  if (g.relu) a = fmaxf(a, 0.f);
+                  a = g.act == 1 ? fmaxf(a, 0.f) : (a < 0.f ? a * sl[c0 + j] : a);
                   const int co = tc.nt * N + c0 + j;
                   if (p.out_mode == kOutNchwF32)
                     static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
@@ -269,9 +272,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 16; ++j) {
               float a = __uint_as_float(v[2 * j]) + bs[c0 + 2 * j];
               float b = __uint_as_float(v[2 * j + 1]) + bs[c0 + 2 * j + 1];
-              if (g.relu) {
+              if (g.act == 1) {
                 a = fmaxf(a, 0.f);
                 b = fmaxf(b, 0.f);
+              } else {
+                if (a < 0.f) a *= sl[c0 + 2 * j];
+                if (b < 0.f) b *= sl[c0 + 2 * j + 1];
               }
               w[j] = valid ? pack_bf16(a, b) : 0u;
             }
@@ -319,21 +325,25 @@ void configure_pm() {
 
 }  // namespace
 
-int conv_pm_subs(int n_tile) { return n_tile == 256 ? 1 : 2; }
+int conv_pm_subs(int n_tile) { return n_tile == 256 ? 1 : 2; }  // 2 acc stages fit TMEM
 
 void conv_pm_configure() {
   configure_pm<64, 2>();
+  configure_pm<96, 2>();
   configure_pm<128, 2>();
   configure_pm<256, 1>();
 }
+
+int conv_pm_tile_n(int cout) { return cout <= 64 ? 64 : cout <= 96 ? 96 : cout <= 128 ? 128 : 256; }
 
 void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
   const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
   switch (p.pm_n) {
     case 64: launch_pm<64, 2>(maps, p, grid, stream); break;
+    case 96: launch_pm<96, 2>(maps, p, grid, stream); break;
     case 128: launch_pm<128, 2>(maps, p, grid, stream); break;
     case 256: launch_pm<256, 1>(maps, p, grid, stream); break;
-    default: fail(AVEC_ERR_UNSUPPORTED, "pixel-major conv supports N tiles of 64/128/256");
+    default: fail(AVEC_ERR_UNSUPPORTED, "pixel-major conv supports N tiles of 64/96/128/256");
   }
 }
 

@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t cb = (co_local & 63) * 2;
 #pragma unroll
               for (int j = 0; j < kChunk; ++j) {
-                const float x = (mask >> j) & 1u ? activate(v[j], bias, g.relu) : 0.f;
+                const float x = (mask >> j) & 1u ? activate(v[j], bias, g.act == 1) : 0.f;
                 *reinterpret_cast<__nv_bfloat16*>(half + j * 128 + ((((cb >> 4) ^ (j & 7)) << 4) | (cb & 15))) =
                     __float2bfloat16_rn(x);
               }
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < kChunk; ++j) {
               if ((mask >> j) & 1u) {
-                const float x = activate(v[j], bias, g.relu);
+                const float x = activate(v[j], bias, g.act == 1);
                 if (p.out_mode == kOutNchwF32) {
                   static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
                                                   p.H + h) * p.W + w] = x;

@@ -63,7 +63,8 @@ struct ConvGroupParams {
   int out_c_off;       // channel offset inside the destination
   int out_c_stride;    // channels of the destination buffer (NHWC) / total channels (NCHW)
   int cout;            // real output channels written
-  int relu;
+  int act;             // 0 none, 1 ReLU, 2 PReLU (pixel-major kernel only)
+  const float* slope;  // PReLU slopes [m_tiles * 128]
 };
 
 struct ConvParams {
@@ -102,7 +103,8 @@ void conv_configure();
 void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
 // pixel-major variant (conv_pm.cu)
 void conv_pm_configure();
-int conv_pm_subs(int n_tile);  // 128-pixel M sub-tiles per tile for a channel tile
+int conv_pm_subs(int n_tile);   // 128-pixel M sub-tiles per tile for a channel tile
+int conv_pm_tile_n(int cout);   // channel tile (MMA N) for a layer's output width
 void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
 
 }  // namespace avec

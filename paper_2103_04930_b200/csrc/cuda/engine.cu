@@ -120,17 +120,6 @@ CUtensorMap make_map_3d_store(const void* base, uint64_t cols, uint64_t rows, ui
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-// internal concat layout of a stage input: [trunk 128][L1 38][L2 19][pad]
-// vs Caffe's concat order [L1, L2, trunk] (prototxt concat_stageN)
-int concat_internal_channel(const PoseFamily& f, int caffe_ci) {
-  const int branches = f.paf_channels + f.heat_channels;
-  return caffe_ci < branches ? caffe_ci + f.trunk_channels : caffe_ci - branches;
-}
-
-bool is_stage_input_layer(const ConvDef& d, const PoseFamily& f) {
-  return d.cin == f.paf_channels + f.heat_channels + f.trunk_channels;
-}
-
 // ------------------------------------------------------------------ slots
 struct SlotLease {
   avec_ctx* ctx;
@@ -251,10 +240,10 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
     L.def = f.convs[i];
     // the 3-channel first layer runs as a 1x1 conv over its 64-channel im2col
     L.exec_k = i == 0 ? 1 : L.def.k;
-    L.cin_pad = i == 0 ? 64 : round_up(L.def.cin, 64);
+    L.cin_pad = i == 0 ? 64 : L.def.cin_pad ? L.def.cin_pad : round_up(L.def.cin, 64);
     L.cout_pad = round_up(L.def.cout, 128);
     w_off[i] = take(size_t(L.cout_pad) * L.exec_k * L.exec_k * L.cin_pad * 2);
-    b_off[i] = take(size_t(L.cout_pad) * 4);
+    b_off[i] = take(size_t(L.cout_pad) * 4 * 2);  // bias, then PReLU slopes
   }
   std::vector<uint8_t> host(total, 0);
   const float* src = weights;
@@ -269,24 +258,28 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
         for (int t = 0; t < 27; ++t)  // t = ci*9 + r*3 + s, the im2col channel order
           w[size_t(co) * 64 + t] = bf16_bits(src[size_t(co) * 27 + t]);
       src += size_t(d.cout) * 27;
-      std::memcpy(host.data() + b_off[i], src, d.cout * 4);
-      src += d.cout;
-      continue;
+    } else {
+      // Caffe input channel ci -> internal channel of the layer's input window
+      if (!d.cin_map.empty() && int(d.cin_map.size()) != d.cin)
+        fail(AVEC_ERR_INVALID_MODEL, "bad input channel map for " + d.name);
+      uint16_t* w = reinterpret_cast<uint16_t*>(host.data() + w_off[i]);
+      for (int co = 0; co < d.cout; ++co)
+        for (int ci = 0; ci < d.cin; ++ci) {
+          const int cint = d.cin_map.empty() ? ci : d.cin_map[ci];
+          if (cint < 0 || cint >= L.cin_pad) fail(AVEC_ERR_INVALID_MODEL, "channel map out of range");
+          for (int r = 0; r < k; ++r)
+            for (int s = 0; s < k; ++s)
+              w[(size_t(co) * k * k + r * k + s) * L.cin_pad + cint] =
+                  bf16_bits(src[((size_t(co) * d.cin + ci) * k + r) * k + s]);
+        }
+      src += size_t(d.cout) * d.cin * k * k;
     }
-    const bool perm = is_stage_input_layer(d, f);
-    if (perm && L.cin_pad != 192) fail(AVEC_ERR_INVALID_MODEL, "stage input must pad to 192");
-    uint16_t* w = reinterpret_cast<uint16_t*>(host.data() + w_off[i]);
-    for (int co = 0; co < d.cout; ++co)
-      for (int ci = 0; ci < d.cin; ++ci) {
-        const int cint = perm ? concat_internal_channel(f, ci) : ci;
-        for (int r = 0; r < k; ++r)
-          for (int s = 0; s < k; ++s)
-            w[(size_t(co) * k * k + r * k + s) * L.cin_pad + cint] =
-                bf16_bits(src[((size_t(co) * d.cin + ci) * k + r) * k + s]);
-      }
-    src += size_t(d.cout) * d.cin * k * k;
     std::memcpy(host.data() + b_off[i], src, d.cout * 4);
     src += d.cout;
+    if (d.act == kActPrelu) {
+      std::memcpy(host.data() + b_off[i] + size_t(L.cout_pad) * 4, src, d.cout * 4);
+      src += d.cout;
+    }
   }
   check_cuda(cudaSetDevice(device), "cudaSetDevice");
   net->mem.ensure(total, device);
@@ -295,6 +288,7 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
   for (size_t i = 0; i < f.convs.size(); ++i) {
     net->layers[i].w = base + w_off[i];
     net->layers[i].bias = reinterpret_cast<float*>(base + b_off[i]);
+    net->layers[i].slope = reinterpret_cast<float*>(base + b_off[i]) + net->layers[i].cout_pad;
   }
   return net;
 }
@@ -316,14 +310,13 @@ struct PlanBuilder {
     return int(plan.bufs.size()) - 1;
   }
 
-  TensorView view(int buf, int c_off, int c, int perm = 0) {
+  TensorView view(int buf, int c_off, int c) {
     TensorView v;
     v.buf = buf;
     v.level = buf >= 0 ? plan.buf_level[buf] : 3;
     v.c_stride = buf >= 0 ? plan.buf_c[buf] : net.fam.out_channels();
     v.c_off = c_off;
     v.c = c;
-    v.concat_perm = perm;
     return v;
   }
 
@@ -352,19 +345,22 @@ struct PlanBuilder {
     p.Wp = gi.Wp();
     p.P = gi.P;
     const bool to_output = out[0].buf == -1;
-    // 64-channel slabs at 8-aligned offsets go out through TMA stores
-    bool slab = !to_output;
-    for (size_t g = 0; g < layers.size(); ++g)
-      slab = slab && net.layers[layers[g]].def.cout % 64 == 0 && out[g].c_off % 8 == 0 &&
-             out[g].level == in[g].level;
-    p.out_mode = to_output ? kOutNchwF32 : slab ? kOutTmaBf16 : kOutDirectBf16;
     // Short-K layers run pixel-major (the epilogue writes pixel rows or NCHW
     // planes directly); the long-K 7x7 stage layers run swap-AB with wide
     // tiles that share each weight k-block across 512 pixels.
     p.pixel_major = L0.exec_k != 7 ? 1 : 0;
+    // channel slabs at 8-aligned offsets take the vector / TMA-store path:
+    // 32-channel granules for pixel-major, 64-channel TMA boxes for swap-AB
+    bool slab = !to_output;
+    for (size_t g = 0; g < layers.size(); ++g)
+      slab = slab && net.layers[layers[g]].def.cout % (p.pixel_major ? 32 : 64) == 0 &&
+             out[g].c_off % 8 == 0 && out[g].level == in[g].level;
+    p.out_mode = to_output ? kOutNchwF32 : slab ? kOutTmaBf16 : kOutDirectBf16;
+    if (!p.pixel_major)
+      for (int li : layers)
+        if (net.layers[li].def.act == kActPrelu) fail(AVEC_ERR_UNSUPPORTED, "PReLU on a 7x7 layer");
     if (p.pixel_major) {
-      const int c64 = round_up(L0.def.cout, 64);
-      p.pm_n = c64 >= 256 ? 256 : c64;
+      p.pm_n = conv_pm_tile_n(L0.def.cout);
       p.subs = conv_pm_subs(p.pm_n);
       p.m_tiles = (L0.def.cout + p.pm_n - 1) / p.pm_n;
       p.tiles_per_image = (p.H * p.Wp + 128 * p.subs - 1) / (128 * p.subs);
@@ -405,7 +401,8 @@ struct PlanBuilder {
       gp.out_c_off = out[g].c_off;
       gp.out_c_stride = out[g].c_stride;
       gp.cout = L.def.cout;
-      gp.relu = L.def.relu;
+      gp.act = L.def.act;
+      gp.slope = L.slope;
       const int ib = in[g].buf;
       const uint64_t rows = uint64_t(plan.n) * gi.Hp() * gi.Wp();
       op.maps.act_big[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 256);
@@ -430,13 +427,9 @@ struct PlanBuilder {
   }
 };
 
-// COCO program (pose_deploy_linevec.prototxt) on padded-flat buffers
-void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
-  const PoseFamily& f = net.fam;
-  PlanBuilder b{plan, net, device};
-  const int nl = int(f.convs.size());
-  plan.layer_in.assign(nl, TensorView{});
-  plan.layer_out.assign(nl, TensorView{});
+// VGG-19[:10] + CPM adapters (shared by both families); conv4_4_CPM writes the
+// 128-channel trunk into `cat` at channel `trunk_off`. Returns the next layer.
+int build_trunk(PlanBuilder& b, Plan& plan, int cat, int trunk_off) {
   int li = 0;
   // level 0
   const int a0 = b.buffer(0, 64), b0 = b.buffer(0, 64), i2c = b.buffer(0, 64);
@@ -463,13 +456,25 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
   b.conv({li++}, {b.view(b2, 0, 256)}, {b.view(a2, 0, 256)});  // conv3_3
   b.conv({li++}, {b.view(a2, 0, 256)}, {b.view(b2, 0, 256)});  // conv3_4
   const int p3 = b.buffer(3, 256), a3 = b.buffer(3, 512), b3 = b.buffer(3, 512),
-            c3 = b.buffer(3, 256), cat = b.buffer(3, 192);
+            c3 = b.buffer(3, 256);
   b.pool(b2, p3);
   b.conv({li++}, {b.view(p3, 0, 256)}, {b.view(a3, 0, 512)});  // conv4_1
   b.conv({li++}, {b.view(a3, 0, 512)}, {b.view(b3, 0, 512)});  // conv4_2
   b.conv({li++}, {b.view(b3, 0, 512)}, {b.view(c3, 0, 256)});  // conv4_3_CPM
+  b.conv({li++}, {b.view(c3, 0, 256)}, {b.view(cat, trunk_off, 128)});  // conv4_4_CPM -> trunk slot
+  return li;
+}
+
+// COCO program (pose_deploy_linevec.prototxt) on padded-flat buffers
+void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
+  const PoseFamily& f = net.fam;
+  PlanBuilder b{plan, net, device};
+  const int nl = int(f.convs.size());
+  plan.layer_in.assign(nl, TensorView{});
+  plan.layer_out.assign(nl, TensorView{});
+  const int cat = b.buffer(3, 192);  // [trunk 128 | L1 38 | L2 19 | pad]
+  int li = build_trunk(b, plan, cat, 0);
   const int T = f.trunk_channels, C1 = f.paf_channels, C2 = f.heat_channels;
-  b.conv({li++}, {b.view(c3, 0, 256)}, {b.view(cat, 0, T)});   // conv4_4_CPM -> trunk slot
   // branch buffers
   const int l1a = b.buffer(3, 128), l1b = b.buffer(3, 128), l2a = b.buffer(3, 128),
             l2b = b.buffer(3, 128), l1x = b.buffer(3, 512), l2x = b.buffer(3, 512);
@@ -484,7 +489,7 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
   for (int t = 2; t <= f.stages; ++t) {
     const int s = li;  // L1: s..s+6, L2: s+7..s+13
     const int catc = T + C1 + C2;
-    b.conv({s + 0, s + 7}, {b.view(cat, 0, catc, 1), b.view(cat, 0, catc, 1)},
+    b.conv({s + 0, s + 7}, {b.view(cat, 0, catc), b.view(cat, 0, catc)},
            {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
     int x = l1a, y = l1b, u = l2a, v = l2b;
     for (int i = 1; i <= 5; ++i) {  // Mconv2..5 (7x7) then Mconv6 (1x1)
@@ -502,6 +507,43 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
     }
     li += 14;
   }
+  if (li != nl) fail(AVEC_ERR_INVALID_MODEL, "plan/layer table mismatch");
+}
+
+// BODY_25 program: 4 PAF stages then 2 heatmap stages, each 5 dense blocks of
+// three 3x3 PReLU convs concatenated in place (ping-pong X/Y buffers) + Mconv6/7.
+// Stage concat buffer: [heat 0..25 | PAF 32..83 | trunk 88..215] (netspec.hpp).
+void build_body25_plan(Plan& plan, const PoseNet& net, int device) {
+  const PoseFamily& f = net.fam;
+  PlanBuilder b{plan, net, device};
+  const int nl = int(f.convs.size());
+  plan.layer_in.assign(nl, TensorView{});
+  plan.layer_out.assign(nl, TensorView{});
+  const int cat = b.buffer(3, kB25CatChannels);
+  int li = build_trunk(b, plan, cat, kB25Trunk);
+  const int X0 = b.buffer(3, 384), Y0 = b.buffer(3, 384), m6 = b.buffer(3, 512);
+  const int P = f.paf_channels, Hc = f.heat_channels;
+  auto stage = [&](TensorView in, int w, int c6, std::vector<TensorView> heads) {
+    int X = X0, Y = Y0;
+    for (int blk = 1; blk <= 5; ++blk) {
+      b.conv({li++}, {blk == 1 ? in : b.view(X, 0, 3 * w)}, {b.view(Y, 0, w)});
+      b.conv({li++}, {b.view(Y, 0, w)}, {b.view(Y, w, w)});
+      b.conv({li++}, {b.view(Y, w, w)}, {b.view(Y, 2 * w, w)});
+      std::swap(X, Y);
+    }
+    b.conv({li++}, {b.view(X, 0, 3 * w)}, {b.view(m6, 0, c6)});  // Mconv6
+    const int head = li++;
+    for (const TensorView& o : heads) b.conv({head}, {b.view(m6, 0, c6)}, {o});  // Mconv7
+  };
+  // PAF stage 0 reads the trunk; stages 1..3 read [PAF | trunk] = window [32, 224)
+  stage(b.view(cat, kB25Trunk, 128), 96, 256, {b.view(cat, kB25Paf, P)});
+  for (int t = 1; t <= 3; ++t) {
+    std::vector<TensorView> heads{b.view(cat, kB25Paf, P)};
+    if (t == 3) heads.push_back(b.view(-1, Hc, P));  // final PAFs also go out on the wire (fp32)
+    stage(b.view(cat, kB25Paf, 192), 128, 512, heads);
+  }
+  stage(b.view(cat, kB25Paf, 192), 96, 256, {b.view(cat, kB25Heat, Hc)});  // heat stage 0
+  stage(b.view(cat, 0, 256), 128, 512, {b.view(-1, 0, Hc)});               // heat stage 1
   if (li != nl) fail(AVEC_ERR_INVALID_MODEL, "plan/layer table mismatch");
 }
 
@@ -543,7 +585,10 @@ Plan* get_plan(avec_ctx* ctx, Slot* slot, const Model& m, int n_img, int H, int 
   plan->out_elems = uint64_t(n_img) * m.net->fam.out_channels() * (H / 8) * (W / 8);
   plan->in.ensure(plan->in_elems * 4, ctx->device);
   plan->out.ensure(plan->out_elems * 4, ctx->device);
-  build_coco_plan(*plan, *m.net, ctx->device);
+  if (m.net->fam.body25())
+    build_body25_plan(*plan, *m.net, ctx->device);
+  else
+    build_coco_plan(*plan, *m.net, ctx->device);
   // capture the whole op sequence once; replays cost one launch
   cudaGraph_t g = nullptr;
   check_cuda(cudaStreamBeginCapture(slot->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
@@ -853,7 +898,8 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
     if (plan->ops[i].layers[0] == layer || plan->ops[i].layers[1] == layer) last = i + 1;
   run_ops(ctx, *plan, *m.net, 0, last, s->stream);
   check_cuda(cudaStreamSynchronize(s->stream), "layer io sync");
-  auto fetch = [&](const TensorView& v, int cdim, float* dst) {
+  // `map`: Caffe channel -> channel inside the view's window (stage inputs)
+  auto fetch = [&](const TensorView& v, int cdim, float* dst, const std::vector<int>& map) {
     const Geometry& g = plan->geo[d.level];
     if (v.buf == -2) {  // network input as the first layer sees it: bf16(x - 0.5), NHWC
       for (int b = 0; b < n_img; ++b)
@@ -876,8 +922,8 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
                   all[((size_t(b) * C + v.c_off + ch) * Hl + y) * Wl + x];
       return;
     }
-    const int grab = v.concat_perm ? v.c_stride : v.c;
-    const int off = v.concat_perm ? 0 : v.c_off;
+    const int off = v.c_off;
+    const int grab = map.empty() ? v.c : v.c_stride - v.c_off;
     DevMem tmp;
     tmp.ensure(size_t(n_img) * Hl * Wl * grab * 4, ctx->device);
     launch_unpad_to_f32(plan->bufs[v.buf]->p, n_img, Hl, Wl, g.P, v.c_stride, off, grab,
@@ -887,12 +933,12 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
     check_cuda(cudaStreamSynchronize(s->stream), "sync");
     for (size_t p = 0; p < size_t(n_img) * Hl * Wl; ++p)
       for (int ch = 0; ch < cdim; ++ch) {
-        const int src_ch = v.concat_perm ? concat_internal_channel(f, ch) : ch;
+        const int src_ch = map.empty() ? ch : map[ch];
         dst[p * cdim + ch] = hostv[p * grab + src_ch];
       }
   };
-  fetch(plan->layer_in[layer], d.cin, layer_in);
-  fetch(plan->layer_out[layer], d.cout, layer_out);
+  fetch(plan->layer_in[layer], d.cin, layer_in, layer == 0 ? std::vector<int>{} : d.cin_map);
+  fetch(plan->layer_out[layer], d.cout, layer_out, {});
 }
 
 }  // namespace avec

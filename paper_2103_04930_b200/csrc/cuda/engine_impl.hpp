@@ -48,8 +48,9 @@ struct ConvLayerDev {
   ConvDef def;
   int exec_k = 0;  // filter size as executed (the first layer runs 1x1 over its im2col)
   int cin_pad = 0, cout_pad = 0;
-  void* w = nullptr;      // bf16 [cout_pad][k*k][cin_pad]
-  float* bias = nullptr;  // [cout_pad]
+  void* w = nullptr;       // bf16 [cout_pad][k*k][cin_pad]
+  float* bias = nullptr;   // [cout_pad]
+  float* slope = nullptr;  // [cout_pad] PReLU slopes (zeros unless act == prelu)
 };
 
 struct PoseNet {
@@ -69,7 +70,6 @@ struct TensorView {
   int buf = -1;  // index into Plan::bufs; -1 = plan output (fp32 NCHW), -2 = plan input
   int level = 0;
   int c_stride = 0, c_off = 0, c = 0;
-  int concat_perm = 0;  // 1: channels are the internal concat layout of a stage input
 };
 
 struct PlanOp {

@@ -37,7 +37,7 @@ def lib():
         L.oracle_synth_blobs.argtypes = [u64, u8p, ctypes.c_size_t, u8p, ctypes.c_size_t]
         L.oracle_bf16_round.argtypes = [ctypes.c_float]
         L.oracle_bf16_round.restype = ctypes.c_float
-        L.oracle_conv2d_nhwc.argtypes = [f32p, i, i, i, i, f32p, f32p, i, i, i, i, f32p]
+        L.oracle_conv2d_nhwc.argtypes = [f32p, i, i, i, i, f32p, f32p, i, i, i, f32p, i, f32p]
         L.oracle_maxpool2_nhwc.argtypes = [f32p, i, i, i, i, f32p]
         L.oracle_upsample_plane.argtypes = [f32p, i, i, i, f32p]
         L.oracle_nms_plane.argtypes = [f32p, i, i, ctypes.c_float, i, i32p, f32p, f32p]
@@ -105,14 +105,21 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
     return r.view(np.float32).reshape(a.shape)
 
 
-def conv2d_nhwc(x: np.ndarray, w: np.ndarray, b: np.ndarray, relu: bool, round_bf16: bool) -> np.ndarray:
+def conv2d_nhwc(x: np.ndarray, w: np.ndarray, b: np.ndarray, relu, round_bf16: bool,
+                slope: np.ndarray = None) -> np.ndarray:
+    """`relu`: activation code 0 none / 1 ReLU / 2 PReLU (bool True = ReLU);
+    PReLU takes the per-channel `slope`."""
     n, h, wd, cin = x.shape
     cout, cin2, k, _ = w.shape
     assert cin == cin2
+    act = int(relu)
+    if act == 2 and slope is None:
+        raise ValueError("PReLU needs slopes")
+    sl = np.ascontiguousarray(slope if slope is not None else np.zeros(cout), np.float32)
     out = np.empty((n, h, wd, cout), np.float32)
     lib().oracle_conv2d_nhwc(np.ascontiguousarray(x, np.float32), n, h, wd, cin,
                              np.ascontiguousarray(w, np.float32), np.ascontiguousarray(b, np.float32),
-                             cout, k, int(relu), int(round_bf16), out)
+                             cout, k, act, sl, int(round_bf16), out)
     return out
 
 

@@ -1,0 +1,79 @@
+"""GPU parity of the BODY_25 family (PReLU, dense blocks, 4 PAF + 2 heatmap
+stages) against the CPU oracle — same tolerances as tests/test_gpu_posenet.py:
+per layer ||gpu-oracle||/||oracle|| <= 1e-3 and every element within one bf16
+ulp + 1e-4*max|oracle| (intermediate layers); fp32 outputs to 1e-3 relative."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+H, W, NB = 64, 96, 2
+
+
+@pytest.fixture(scope="module")
+def b25():
+    from paper_2103_04930_b200 import B200Backend, Dims, Frame, make_model, netspec, synth_posenet_weights
+    be = B200Backend(0)
+    s = netspec.spec("openpose_body25")
+    h = be.register_model(make_model("body25", s, b"", netspec.BODY25_DIVISOR))
+    layers = netspec.body25_layers()
+    wb = [(O.bf16_round(w), b, sl) for w, b, sl in netspec.split_weights(layers, synth_posenet_weights(s))]
+    frame = Frame(Dims(1, 3 * NB, H, W), O.batched_frame(W, H, NB, seed=3))
+    yield dict(be=be, h=h, layers=layers, wb=wb, frame=frame)
+    be.close()
+
+
+def ulp_bf16(x):
+    x = np.abs(x).astype(np.float32)
+    return np.exp2(np.floor(np.log2(np.maximum(x, 1e-30))) - 7)
+
+
+def test_layer_table(b25):
+    from paper_2103_04930_b200 import netspec
+    assert b25["be"].num_layers(b25["h"]) == 114
+    assert netspec.macs_per_pixel(b25["layers"]) == 594970
+
+
+def test_output_size_and_law(b25):
+    be, h = b25["be"], b25["h"]
+    out = be.forward(h, b25["frame"]).data
+    assert out.size == NB * 78 * (H // 8) * (W // 8)
+    assert np.isfinite(out).all()
+
+
+def test_all_layers_parity(b25):
+    be, h, layers = b25["be"], b25["h"], b25["layers"]
+    finals = {i for i, L in enumerate(layers) if L.name in ("Mconv7_stage3_L2", "Mconv7_stage1_L1")}
+    for i, L in enumerate(layers):
+        lin, lout = be.layer_io(h, b25["frame"], i)
+        w, b, sl = b25["wb"][i]
+        final = i in finals
+        ref = O.conv2d_nhwc(lin, w, b, relu=L.act, round_bf16=not final, slope=sl)
+        err = np.linalg.norm(lout - ref) / max(np.linalg.norm(ref), 1e-30)
+        assert err <= 1e-3, (L.name, err)
+        if not final:
+            tol = ulp_bf16(ref) + 1e-4 * float(np.abs(ref).max())
+            assert not (np.abs(lout - ref) > tol).any(), L.name
+
+
+def test_wire_layout_heat_then_paf(b25):
+    be, h = b25["be"], b25["h"]
+    out = be.forward(h, b25["frame"]).data.reshape(NB, 78, H // 8, W // 8)
+    names = [L.name for L in b25["layers"]]
+    _, heat = be.layer_io(h, b25["frame"], names.index("Mconv7_stage1_L1"))
+    _, paf = be.layer_io(h, b25["frame"], names.index("Mconv7_stage3_L2"))
+    assert np.array_equal(out[:, :26], heat.transpose(0, 3, 1, 2))
+    assert np.array_equal(out[:, 26:], paf.transpose(0, 3, 1, 2))
+
+
+def test_split_batch_equals_whole(b25):
+    """Frame groups (the multi-GPU split) give the same bits as one batch."""
+    from paper_2103_04930_b200 import Dims, Frame
+    be, h = b25["be"], b25["h"]
+    whole = be.forward(h, b25["frame"]).data.reshape(NB, -1)
+    per = b25["frame"].data.reshape(NB, -1)
+    for i in range(NB):
+        one = be.forward(h, Frame(Dims(1, 3, H, W), per[i])).data
+        assert one.tobytes() == whole[i].tobytes()

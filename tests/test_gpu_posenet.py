@@ -29,7 +29,7 @@ def net():
     h = be.register_model(model)
     blob = synth_posenet_weights(s)
     layers = netspec.coco_layers()
-    wb = [(O.bf16_round(w), b) for w, b in netspec.split_weights(layers, blob)]
+    wb = [(O.bf16_round(w), b, sl) for w, b, sl in netspec.split_weights(layers, blob)]
     frame = O.batched_frame(W, H, NB, seed=7)
     yield dict(be=be, h=h, layers=layers, wb=wb, frame=Frame(Dims(1, 3 * NB, H, W), frame), blob=blob)
     be.close()
@@ -45,9 +45,9 @@ def check_layer(net, i):
     be, h = net["be"], net["h"]
     L = net["layers"][i]
     lin, lout = be.layer_io(h, net["frame"], i)
-    w, b = net["wb"][i]
-    final = L.name.startswith("Mconv7") and L.name.find("stage6") >= 0
-    ref = O.conv2d_nhwc(lin, w, b, relu=bool(L.relu), round_bf16=not final)
+    w, b, sl = net["wb"][i]
+    final = i in net.get("final_layers", ()) or (L.name.startswith("Mconv7") and "stage6" in L.name)
+    ref = O.conv2d_nhwc(lin, w, b, relu=L.act, round_bf16=not final, slope=sl)
     err = np.linalg.norm(lout - ref) / max(np.linalg.norm(ref), 1e-30)
     assert err <= 1e-3, (L.name, err)
     if not final:
@@ -114,8 +114,8 @@ def test_end_to_end_against_oracle_chain(net):
     cur = x
     i = 0
     def conv(t, idx, final=False):
-        w, b = wb[idx]
-        return O.conv2d_nhwc(t, w, b, relu=bool(layers[idx].relu), round_bf16=not final)
+        w, b, _ = wb[idx]
+        return O.conv2d_nhwc(t, w, b, relu=layers[idx].act, round_bf16=not final)
     cur = conv(cur, 0); cur = conv(cur, 1); cur = O.maxpool2_nhwc(cur)
     cur = conv(cur, 2); cur = conv(cur, 3); cur = O.maxpool2_nhwc(cur)
     for j in (4, 5, 6, 7):
