@@ -37,8 +37,18 @@ import time
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-W, H, BATCH = 656, 368, 8
 METRIC = "OpenPose frames/sec through AVEC server at 1/2/4/8 B200; conv tensor-pipe %"
+# BASELINE.json configs[1] (C2, default) and configs[4] (C5)
+CONFIGS = {
+    "c2": dict(family="openpose_coco", divisor=192.0 / 57.0, width=656, height=368, global_batch=8,
+               per_gpu_batch=True, scaling="weak",
+               workload="C2: OpenPose COCO pose net, 656x368 frames, batch 8 per GPU"),
+    "c5": dict(family="openpose_body25", divisor=192.0 / 78.0, width=1312, height=736, global_batch=32,
+               per_gpu_batch=False, scaling="strong",
+               workload="C5: OpenPose BODY_25 1312x736, batch 32 sharded across the GPUs"),
+}
+CFG = CONFIGS["c2"]
+W, H, BATCH = CFG["width"], CFG["height"], CFG["global_batch"]  # BATCH = frames per rank per step
 
 
 def load_peaks() -> dict:
@@ -92,7 +102,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def run_reference_arm(steps: int, warmup: int, width=W, height=H, batch=BATCH, clients=1) -> dict:
+def run_reference_arm(steps: int, warmup: int, width=None, height=None, batch=None, clients=1) -> dict:
+    width, height = width or W, height or H
+    batch = batch or CFG["global_batch"]
     exe = ROOT / "oracle" / "_ref" / "ref_arm"
     if not exe.exists():
         return {"ok": False, "error": f"{exe} not built"}
@@ -113,15 +125,16 @@ def reference_main(args, rank: int, world: int) -> int:
         print(json.dumps({"impl": "reference", "unavailable": r.get("error", "ref_arm failed")}))
         return 0
     fps = r["fps"]
+    gb = CFG["global_batch"]
     sample = (f"reference accelfwd Server+MockPoseBackend via Session over TCP loopback, "
-              f"{args.steps} cycles of {BATCH}x{W}x{H} frames (reference emulates OpenPose with segment means)")
+              f"{args.steps} cycles of {gb}x{W}x{H} frames (reference emulates OpenPose with segment means)")
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_cycle"],
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": CFG["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference harness gen_frame, seed 7)",
-        "config": {"workload": "C2: OpenPose COCO 656x368 batch 8 (reference path: MockPose segment means)",
-                   "global_batch": BATCH, "parallelism": "cpu, FIFO single backend thread"},
+        "config": {"workload": CFG["workload"] + " (reference path: MockPose segment means)",
+                   "global_batch": gb, "parallelism": "cpu, FIFO single backend thread"},
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": 1, "kind": "reference", "sample": sample},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -145,7 +158,7 @@ def cpu_posenet_oracle_sample() -> dict:
     O.conv2d_nhwc(x, w, b, relu=True, round_bf16=True)
     dt = time.perf_counter() - t0
     fl = 2.0 * (H // 8) * (W // 8) * 128 * 128 * 49
-    per_frame = netspec.flops_per_frame(netspec.coco_layers(), H, W)
+    per_frame = netspec.flops_per_frame(netspec.layers_for(CFG["family"]), H, W)
     return {"gflops": fl / dt / 1e9, "fps_extrapolated": (fl / dt) / per_frame,
             "cores": O.lib().oracle_threads(), "seconds": dt}
 
@@ -162,9 +175,10 @@ def wire_run(device: int, steps: int, clients: int) -> dict:
         if not line.startswith("listening on"):
             return {"ok": False, "error": "server did not start: " + line + p.stderr.read()[-300:]}
         ep = line.split()[2]
+        model = "posenet-body25" if CFG["family"] == "openpose_body25" else "posenet"
         r = subprocess.run([str(loadgen), "--endpoint", ep, "--clients", str(clients), "--steps", str(steps),
-                            "--warmup", "3", "--batch", str(BATCH), "--width", str(W), "--height", str(H)],
-                           capture_output=True, text=True, timeout=900)
+                            "--warmup", "2", "--batch", str(BATCH), "--width", str(W), "--height", str(H),
+                            "--model", model], capture_output=True, text=True, timeout=900)
         out = json.loads(r.stdout.strip().splitlines()[-1])
         out["transport"] = "TCP loopback, native client (bin/avec-loadgen), avec-server --slots 2"
         return out
@@ -188,16 +202,18 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     dev = local_rank
     torch.cuda.set_device(dev)
     be = B200Backend(dev, slots=2)
-    model = make_model("openpose_coco", netspec.spec(), b"", netspec.COCO_DIVISOR)
+    model = make_model(CFG["family"], netspec.spec(CFG["family"]), b"", CFG["divisor"])
     h = be.register_model(model)
     dims = Dims(1, 3 * BATCH, H, W)
     E, K = dims.elem_count(), be.output_elems(h, dims)
 
-    # synthetic frames: the reference's generator (seed 7), distinct per rank and
-    # per rotating input buffer so consecutive steps never reuse an input
-    import oracle_lib as O
+    # synthetic frames with the harness's value distribution (U[0,1) on a 2^-24
+    # grid, harness.cpp:29-42), distinct per rank and per rotating input buffer
+    # so consecutive steps never reuse an input
     n_rot = 4
-    host_frames = [O.batched_frame(W, H, BATCH, seed=7, first=(rank * n_rot + i) * BATCH) for i in range(n_rot)]
+    rng = np.random.default_rng(7 + 1000 * rank)
+    host_frames = [(rng.integers(0, 1 << 24, E, dtype=np.int64) * (1.0 / (1 << 24))).astype(np.float32)
+                   for _ in range(n_rot)]
     d_in = [torch.from_numpy(f).to(f"cuda:{dev}") for f in host_frames]
     d_out = [torch.empty(K, dtype=torch.float32, device=f"cuda:{dev}") for _ in range(2)]
     # two cycles in flight, like the server's two execution slots
@@ -289,8 +305,11 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     prof = be.profile(h, dims, d_in[0].data_ptr(), reps=3)
     peaks = load_peaks()
     step_ms_prof = sum(p["ms"] for p in prof)
-    # dominant kernel: the swap-AB 7x7 stage conv (conv_tc_kernel<2>), ~55% of the step
-    dom = [p for p in prof if p["kind"] == "conv_tc"]
+    # dominant kernel = the conv variant with the largest share of the step:
+    # COCO: the swap-AB 7x7 stage conv (conv_tc_kernel<2>); BODY_25: pixel-major
+    share = {k: sum(p["ms"] for p in prof if p["kind"] == k) for k in ("conv_tc", "conv_pm")}
+    dom_kind = max(share, key=share.get)
+    dom = [p for p in prof if p["kind"] == dom_kind]
     dom_fl = sum(p["flops"] for p in dom) / max(len(dom), 1)   # per launch
     dom_ms = sum(p["ms"] for p in dom) / max(len(dom), 1)      # mean launch duration
     dom_tf = dom_fl / (dom_ms / 1e3) / 1e12
@@ -298,15 +317,17 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     all_fl, all_ms = sum(p["flops"] for p in allc), sum(p["ms"] for p in allc)
     traffic = None
     tp = ROOT / "profiles" / "conv_traffic.json"
-    if tp.exists():
+    if tp.exists() and args.config == "c2":  # ncu capture of the C2 dominant kernel
         try:
             traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
         except Exception:
             pass
-    net_fl = netspec.flops_per_frame(netspec.coco_layers(), H, W)
+    net_fl = netspec.flops_per_frame(netspec.layers_for(CFG["family"]), H, W)
+    kernel_name = {"conv_tc": "conv_tc_kernel<2>: tcgen05 swap-AB 7x7 stage conv (L1+L2 branch pair per launch)",
+                   "conv_pm": "conv_pm_kernel<N,S>: tcgen05 pixel-major conv (all launches of the class)"}
     roofline = {
         "bound": "tensor",
-        "kernel": "conv_tc_kernel<2>: tcgen05 swap-AB 7x7 stage conv (L1+L2 branch pair per launch)",
+        "kernel": kernel_name[dom_kind],
         "achieved": round(dom_tf, 1), "peak": peaks["bf16_sust"], "unit": "TFLOP/s",
         "frac": round(dom_tf / peaks["bf16_sust"], 4), "traffic": traffic,
         "peak_kind": f"{peaks['src']} sustained bf16 (kernel timed inside a long step)",
@@ -326,7 +347,8 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
         breakdown[k]["launches"] += 1
 
     if rank == 0:
-        ref = run_reference_arm(steps=120, warmup=3) if world == 1 else {"ok": False, "error": "rank0 N>1"}
+        ref_cycles = 120 if args.config == "c2" else 3  # ~10 s of reference CPU work either way
+        ref = run_reference_arm(steps=ref_cycles, warmup=1) if world == 1 else {"ok": False, "error": "rank0 N>1"}
         try:
             port = cpu_posenet_oracle_sample() if world == 1 else None
         except Exception as e:  # noqa: BLE001
@@ -334,17 +356,19 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
         cpu = None
         if ref.get("ok"):
             cpu = {"value": ref["fps"], "unit": "frames/s", "cores": 1, "kind": "reference",
-                   "sample": "reference Server+MockPoseBackend via Session over TCP loopback, 120 cycles of "
-                             "8x656x368 (the reference emulates OpenPose with segment means)",
+                   "sample": f"reference Server+MockPoseBackend via Session over TCP loopback, {ref_cycles} cycles "
+                             f"of {CFG['global_batch']}x{W}x{H} (the reference emulates OpenPose with segment means)",
                    "posenet_oracle_port": port}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic frames (reference gen_frame, seed 7), random-init He-uniform weights (seed 1)",
-            "config": {"workload": "C2: OpenPose COCO pose net, 656x368 frames, batch 8 per GPU",
-                       "global_batch": BATCH * world, "frame": f"{W}x{H}", "parallelism": f"frame groups x{world}",
-                       "l2": "4 rotating input buffers; per-step activation working set ~1.4 GB >> 126 MB L2"},
+            "higher_is_better": True, "scaling": CFG["scaling"], "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic frames (harness distribution U[0,1) on a 2^-24 grid), random-init He-uniform "
+                    "weights (seed 1)",
+            "config": {"workload": CFG["workload"], "family": CFG["family"],
+                       "global_batch": BATCH * world, "frame": f"{W}x{H}", "frames_per_gpu": BATCH,
+                       "parallelism": f"frame groups x{world}",
+                       "l2": "4 rotating input buffers; per-step activation working set >> 126 MB L2"},
             "e2e": {"value": round(e2e, 2), "unit": "frames/s", "h2d_bytes_per_step": E * 4,
                     "d2h_bytes_per_step": K * 4,
                     "api": f"avec_forward (pinned host buffers), {e2e_threads} host thread(s) over 2 slots",
@@ -367,11 +391,23 @@ def main() -> int:
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    global CFG, W, H, BATCH
+    CFG = CONFIGS[args.config]
+    W, H = CFG["width"], CFG["height"]
+    if CFG["per_gpu_batch"]:
+        BATCH = CFG["global_batch"]  # weak scaling: every GPU runs its own batch
+    else:
+        if CFG["global_batch"] % world:
+            raise SystemExit(f"{args.config}: global batch {CFG['global_batch']} does not split over {world} GPUs")
+        BATCH = CFG["global_batch"] // world  # strong scaling: one batch sharded into frame groups
+    if args.config == "c5" and args.steps == 200:
+        args.steps = 20  # 32 frames of 1312x736 per step: keep the default run within minutes
     if args.impl == "reference":
         return reference_main(args, rank, world)
     if world > 1:

@@ -109,9 +109,11 @@ struct WorkIter {
   }
 };
 
-__device__ __forceinline__ float activate(uint32_t bits, float bias, int relu) {
-  float x = __uint_as_float(bits) + bias;
-  return relu ? fmaxf(x, 0.f) : x;
+// Branch-free activation: max(x,0) + neg*min(x,0) with neg = 1 (none),
+// 0 (ReLU, +0 for negatives) or the channel's PReLU slope (lane = channel).
+__device__ __forceinline__ float activate(uint32_t bits, float bias, float neg) {
+  const float x = __uint_as_float(bits) + bias;
+  return fmaxf(x, 0.f) + neg * fminf(x, 0.f);
 }
 
 template <int SUBS>
@@ -277,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cout_m = min(kTileM, g.cout - tc.mt * kTileM);  // channels of this m-tile
       const bool live = co_local < cout_m;
       const float bias = live ? g.bias[co] : 0.f;
+      const float neg = g.act == 1 ? 0.f : (live && g.act == 2) ? g.slope[co] : 1.f;
       mbar_wait(&acc_full[acc], aph);
       tc_fence_after();
       for (int sub = 0; sub < SUBS; ++sub) {
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t cb = (co_local & 63) * 2;
 #pragma unroll
               for (int j = 0; j < kChunk; ++j) {
-                const float x = (mask >> j) & 1u ? activate(v[j], bias, g.act == 1) : 0.f;
+                const float x = (mask >> j) & 1u ? activate(v[j], bias, neg) : 0.f;
                 *reinterpret_cast<__nv_bfloat16*>(half + j * 128 + ((((cb >> 4) ^ (j & 7)) << 4) | (cb & 15))) =
                     __float2bfloat16_rn(x);
               }
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < kChunk; ++j) {
               if ((mask >> j) & 1u) {
-                const float x = activate(v[j], bias, g.act == 1);
+                const float x = activate(v[j], bias, neg);
                 if (p.out_mode == kOutNchwF32) {
                   static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
                                                   p.H + h) * p.W + w] = x;

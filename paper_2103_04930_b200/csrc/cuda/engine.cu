@@ -345,10 +345,23 @@ struct PlanBuilder {
     p.Wp = gi.Wp();
     p.P = gi.P;
     const bool to_output = out[0].buf == -1;
-    // Short-K layers run pixel-major (the epilogue writes pixel rows or NCHW
-    // planes directly); the long-K 7x7 stage layers run swap-AB with wide
-    // tiles that share each weight k-block across 512 pixels.
-    p.pixel_major = L0.exec_k != 7 ? 1 : 0;
+    // Kernel choice (measured): swap-AB (M = 128 Cout,
+    // N = 256-pixel MMAs, 96 B/clk of smem operand reads) for the 7x7 layers
+    // and for 3x3 layers with exactly 128 output channels; pixel-major
+    // (M = 128 pixels, N = Cout) elsewhere — with N = 256 it is as lean, with
+    // N <= 128 it hits the 128 B/clk operand-read ceiling, but it is the only
+    // sensible tile for 64-channel and thin-head outputs and its direct-store
+    // epilogue suits the short-K, high-resolution layers.
+    static const int tc3 = [] {
+      const char* e = std::getenv("AVEC_TC3");
+      return e ? std::atoi(e) : 0;
+    }();
+    const bool want_tc = L0.exec_k == 7 || (tc3 && L0.exec_k == 3 && L0.def.cout == 128 && L0.cin_pad >= 128);
+    bool tc_ok = want_tc && !to_output;
+    for (size_t g = 0; g < layers.size(); ++g)
+      tc_ok = tc_ok && out[g].c_off % 8 == 0 && out[g].level == in[g].level;
+    p.pixel_major = tc_ok ? 0 : 1;
+    if (L0.exec_k == 7 && p.pixel_major) fail(AVEC_ERR_UNSUPPORTED, "7x7 layer needs the swap-AB kernel");
     // channel slabs at 8-aligned offsets take the vector / TMA-store path:
     // 32-channel granules for pixel-major, 64-channel TMA boxes for swap-AB
     bool slab = !to_output;
@@ -356,9 +369,6 @@ struct PlanBuilder {
       slab = slab && net.layers[layers[g]].def.cout % (p.pixel_major ? 32 : 64) == 0 &&
              out[g].c_off % 8 == 0 && out[g].level == in[g].level;
     p.out_mode = to_output ? kOutNchwF32 : slab ? kOutTmaBf16 : kOutDirectBf16;
-    if (!p.pixel_major)
-      for (int li : layers)
-        if (net.layers[li].def.act == kActPrelu) fail(AVEC_ERR_UNSUPPORTED, "PReLU on a 7x7 layer");
     if (p.pixel_major) {
       p.pm_n = conv_pm_tile_n(L0.def.cout);
       p.subs = conv_pm_subs(p.pm_n);
@@ -366,8 +376,11 @@ struct PlanBuilder {
       p.tiles_per_image = (p.H * p.Wp + 128 * p.subs - 1) / (128 * p.subs);
     } else {
       p.pm_n = 0;
-      p.subs = L0.exec_k == 7 ? 2 : 1;
       p.m_tiles = L0.cout_pad / 128;
+      // 512-pixel tiles share each weight k-block across two MMAs; fall back to
+      // 256-pixel tiles (double-buffered TMEM) when that leaves SMs idle
+      const int wide = int(layers.size()) * plan.n * ((p.H * p.Wp + 511) / 512) * p.m_tiles;
+      p.subs = (L0.exec_k == 7 || tc3 == 3 || (tc3 == 1 && wide >= 2 * 148)) ? 2 : 1;
       p.tiles_per_image = (p.H * p.Wp + 256 * p.subs - 1) / (256 * p.subs);
     }
     p.n_groups = int(layers.size());

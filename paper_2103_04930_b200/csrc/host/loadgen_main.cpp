@@ -56,6 +56,9 @@ int main(int argc, char** argv) {
   if (model == "posenet") {
     std::string s = "avecnet 1\nfamily openpose_coco\ninit he_uniform 1\n";
     md = wire::make_model("openpose_coco", {s.begin(), s.end()}, {}, 192.0 / 57.0);
+  } else if (model == "posenet-body25") {
+    std::string s = "avecnet 1\nfamily openpose_body25\ninit he_uniform 1\n";
+    md = wire::make_model("openpose_body25", {s.begin(), s.end()}, {}, 192.0 / 78.0);
   } else {
     // the reference's model: opaque structure -> segment means; "mockpose-c1"
     // (divisor 1) returns as many floats as it receives (memcpy sweep, C3)
