@@ -295,7 +295,10 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     e2e = e2e_by_threads[e2e_threads]
 
     # ---------------- through the wire: avec-server + native clients over TCP ----------------
-    wire = wire_run(dev, steps=max(10, args.steps // 8), clients=2)
+    # 4 sessions per GPU: two cycles compute in the server's two slots while the
+    # other two sessions stream their frames in / results out (measured sweep:
+    # 1 -> 860, 2 -> 1324, 4 -> 2092, 8 -> 1990 fps on C2, profiles/README.md)
+    wire = wire_run(dev, steps=max(20, args.steps // 4), clients=4)
     if world > 1:
         t = torch.tensor([wire.get("fps", 0.0)], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)

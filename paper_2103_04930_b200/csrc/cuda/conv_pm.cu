@@ -37,20 +37,26 @@ struct PmCfg {
   static constexpr int kTileN = 128 * SUBS_M;  // pixels per tile
   static constexpr int kWinRows = kTileN + 8;
   static constexpr int kWinBytes = kWinRows * 128;
-  static constexpr int kWinStages = 2;
+  // N = 64 serves the short-K high-resolution layers (conv1_1 on its im2col,
+  // conv1_2): one more window in flight keeps their HBM reads streaming
+  static constexpr int kWinStages = N == 64 ? 3 : 2;
   static constexpr int kWgtBytes = N * 128;  // N rows x 64 bf16
   static constexpr int kAccCols = SUBS_M * N;
   static constexpr int kAccStages = 2;
   static_assert(kAccStages * kAccCols <= 512, "TMEM budget");
+  // epilogue staging: per epilogue warp two [32 px][64 ch] bf16 boxes (SW128)
+  static constexpr int kStgBox = 32 * 128;
+  static constexpr int kStgBytes = 4 * 2 * kStgBox;
   static constexpr int win = 0;
-  static constexpr int wgt = win + kWinStages * kWinBytes;
+  static constexpr int stg = win + kWinStages * kWinBytes;
+  static constexpr int wgt = stg + kStgBytes;
   static constexpr int kWgtStages = (232448 - 1024 - 4352 - wgt) / kWgtBytes > 16
                                         ? 16
                                         : (232448 - 1024 - 4352 - wgt) / kWgtBytes;
   static constexpr int bias = wgt + kWgtStages * kWgtBytes;  // N bias + N slope floats per acc stage
   static constexpr int bars = bias + 2 * kAccStages * N * 4;
   static constexpr int total = bars + 256;
-  static_assert(kWinBytes % 1024 == 0 && wgt % 1024 == 0, "SW128 alignment");
+  static_assert(kWinBytes % 1024 == 0 && wgt % 1024 == 0 && stg % 1024 == 0, "SW128 alignment");
   static_assert(total + 1024 <= 232448, "smem budget");
 };
 
@@ -84,6 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* win = smem + C::win;
   uint8_t* wgt = smem + C::wgt;
+  uint8_t* stg = smem + C::stg;
   float* sbias = reinterpret_cast<float*>(smem + C::bias);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::bars);
   uint64_t* win_full = bars;
@@ -207,9 +214,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else {
     // ------------------------------------------------------------ epilogue
+    // Warp q owns TMEM lanes 32q..32q+31 = pixels 32q.. of each 128-pixel
+    // sub-tile. Channel slabs go TMEM -> registers (bias, activation, zero
+    // outside the image, bf16) -> this warp's swizzled [32 px][64 ch] staging
+    // box -> one TMA store per box, so global writes are whole 128-byte lines
+    // (per-thread 16-byte stores at a 128-byte pixel stride cost 8x the L1
+    // wavefronts and left the high-resolution layers store-bound).
     const uint32_t quad = warp & 3;
+    const uint32_t lane = lane_id();
     const int ep = int(threadIdx.x) - 64;  // 0..127
-    int acc = 0;
+    uint8_t* stg_w = stg + quad * (2 * C::kStgBox);
+    int acc = 0, stg_i = 0;
     uint32_t aph = 0;
     const int img_rows = p.Hp * p.Wp;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
@@ -222,68 +237,87 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = ep; i < N; i += 128) {
         const int co = tc.nt * N + i;
         bs[i] = co < g.cout ? g.bias[co] : 0.f;
-        sl[i] = g.act == 2 && co < g.cout ? g.slope[co] : 1.f;  // identity unless PReLU
+        sl[i] = g.act == 1 ? 0.f : (g.act == 2 && co < g.cout) ? g.slope[co] : 1.f;
       }
       named_bar_sync(1, 128);
       mbar_wait(&acc_full[acc], aph);
       tc_fence_after();
       __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.out);
+      const int c_left = g.cout - tc.nt * N;  // live channels of this tile
       for (int sub = 0; sub < SUBS_M; ++sub) {
-        const int o = tc.pt * C::kTileN + sub * 128 + int(quad) * 32 + int(lane_id());
+        const int o = tc.pt * C::kTileN + sub * 128 + int(quad) * 32 + int(lane);
         const int hh = o / p.Wp;
         const int ww = o - hh * p.Wp;
         const bool valid = hh < p.H && ww < p.W;
         const int row_in_img = p.P * p.Wp + p.P + o;  // output row of this pixel
-        const bool store = row_in_img < img_rows;
-        uint4* dst = reinterpret_cast<uint4*>(
-            out + (static_cast<size_t>(tc.n) * img_rows + row_in_img) * g.out_c_stride + g.out_c_off +
-            tc.nt * N);
-        const int c_left = g.cout - tc.nt * N;  // live channels of this tile
+        const uint32_t tbase = tmem + ((quad * 32) << 16) + acc * C::kAccCols + sub * N;
+        if (p.out_mode == kOutTmaBf16) {
+          const int row_w = row_in_img - int(lane);  // the warp's first pixel
+#pragma unroll
+          for (int c0 = 0; c0 < N; c0 += 64) {
+            if (c0 >= c_left) break;                       // warp-uniform
+            const bool tail = c0 + 32 >= N || c_left - c0 <= 32;  // 32-channel box
+            uint32_t va[32], vb[32];
+            tmem_ld32(tbase + c0, va);
+            if (!tail) tmem_ld32(tbase + c0 + 32, vb);
+            tmem_ld_wait();
+            uint8_t* buf = stg_w + (stg_i & 1) * C::kStgBox;
+            if (lane == 0) bulk_wait_read<1>();  // the store that last read `buf` is done
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (q >= 4 && tail) break;
+              uint32_t w[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int c = q * 8 + 2 * j;  // channel within the 64-wide box
+                const uint32_t x0 = q < 4 ? va[c] : vb[c - 32];
+                const uint32_t x1 = q < 4 ? va[c + 1] : vb[c - 31];
+                float a = __uint_as_float(x0) + bs[c0 + c];
+                float b = __uint_as_float(x1) + bs[c0 + c + 1];
+                a = fmaxf(a, 0.f) + sl[c0 + c] * fminf(a, 0.f);
+                b = fmaxf(b, 0.f) + sl[c0 + c + 1] * fminf(b, 0.f);
+                w[j] = valid ? pack_bf16(a, b) : 0u;
+              }
+              // SW128: 16-byte chunk q of row r sits at chunk q ^ (r & 7);
+              // SW64 (32-channel rows of 64 bytes): chunk q ^ ((r >> 1) & 3)
+              const uint32_t off = tail ? lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)
+                                        : lane * 128 + ((q ^ (lane & 7)) << 4);
+              *reinterpret_cast<uint4*>(buf + off) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(tail ? &maps.out_tail[tc.g] : &maps.out[tc.g], buf, g.out_c_off + tc.nt * N + c0,
+                           row_w, tc.n);
+              bulk_commit();
+            }
+            ++stg_i;
+          }
+          continue;
+        }
+        // thin heads (38/19 channels into the stage concat) and the fp32 NCHW
+        // network output: per-channel stores of valid pixels only; lanes are
+        // consecutive pixels, so NCHW stores coalesce along W
 #pragma unroll
         for (int c0 = 0; c0 < N; c0 += 32) {
+          if (c0 >= c_left) break;
           uint32_t v[32];
-          tmem_ld32(tmem + ((quad * 32) << 16) + acc * C::kAccCols + sub * N + c0, v);
+          tmem_ld32(tbase + c0, v);
           tmem_ld_wait();
-          if (p.out_mode != kOutTmaBf16) {
-            // thin heads (38/19 channels into the stage concat) and the fp32
-            // NCHW network output: per-channel stores of valid pixels only;
-            // lanes are consecutive pixels, so NCHW stores coalesce along W
-            if (valid && c0 < c_left) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (c0 + j < c_left) {
-                  float a = __uint_as_float(v[j]) + bs[c0 + j];
-                  a = g.act == 1 ? fmaxf(a, 0.f) : (a < 0.f ? a * sl[c0 + j] : a);
-                  const int co = tc.nt * N + c0 + j;
-                  if (p.out_mode == kOutNchwF32)
-                    static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
-                                                    p.H + hh) * p.W + ww] = a;
-                  else
-                    out[(static_cast<size_t>(tc.n) * img_rows + row_in_img) * g.out_c_stride + g.out_c_off + co] =
-                        __float2bfloat16_rn(a);
-                }
-              }
+          for (int j = 0; j < 32; ++j) {
+            if (valid && c0 + j < c_left) {
+              float a = __uint_as_float(v[j]) + bs[c0 + j];
+              a = fmaxf(a, 0.f) + sl[c0 + j] * fminf(a, 0.f);
+              const int co = tc.nt * N + c0 + j;
+              if (p.out_mode == kOutNchwF32)
+                static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
+                                                p.H + hh) * p.W + ww] = a;
+              else
+                out[(static_cast<size_t>(tc.n) * img_rows + row_in_img) * g.out_c_stride + g.out_c_off + co] =
+                    __float2bfloat16_rn(a);
             }
-            continue;
-          }
-          if (store && c0 < c_left) {
-            uint32_t w[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              float a = __uint_as_float(v[2 * j]) + bs[c0 + 2 * j];
-              float b = __uint_as_float(v[2 * j + 1]) + bs[c0 + 2 * j + 1];
-              if (g.act == 1) {
-                a = fmaxf(a, 0.f);
-                b = fmaxf(b, 0.f);
-              } else {
-                if (a < 0.f) a *= sl[c0 + 2 * j];
-                if (b < 0.f) b *= sl[c0 + 2 * j + 1];
-              }
-              w[j] = valid ? pack_bf16(a, b) : 0u;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              dst[c0 / 8 + q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
           }
         }
       }
@@ -291,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&acc_empty[acc]);
       if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();

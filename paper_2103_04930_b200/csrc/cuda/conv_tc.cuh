@@ -94,7 +94,9 @@ struct ConvMaps {
   CUtensorMap act_small[kConvMaxGroups];  // 2D, box {64 ch, 8 rows}
   CUtensorMap act_mid[kConvMaxGroups];    // 2D, box {64 ch, 128 rows}
   CUtensorMap wgt[kConvMaxGroups];        // 2D [cout_pad][k*k*cin_pad], box {64, 128 (or pm_n) rows}
-  CUtensorMap out[kConvMaxGroups];        // 3D [N][Hp*Wp][C_out], box {64 ch, 32 rows, 1}
+  CUtensorMap out[kConvMaxGroups];        // 3D [N][Hp*Wp][C_out], box {64 ch, 32 rows, 1}, SW128
+  CUtensorMap out_tail[kConvMaxGroups];   // same view, box {32 ch, 32 rows, 1}, SW64 (pixel-major
+                                          // layers whose cout % 64 == 32)
 };
 
 // host side

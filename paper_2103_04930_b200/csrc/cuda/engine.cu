@@ -104,15 +104,18 @@ CUtensorMap make_map_2d(const void* base, uint64_t cols, uint64_t rows, uint32_t
 }
 
 // 3D bf16 [n][rows][cols] (the padded-flat buffer seen per image), box {64, 32, 1}
-CUtensorMap make_map_3d_store(const void* base, uint64_t cols, uint64_t rows, uint64_t n) {
+// [32 rows][box_c channels] store boxes: 64 channels with the 128-byte
+// swizzle, or 32 channels (64-byte rows) with the 64-byte swizzle
+CUtensorMap make_map_3d_store(const void* base, uint64_t cols, uint64_t rows, uint64_t n, uint32_t box_c = 64) {
   CUtensorMap m;
   cuuint64_t dims[3] = {cols, rows, n};
   cuuint64_t strides[2] = {cols * 2, rows * cols * 2};
-  cuuint32_t box[3] = {64, 32, 1};
+  cuuint32_t box[3] = {box_c, 32, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           box_c == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled (store) failed: " + std::to_string(int(r)));
   return m;
@@ -403,10 +406,12 @@ struct PlanBuilder {
       if (L.exec_k != p.k || L.cin_pad != L0.cin_pad || L.cout_pad != L0.cout_pad ||
           in[g].c_off != p.in_c_off || (out[g].buf == -1) != to_output)
         fail(AVEC_ERR_INVALID_MODEL, "grouped conv layers differ in shape");
-      if (p.out_mode == kOutTmaBf16 && !p.pixel_major) {
+      if (p.out_mode == kOutTmaBf16) {
         const int ob = out[g].buf;
         op.maps.out[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob], uint64_t(gi.Hp()) * gi.Wp(),
                                            plan.n);
+        op.maps.out_tail[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob],
+                                                uint64_t(gi.Hp()) * gi.Wp(), plan.n, 32);
       }
       ConvGroupParams& gp = p.g[g];
       gp.bias = L.bias;
