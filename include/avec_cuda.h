@@ -107,7 +107,7 @@ int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c
                           uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);
 /* Profiling hook (bench.py roofline): replays the plan of this shape op by op
  * with CUDA events on the slot stream, `reps` times, after one warm graph run.
- * Per op i < *n_ops: kind (0 = first-layer im2col, 1 = pixel-major tcgen05 conv,
+ * Per op i < *n_ops: kind (0 = fused first layer, 1 = pixel-major tcgen05 conv,
  * 2 = max-pool, 3 = swap-AB tcgen05 conv), algorithmic FLOPs and bytes of the
  * launch, mean duration (ms). */
 int avec_posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,

@@ -37,8 +37,8 @@ struct PmCfg {
   static constexpr int kTileN = 128 * SUBS_M;  // pixels per tile
   static constexpr int kWinRows = kTileN + 8;
   static constexpr int kWinBytes = kWinRows * 128;
-  // N = 64 serves the short-K high-resolution layers (conv1_1 on its im2col,
-  // conv1_2): one more window in flight keeps their HBM reads streaming
+  // N = 64 serves the short-K high-resolution conv1_2 (and the thin heads):
+  // one more window in flight keeps its HBM reads streaming
   static constexpr int kWinStages = N == 64 ? 3 : 2;
   static constexpr int kWgtBytes = N * 128;  // N rows x 64 bf16
   static constexpr int kAccCols = SUBS_M * N;

@@ -108,5 +108,10 @@ void conv_pm_configure();
 int conv_pm_subs(int n_tile);   // 128-pixel M sub-tiles per tile for a channel tile
 int conv_pm_tile_n(int cout);   // channel tile (MMA N) for a layer's output width
 void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
+// first layer fused with the input conversion (conv_first.cu): fp32 NCHW frames
+// -> 3x3x3 taps built in smem -> tcgen05 -> 64-channel padded-flat NHWC output
+void conv_first_configure();
+void launch_conv_first(const ConvMaps& maps, const ConvParams& p, const float* frames, int sm_count,
+                       cudaStream_t stream);
 
 }  // namespace avec

@@ -241,7 +241,7 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
   for (size_t i = 0; i < f.convs.size(); ++i) {
     ConvLayerDev& L = net->layers[i];
     L.def = f.convs[i];
-    // the 3-channel first layer runs as a 1x1 conv over its 64-channel im2col
+    // the 3-channel first layer: one 64-wide K row of its 27 taps (conv_first.cu)
     L.exec_k = i == 0 ? 1 : L.def.k;
     L.cin_pad = i == 0 ? 64 : L.def.cin_pad ? L.def.cin_pad : round_up(L.def.cin, 64);
     L.cout_pad = round_up(L.def.cout, 128);
@@ -326,6 +326,45 @@ struct PlanBuilder {
   void record_io(int layer, TensorView in, TensorView out) {
     plan.layer_in[layer] = in;
     plan.layer_out[layer] = out;
+  }
+
+  // conv1_1 fused with the input conversion (conv_first.cu): reads the fp32
+  // frames, writes the 64-channel level-0 activation `out`
+  void first(int layer, TensorView out) {
+    const ConvLayerDev& L = net.layers[layer];
+    if (L.def.cout > 64 || out.level != 0 || out.c_off % 8 != 0)
+      fail(AVEC_ERR_UNSUPPORTED, "first layer must write <= 64 channels at level 0");
+    PlanOp op;
+    op.kind = PlanOp::kFirst;
+    op.layers[0] = layer;
+    ConvParams& p = op.cp;
+    const Geometry& gi = plan.geo[0];
+    p.k = 3;
+    p.n_images = plan.n;
+    p.H = gi.H;
+    p.W = gi.W;
+    p.Hp = gi.Hp();
+    p.Wp = gi.Wp();
+    p.P = gi.P;
+    p.n_groups = 1;
+    p.tiles_per_image = (p.H * p.Wp + 127) / 128;
+    p.total_tiles = p.n_images * p.tiles_per_image;
+    ConvGroupParams& gp = p.g[0];
+    gp.bias = L.bias;
+    gp.slope = L.slope;
+    gp.act = L.def.act;
+    gp.cout = L.def.cout;
+    gp.out = plan.bufs[out.buf]->p;
+    gp.out_c_off = out.c_off;
+    gp.out_c_stride = out.c_stride;
+    op.maps.wgt[0] = make_map_2d(L.w, 64, L.cout_pad, 64);
+    op.maps.out[0] = make_map_3d_store(plan.bufs[out.buf]->p, plan.buf_c[out.buf], uint64_t(gi.Hp()) * gi.Wp(),
+                                       plan.n);
+    TensorView in;
+    in.buf = -2;
+    in.c = 3;
+    record_io(layer, in, out);  // parity hook shows the layer its real 3-channel input
+    plan.ops.push_back(op);
   }
 
   // one launch covering 1 or 2 conv layers (sibling branches) of equal shape
@@ -450,18 +489,8 @@ struct PlanBuilder {
 int build_trunk(PlanBuilder& b, Plan& plan, int cat, int trunk_off) {
   int li = 0;
   // level 0
-  const int a0 = b.buffer(0, 64), b0 = b.buffer(0, 64), i2c = b.buffer(0, 64);
-  {
-    PlanOp op;  // frames -> normalised bf16 im2col of the 3x3x3 taps
-    op.kind = PlanOp::kFirst;
-    op.dst = i2c;
-    plan.ops.push_back(op);
-    b.conv({li++}, {b.view(i2c, 0, 64)}, {b.view(a0, 0, 64)});  // conv1_1 as 1x1 over the im2col
-    TensorView in;
-    in.buf = -2;
-    in.c = 3;
-    plan.layer_in[0] = in;  // parity hook shows the layer its real 3-channel input
-  }
+  const int a0 = b.buffer(0, 64), b0 = b.buffer(0, 64);
+  b.first(li++, b.view(a0, 0, 64));  // conv1_1 fused with the frame conversion
   b.conv({li++}, {b.view(a0, 0, 64)}, {b.view(b0, 0, 64)});  // conv1_2
   const int p1 = b.buffer(1, 64), a1 = b.buffer(1, 128), b1 = b.buffer(1, 128);
   b.pool(b0, p1);
@@ -571,8 +600,7 @@ void run_ops(avec_ctx* ctx, const Plan& plan, const PoseNet& net, size_t first, 
     const PlanOp& op = plan.ops[i];
     switch (op.kind) {
       case PlanOp::kFirst:
-        launch_im2col_first(plan.in.as<float>(), plan.n, plan.H, plan.W, plan.bufs[op.dst]->p,
-                            plan.geo[0].P, st);
+        launch_conv_first(op.maps, op.cp, plan.in.as<float>(), ctx->sms, st);
         break;
       case PlanOp::kConv:
         if (op.cp.pixel_major)
@@ -660,6 +688,7 @@ void ctx_init(avec_ctx* ctx, int device, int slots) {
   ctx->label = "b200:" + std::to_string(device);
   conv_configure();
   conv_pm_configure();
+  conv_first_configure();
   if (slots <= 0) slots = 2;
   for (int i = 0; i < slots; ++i) {
     auto s = std::make_unique<Slot>();
@@ -871,12 +900,7 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
       p.bytes = double(n_img) * g.H * g.W * op.C * 2 * 1.25;  // read 4, write 1 bf16 per window
       continue;
     }
-    if (op.kind == PlanOp::kFirst) {  // im2col: 3 fp32 in + 64 bf16 out per pixel
-      p.kind = 0;
-      p.bytes = double(n_img) * h * w * (12.0 + 128.0);
-      continue;
-    }
-    p.kind = op.cp.pixel_major ? 1 : 3;
+    p.kind = op.kind == PlanOp::kFirst ? 0 : op.cp.pixel_major ? 1 : 3;
     for (int g = 0; g < 2; ++g) {
       if (op.layers[g] < 0) continue;
       const ConvDef& d = f.convs[op.layers[g]];

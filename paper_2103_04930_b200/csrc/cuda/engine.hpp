@@ -33,11 +33,6 @@ bool pdl_enabled();
 void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K,
                           cudaStream_t stream);
 
-// input fp32 NCHW frames -> (x - 0.5) -> bf16 -> im2col of the 3x3x3 first-layer
-// taps into 64-channel rows of a padded-flat NHWC buffer [n][H+2P][W+2P][64]
-void launch_im2col_first(const float* d_in, int n, int H, int W, void* d_out, int P,
-                         cudaStream_t stream);
-
 // 2x2/2 max pool, padded-flat NHWC bf16 -> padded-flat NHWC bf16
 void launch_maxpool2(const void* d_in, int n, int H, int W, int P_in, int C, void* d_out,
                      int P_out, cudaStream_t stream);

@@ -46,7 +46,7 @@ struct PinnedMem {
 // one conv layer resident on the device (bf16 packed for the TMA/UMMA path)
 struct ConvLayerDev {
   ConvDef def;
-  int exec_k = 0;  // filter size as executed (the first layer runs 1x1 over its im2col)
+  int exec_k = 0;  // filter size as executed (the first layer: 1, K = its 27 taps, conv_first.cu)
   int cin_pad = 0, cout_pad = 0;
   void* w = nullptr;       // bf16 [cout_pad][k*k][cin_pad]
   float* bias = nullptr;   // [cout_pad]

@@ -1,5 +1,5 @@
-// Streaming layers of the pose net: input conversion fused with the first
-// (3-channel) convolution, 2x2 max-pool, and an unpad/convert helper.
+// Streaming layers of the pose net: 2x2 max-pool and an unpad/convert helper
+// (the input conversion is fused into the first convolution, conv_first.cu).
 // All are HBM-bound; loads/stores are 16-byte vectors over channels.
 #include <cuda_bf16.h>
 
@@ -8,48 +8,6 @@
 namespace avec {
 
 namespace {
-
-// conv1_1 has 3 input channels (K = 27), too thin to feed the tensor cores
-// directly. This streaming kernel fuses the wire-format conversion with an
-// im2col: fp32 NCHW frame -> (x - 0.5) -> bf16 (the net's input precision) ->
-// one 64-channel row per pixel holding the 27 taps (ci*9 + r*3 + s) and 37
-// zeros, in the level-0 padded-flat layout. conv1_1 then runs as a 1x1
-// tcgen05 conv over those 64 channels (weights packed to match).
-// HBM-bound: 12 B read + 128 B written per pixel.
-__global__ void __launch_bounds__(128) im2col_first_kernel(const float* __restrict__ in, int n,
-                                                           int H, int W,
-                                                           __nv_bfloat16* __restrict__ out, int P) {
-  const long long pix = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long total = static_cast<long long>(n) * H * W;
-  if (pix >= total) return;
-  const int x = static_cast<int>(pix % W);
-  const int y = static_cast<int>((pix / W) % H);
-  const int b = static_cast<int>(pix / (static_cast<long long>(W) * H));
-  uint32_t packed[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) packed[i] = 0;
-#pragma unroll
-  for (int ci = 0; ci < 3; ++ci) {
-    const float* plane = in + (static_cast<size_t>(b) * 3 + ci) * H * W;
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        const int yy = y + r - 1, xx = x + s - 1;
-        float v = 0.f;
-        if (yy >= 0 && yy < H && xx >= 0 && xx < W) v = __ldg(plane + yy * W + xx) - 0.5f;
-        const int t = ci * 9 + r * 3 + s;
-        const uint32_t bits = __bfloat16_as_ushort(__float2bfloat16_rn(v));
-        packed[t >> 1] |= (t & 1) ? (bits << 16) : bits;
-      }
-    }
-  }
-  uint4* dst = reinterpret_cast<uint4*>(
-      out + ((static_cast<size_t>(b) * (H + 2 * P) + y + P) * (W + 2 * P) + x + P) * 64);
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-}
 
 __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n, int H, int W,
                                 int P_in, int C, __nv_bfloat16* __restrict__ out, int P_out) {
@@ -103,13 +61,6 @@ unsigned blocks_for(long long total, int threads) {
 
 }  // namespace
 
-void launch_im2col_first(const float* d_in, int n, int H, int W, void* d_out, int P,
-                         cudaStream_t stream) {
-  const long long total = static_cast<long long>(n) * H * W;
-  im2col_first_kernel<<<blocks_for(total, 128), 128, 0, stream>>>(
-      d_in, n, H, W, static_cast<__nv_bfloat16*>(d_out), P);
-  check_cuda(cudaGetLastError(), "im2col_first launch");
-}
 
 void launch_maxpool2(const void* d_in, int n, int H, int W, int P_in, int C, void* d_out,
                      int P_out, cudaStream_t stream) {
