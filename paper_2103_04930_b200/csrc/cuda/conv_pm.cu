@@ -19,6 +19,8 @@
 // padding; rows past the image's padded extent are not written.
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "conv_tc.cuh"
 #include "engine.hpp"
 #include "ptx.cuh"
@@ -253,46 +255,75 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tbase = tmem + ((quad * 32) << 16) + acc * C::kAccCols + sub * N;
         if (p.out_mode == kOutTmaBf16) {
           const int row_w = row_in_img - int(lane);  // the warp's first pixel
-#pragma unroll
-          for (int c0 = 0; c0 < N; c0 += 64) {
-            if (c0 >= c_left) break;                       // warp-uniform
-            const bool tail = c0 + 32 >= N || c_left - c0 <= 32;  // 32-channel box
-            uint32_t va[32], vb[32];
-            tmem_ld32(tbase + c0, va);
-            if (!tail) tmem_ld32(tbase + c0 + 32, vb);
+          // one [32 px][W ch] box: TMEM -> bias/activation/bf16 -> swizzled
+          // staging (swizzle span = box row: 16-byte chunk q of row r lands at
+          // q ^ (r & 7) for 128 B rows, q ^ ((r >> 1) & 3) for 64 B,
+          // q ^ ((r >> 2) & 1) for 32 B; 16 B rows are unswizzled) -> TMA store
+          auto box = [&](auto width, int c0) {
+            constexpr int W = decltype(width)::value;
+            uint32_t va[W < 16 ? 16 : W > 32 ? 32 : W], vb[W == 64 ? 32 : 1];
+            if constexpr (W >= 32) {
+              tmem_ld32(tbase + c0, va);
+              if constexpr (W == 64) tmem_ld32(tbase + c0 + 32, vb);
+            } else {
+              tmem_ld16(tbase + c0, va);  // c0 + 16 <= N: N is a multiple of 16
+            }
             tmem_ld_wait();
             uint8_t* buf = stg_w + (stg_i & 1) * C::kStgBox;
             if (lane == 0) bulk_wait_read<1>();  // the store that last read `buf` is done
             __syncwarp();
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              if (q >= 4 && tail) break;
+            for (int q = 0; q < W / 8; ++q) {
               uint32_t w[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const int c = q * 8 + 2 * j;  // channel within the 64-wide box
-                const uint32_t x0 = q < 4 ? va[c] : vb[c - 32];
-                const uint32_t x1 = q < 4 ? va[c + 1] : vb[c - 31];
+                const int c = q * 8 + 2 * j;  // channel within the box
+                uint32_t x0, x1;
+                if constexpr (W == 64) {
+                  x0 = q < 4 ? va[c & 31] : vb[c & 31];
+                  x1 = q < 4 ? va[(c + 1) & 31] : vb[(c + 1) & 31];
+                } else {
+                  x0 = va[c];
+                  x1 = va[c + 1];
+                }
                 float a = __uint_as_float(x0) + bs[c0 + c];
                 float b = __uint_as_float(x1) + bs[c0 + c + 1];
                 a = fmaxf(a, 0.f) + sl[c0 + c] * fminf(a, 0.f);
                 b = fmaxf(b, 0.f) + sl[c0 + c + 1] * fminf(b, 0.f);
                 w[j] = valid ? pack_bf16(a, b) : 0u;
               }
-              // SW128: 16-byte chunk q of row r sits at chunk q ^ (r & 7);
-              // SW64 (32-channel rows of 64 bytes): chunk q ^ ((r >> 1) & 3)
-              const uint32_t off = tail ? lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)
-                                        : lane * 128 + ((q ^ (lane & 7)) << 4);
+              uint32_t off;
+              if constexpr (W == 64) off = lane * 128 + ((q ^ (lane & 7)) << 4);
+              else if constexpr (W == 32) off = lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4);
+              else if constexpr (W == 16) off = lane * 32 + ((q ^ ((lane >> 2) & 1)) << 4);
+              else off = lane * 16;
               *reinterpret_cast<uint4*>(buf + off) = make_uint4(w[0], w[1], w[2], w[3]);
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(tail ? &maps.out_tail[tc.g] : &maps.out[tc.g], buf, g.out_c_off + tc.nt * N + c0,
-                           row_w, tc.n);
+              const CUtensorMap* m = W == 64 ? &maps.out[tc.g]
+                                     : W == 32 ? &maps.out32[tc.g]
+                                     : W == 16 ? &maps.out16[tc.g]
+                                               : &maps.out8[tc.g];
+              tma_store_3d(m, buf, g.out_c_off + tc.nt * N + c0, row_w, tc.n);
               bulk_commit();
             }
             ++stg_i;
+          };
+          if (c_left >= N) {  // full tile: compile-time box sequence
+#pragma unroll
+            for (int c0 = 0; c0 + 64 <= N; c0 += 64) box(std::integral_constant<int, 64>{}, c0);
+            if constexpr (N % 64 == 32) box(std::integral_constant<int, 32>{}, N - 32);
+          } else {
+            // round_up(live channels, 8) in boxes of 64/32/16/8 channels; the
+            // channels past cout (zero weights, zero bias) store zeros
+            const int c_end = (c_left + 7) & ~7;
+            int c0 = 0;
+            for (; c0 + 64 <= c_end; c0 += 64) box(std::integral_constant<int, 64>{}, c0);
+            if (c0 + 32 <= c_end) { box(std::integral_constant<int, 32>{}, c0); c0 += 32; }
+            if (c0 + 16 <= c_end) { box(std::integral_constant<int, 16>{}, c0); c0 += 16; }
+            if (c0 + 8 <= c_end) box(std::integral_constant<int, 8>{}, c0);
           }
           continue;
         }

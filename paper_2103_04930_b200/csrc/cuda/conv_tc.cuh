@@ -95,8 +95,11 @@ struct ConvMaps {
   CUtensorMap act_mid[kConvMaxGroups];    // 2D, box {64 ch, 128 rows}
   CUtensorMap wgt[kConvMaxGroups];        // 2D [cout_pad][k*k*cin_pad], box {64, 128 (or pm_n) rows}
   CUtensorMap out[kConvMaxGroups];        // 3D [N][Hp*Wp][C_out], box {64 ch, 32 rows, 1}, SW128
-  CUtensorMap out_tail[kConvMaxGroups];   // same view, box {32 ch, 32 rows, 1}, SW64 (pixel-major
-                                          // layers whose cout % 64 == 32)
+  // narrower boxes of the same view for the pixel-major kernel's channel tails
+  // (96-wide layers, 52/38/26/19-channel heads): 32 ch SW64, 16 ch SW32, 8 ch
+  CUtensorMap out32[kConvMaxGroups];
+  CUtensorMap out16[kConvMaxGroups];
+  CUtensorMap out8[kConvMaxGroups];
 };
 
 // host side

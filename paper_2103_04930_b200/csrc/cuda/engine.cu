@@ -104,8 +104,8 @@ CUtensorMap make_map_2d(const void* base, uint64_t cols, uint64_t rows, uint32_t
 }
 
 // 3D bf16 [n][rows][cols] (the padded-flat buffer seen per image), box {64, 32, 1}
-// [32 rows][box_c channels] store boxes: 64 channels with the 128-byte
-// swizzle, or 32 channels (64-byte rows) with the 64-byte swizzle
+// [32 rows][box_c channels] store boxes; the swizzle span equals the box row
+// (64 ch: 128 B, 32 ch: 64 B, 16 ch: 32 B, 8 ch: none)
 CUtensorMap make_map_3d_store(const void* base, uint64_t cols, uint64_t rows, uint64_t n, uint32_t box_c = 64) {
   CUtensorMap m;
   cuuint64_t dims[3] = {cols, rows, n};
@@ -114,7 +114,10 @@ CUtensorMap make_map_3d_store(const void* base, uint64_t cols, uint64_t rows, ui
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           box_c == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           box_c == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                           : box_c == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                         : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled (store) failed: " + std::to_string(int(r)));
@@ -404,12 +407,16 @@ struct PlanBuilder {
       tc_ok = tc_ok && out[g].c_off % 8 == 0 && out[g].level == in[g].level;
     p.pixel_major = tc_ok ? 0 : 1;
     if (L0.exec_k == 7 && p.pixel_major) fail(AVEC_ERR_UNSUPPORTED, "7x7 layer needs the swap-AB kernel");
-    // channel slabs at 8-aligned offsets take the vector / TMA-store path:
-    // 32-channel granules for pixel-major, 64-channel TMA boxes for swap-AB
+    // outputs at 8-aligned channel offsets take the TMA-store path: swap-AB
+    // stores 64-channel boxes (cout % 64 == 0); pixel-major stores 64/32/16/8-
+    // channel boxes covering round_up(cout, 8) channels, so the buffer layouts
+    // keep the channels up to the next multiple of 8 free (netspec.hpp)
     bool slab = !to_output;
-    for (size_t g = 0; g < layers.size(); ++g)
-      slab = slab && net.layers[layers[g]].def.cout % (p.pixel_major ? 32 : 64) == 0 &&
-             out[g].c_off % 8 == 0 && out[g].level == in[g].level;
+    for (size_t g = 0; g < layers.size(); ++g) {
+      const int cout = net.layers[layers[g]].def.cout;
+      slab = slab && (p.pixel_major || cout % 64 == 0) && out[g].c_off % 8 == 0 &&
+             out[g].c_off + round_up(cout, 8) <= out[g].c_stride && out[g].level == in[g].level;
+    }
     p.out_mode = to_output ? kOutNchwF32 : slab ? kOutTmaBf16 : kOutDirectBf16;
     if (p.pixel_major) {
       p.pm_n = conv_pm_tile_n(L0.def.cout);
@@ -449,8 +456,12 @@ struct PlanBuilder {
         const int ob = out[g].buf;
         op.maps.out[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob], uint64_t(gi.Hp()) * gi.Wp(),
                                            plan.n);
-        op.maps.out_tail[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob],
-                                                uint64_t(gi.Hp()) * gi.Wp(), plan.n, 32);
+        if (p.pixel_major) {
+          const uint64_t rows = uint64_t(gi.Hp()) * gi.Wp();
+          op.maps.out32[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob], rows, plan.n, 32);
+          op.maps.out16[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob], rows, plan.n, 16);
+          op.maps.out8[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob], rows, plan.n, 8);
+        }
       }
       ConvGroupParams& gp = p.g[g];
       gp.bias = L.bias;
@@ -519,9 +530,9 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
   const int nl = int(f.convs.size());
   plan.layer_in.assign(nl, TensorView{});
   plan.layer_out.assign(nl, TensorView{});
-  const int cat = b.buffer(3, 192);  // [trunk 128 | L1 38 | L2 19 | pad]
+  const int cat = b.buffer(3, kCocoCatChannels);  // [trunk | L1 at kCocoPaf | L2 at kCocoHeat]
   int li = build_trunk(b, plan, cat, 0);
-  const int T = f.trunk_channels, C1 = f.paf_channels, C2 = f.heat_channels;
+  const int T = f.trunk_channels, C1 = f.paf_channels, C2 = f.heat_channels;  // T == kCocoPaf
   // branch buffers
   const int l1a = b.buffer(3, 128), l1b = b.buffer(3, 128), l2a = b.buffer(3, 128),
             l2b = b.buffer(3, 128), l1x = b.buffer(3, 512), l2x = b.buffer(3, 512);
@@ -531,11 +542,11 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
   b.conv({s1 + 2, s1 + 7}, {b.view(l1b, 0, 128), b.view(l2b, 0, 128)}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
   b.conv({s1 + 3, s1 + 8}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)}, {b.view(l1x, 0, 512), b.view(l2x, 0, 512)});
   b.conv({s1 + 4, s1 + 9}, {b.view(l1x, 0, 512), b.view(l2x, 0, 512)},
-         {b.view(cat, T, C1), b.view(cat, T + C1, C2)});
+         {b.view(cat, kCocoPaf, C1), b.view(cat, kCocoHeat, C2)});
   li += 10;
   for (int t = 2; t <= f.stages; ++t) {
     const int s = li;  // L1: s..s+6, L2: s+7..s+13
-    const int catc = T + C1 + C2;
+    const int catc = T + C1 + C2;  // Caffe channels (cin_map places them)
     b.conv({s + 0, s + 7}, {b.view(cat, 0, catc), b.view(cat, 0, catc)},
            {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
     int x = l1a, y = l1b, u = l2a, v = l2b;
@@ -550,7 +561,7 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
              {b.view(-1, C2, C1), b.view(-1, 0, C2)});
     } else {
       b.conv({s + 6, s + 13}, {b.view(x, 0, 128), b.view(u, 0, 128)},
-             {b.view(cat, T, C1), b.view(cat, T + C1, C2)});
+             {b.view(cat, kCocoPaf, C1), b.view(cat, kCocoHeat, C2)});
     }
     li += 14;
   }

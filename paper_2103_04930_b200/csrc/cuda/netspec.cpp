@@ -74,10 +74,16 @@ void build_coco(PoseFamily& f) {
   }
   const int branches = f.paf_channels + f.heat_channels;
   const int cat = branches + f.trunk_channels;  // 185
-  // internal concat layout [trunk 128 | L1 38 | L2 19 | pad] (the trunk first
-  // keeps every TMA window 16-byte aligned); Caffe order is [L1, L2, trunk]
+  // internal concat layout (netspec.hpp): [trunk | L1 at kCocoPaf | L2 at
+  // kCocoHeat]; Caffe order is [L1, L2, trunk]
+  if (f.trunk_channels != kCocoPaf || kCocoPaf + f.paf_channels > kCocoHeat ||
+      kCocoHeat + f.heat_channels > kCocoCatChannels)
+    fail(AVEC_ERR_INVALID_MODEL, "COCO stage concat layout does not fit");
   std::vector<int> map(cat);
-  for (int ci = 0; ci < cat; ++ci) map[ci] = ci < branches ? ci + f.trunk_channels : ci - branches;
+  for (int ci = 0; ci < cat; ++ci)
+    map[ci] = ci < f.paf_channels ? kCocoPaf + ci
+              : ci < branches     ? kCocoHeat + (ci - f.paf_channels)
+                                  : ci - branches;
   for (int t = 2; t <= f.stages; ++t) {
     for (int b = 0; b < 2; ++b) {
       const std::string sfx = "_stage" + std::to_string(t) + (b == 0 ? "_L1" : "_L2");

@@ -53,7 +53,13 @@ PoseFamily parse_avecnet(const uint8_t* s, size_t n);
 // deterministic He-uniform init, Caffe order; out has weight_floats() entries
 void synth_weights(const PoseFamily& f, float* out);
 
-// BODY_25 stage-concat buffer layout (256 channels):
+// Stage-concat buffer layouts. Each head slot starts on an 8-channel boundary
+// and owns the channels up to the next one (the pixel-major epilogue stores
+// 8-channel-granular TMA boxes).
+// COCO (192 channels): [trunk 0..127 | PAF 128..165 | pad | heat 168..186 | pad]
+constexpr int kCocoCatChannels = 192;
+constexpr int kCocoPaf = 128, kCocoHeat = 168;
+// BODY_25 (256 channels):
 //   [heat 0..25 | pad | PAF 32..83 | pad | trunk 88..215 | pad]
 // so every stage input is ONE contiguous, 16-byte aligned channel window:
 // PAF stages 1..3 and heat stage 0 read [32, 216), heat stage 1 reads [0, 216).
