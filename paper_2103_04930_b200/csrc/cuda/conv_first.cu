@@ -14,8 +14,9 @@
 //
 // HBM traffic per pixel: 12 B read (each input float is reused by 9 taps
 // through L1) + 128 B written — the floor for this layer. The MMA, with its
-// weights resident in smem for the CTA's lifetime, is negligible. Latency is
-// hidden by several co-resident CTAs per SM rather than an intra-CTA pipeline.
+// weights resident in smem for the CTA's lifetime, is negligible. Load latency
+// is hidden by gathering each tile's taps one tile ahead (in registers) and by
+// several co-resident CTAs per SM.
 // Results are bit-identical to the im2col + 1x1 path it replaces (same bf16
 // operands, same K order, same MMA shape).
 #include <cuda_bf16.h>
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
     conv_first_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p,
                       const float* __restrict__ frames) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* sa = smem + FirstSmem::a;
   uint8_t* sw = smem + FirstSmem::w;
   float* sbias = reinterpret_cast<float*>(smem + FirstSmem::bias);
@@ -91,36 +92,49 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
   }
 
   const int HW = p.H * p.W;
+  const bool relu = g.act == 1;
   uint32_t phase = 0;
   bool first = true;
   uint8_t* stg = smem + FirstSmem::stg + warp * (32 * 128);
+  // The 27 taps of this thread's pixel in tile t, normalised (x - 0.5), zero
+  // outside the frame. Gathered one tile AHEAD: the loads for tile t+grid are
+  // in flight while tile t's MMA and epilogue run.
+  float x[27];
+  auto gather = [&](int t) {
+    const int n = t / p.tiles_per_image;
+    const int o = (t - n * p.tiles_per_image) * 128 + tid;
+    const int hh = o / p.Wp;
+    const int ww = o - hh * p.Wp;
+    const bool valid = hh < p.H && ww < p.W;
+    const float* img = frames + static_cast<size_t>(n) * 3 * HW;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int yy = hh + r - 1;
+      const bool rv = valid && yy >= 0 && yy < p.H;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int xx = ww + s - 1;
+        const bool v = rv && xx >= 0 && xx < p.W;
+        const float* q = img + yy * p.W + xx;
+#pragma unroll
+        for (int ci = 0; ci < 3; ++ci) x[ci * 9 + r * 3 + s] = v ? __ldg(q + ci * HW) - 0.5f : 0.f;
+      }
+    }
+  };
+  if (int(blockIdx.x) < p.total_tiles) gather(blockIdx.x);
   for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
     const int n = t / p.tiles_per_image;
     const int o = (t - n * p.tiles_per_image) * 128 + tid;  // padded-width output position
     const int hh = o / p.Wp;
     const int ww = o - hh * p.Wp;
     const bool valid = hh < p.H && ww < p.W;
-    // ---- im2col row of this pixel: taps t = ci*9 + r*3 + s
-    uint32_t packed[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) packed[i] = 0;
-    if (valid) {
-      const float* img = frames + static_cast<size_t>(n) * 3 * HW;
-#pragma unroll
-      for (int ci = 0; ci < 3; ++ci)
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int s = 0; s < 3; ++s) {
-            const int yy = hh + r - 1, xx = ww + s - 1;
-            float v = 0.f;
-            if (yy >= 0 && yy < p.H && xx >= 0 && xx < p.W) v = __ldg(img + ci * HW + yy * p.W + xx) - 0.5f;
-            const int k = ci * 9 + r * 3 + s;
-            const uint32_t bits = __bfloat16_as_ushort(__float2bfloat16_rn(v));
-            packed[k >> 1] |= (k & 1) ? (bits << 16) : bits;
-          }
-    }
+    // ---- im2col row of this pixel: taps k = ci*9 + r*3 + s
     {
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 13; ++i) packed[i] = pack2(x[2 * i], x[2 * i + 1]);
+      packed[13] = __bfloat16_as_ushort(__float2bfloat16_rn(x[26]));
+      packed[14] = packed[15] = 0;
       uint8_t* row = sa + tid * 128;
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -141,6 +155,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
       mma_commit(mma_done);
     }
     first = false;
+    if (t + int(gridDim.x) < p.total_tiles) gather(t + gridDim.x);  // next tile's taps
     mbar_wait(mma_done, phase);
     phase ^= 1;
     tc_fence_after();
@@ -159,8 +174,13 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
         const int c = q * 8 + 2 * j;
         float a = __uint_as_float(q < 4 ? va[c] : vb[c - 32]) + sbias[c];
         float b = __uint_as_float(q < 4 ? va[c + 1] : vb[c - 31]) + sbias[c + 1];
-        a = fmaxf(a, 0.f) + sslope[c] * fminf(a, 0.f);
-        b = fmaxf(b, 0.f) + sslope[c + 1] * fminf(b, 0.f);
+        if (relu) {
+          a = fmaxf(a, 0.f);
+          b = fmaxf(b, 0.f);
+        } else {
+          a = fmaxf(a, 0.f) + sslope[c] * fminf(a, 0.f);
+          b = fmaxf(b, 0.f) + sslope[c + 1] * fminf(b, 0.f);
+        }
         w[j] = valid ? pack2(a, b) : 0u;
       }
       *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);

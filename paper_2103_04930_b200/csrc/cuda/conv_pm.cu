@@ -88,8 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     conv_pm_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p) {
   using C = PmCfg<N, SUBS_M>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* win = smem + C::win;
   uint8_t* wgt = smem + C::wgt;
   uint8_t* stg = smem + C::stg;
@@ -259,8 +258,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           // staging (swizzle span = box row: 16-byte chunk q of row r lands at
           // q ^ (r & 7) for 128 B rows, q ^ ((r >> 1) & 3) for 64 B,
           // q ^ ((r >> 2) & 1) for 32 B; 16 B rows are unswizzled) -> TMA store
-          auto box = [&](auto width, int c0) {
+          auto box = [&](auto width, auto relu_only, int c0) {
             constexpr int W = decltype(width)::value;
+            constexpr bool kRelu = decltype(relu_only)::value;
             uint32_t va[W < 16 ? 16 : W > 32 ? 32 : W], vb[W == 64 ? 32 : 1];
             if constexpr (W >= 32) {
               tmem_ld32(tbase + c0, va);
@@ -288,8 +288,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 float a = __uint_as_float(x0) + bs[c0 + c];
                 float b = __uint_as_float(x1) + bs[c0 + c + 1];
-                a = fmaxf(a, 0.f) + sl[c0 + c] * fminf(a, 0.f);
-                b = fmaxf(b, 0.f) + sl[c0 + c + 1] * fminf(b, 0.f);
+                if constexpr (kRelu) {
+                  a = fmaxf(a, 0.f);
+                  b = fmaxf(b, 0.f);
+                } else {  // identity (slope 1) or PReLU
+                  a = fmaxf(a, 0.f) + sl[c0 + c] * fminf(a, 0.f);
+                  b = fmaxf(b, 0.f) + sl[c0 + c + 1] * fminf(b, 0.f);
+                }
                 w[j] = valid ? pack_bf16(a, b) : 0u;
               }
               uint32_t off;
@@ -311,20 +316,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ++stg_i;
           };
-          if (c_left >= N) {  // full tile: compile-time box sequence
+          using I64 = std::integral_constant<int, 64>;
+          using I32 = std::integral_constant<int, 32>;
+          using I16 = std::integral_constant<int, 16>;
+          using I8 = std::integral_constant<int, 8>;
+          auto boxes = [&](auto relu_only) {
+            if (c_left >= N) {  // full tile: compile-time box sequence
 #pragma unroll
-            for (int c0 = 0; c0 + 64 <= N; c0 += 64) box(std::integral_constant<int, 64>{}, c0);
-            if constexpr (N % 64 == 32) box(std::integral_constant<int, 32>{}, N - 32);
-          } else {
-            // round_up(live channels, 8) in boxes of 64/32/16/8 channels; the
-            // channels past cout (zero weights, zero bias) store zeros
-            const int c_end = (c_left + 7) & ~7;
-            int c0 = 0;
-            for (; c0 + 64 <= c_end; c0 += 64) box(std::integral_constant<int, 64>{}, c0);
-            if (c0 + 32 <= c_end) { box(std::integral_constant<int, 32>{}, c0); c0 += 32; }
-            if (c0 + 16 <= c_end) { box(std::integral_constant<int, 16>{}, c0); c0 += 16; }
-            if (c0 + 8 <= c_end) box(std::integral_constant<int, 8>{}, c0);
-          }
+              for (int c0 = 0; c0 + 64 <= N; c0 += 64) box(I64{}, relu_only, c0);
+              if constexpr (N % 64 == 32) box(I32{}, relu_only, N - 32);
+            } else {
+              // round_up(live channels, 8) in boxes of 64/32/16/8 channels; the
+              // channels past cout (zero weights, zero bias) store zeros
+              const int c_end = (c_left + 7) & ~7;
+              int c0 = 0;
+              for (; c0 + 64 <= c_end; c0 += 64) box(I64{}, relu_only, c0);
+              if (c0 + 32 <= c_end) { box(I32{}, relu_only, c0); c0 += 32; }
+              if (c0 + 16 <= c_end) { box(I16{}, relu_only, c0); c0 += 16; }
+              if (c0 + 8 <= c_end) box(I8{}, relu_only, c0);
+            }
+          };
+          if (g.act == 1) boxes(std::true_type{});
+          else boxes(std::false_type{});
           continue;
         }
         // thin heads (38/19 channels into the stage concat) and the fp32 NCHW

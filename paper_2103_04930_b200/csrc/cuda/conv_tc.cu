@@ -121,8 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p) {
   using C = Cfg<SUBS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* win = smem + C::win;
   uint8_t* wgt = smem + C::wgt;
   uint8_t* stg = smem + C::stg;
