@@ -101,8 +101,8 @@ struct WorkIter {
       w.g = tc.g;
       w.n = tc.n;
       w.mt = tc.mt;
-      w.o0 = tc.pt * kMaxLen;
-      w.len = kMaxLen;
+      w.o0 = tc.pt * p.tile_px;
+      w.len = p.tile_px;
       cur += gridDim.x;
     }
     return true;

@@ -80,6 +80,7 @@ struct ConvParams {
   int pm_n;            // pixel-major channel tile: 64, 128 or 256
   int m_tiles;         // channel tiles: ceil(cout / 128), or ceil(cout / pm_n)
   int tiles_per_image; // ceil(H*Wp / pixels per tile)
+  int tile_px;         // swap-AB regular tiles: pixels per tile (<= 256 * subs, multiple of 32)
   int n_groups;
   int total_tiles;
   // swap-AB balanced partition (0 = regular tiles): 32-position units over the

@@ -304,6 +304,12 @@ struct PlanBuilder {
   const PoseNet& net;
   int device;
 
+  int sm_count() const {
+    int n = 0;
+    check_cuda(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device), "SM count");
+    return n;
+  }
+
   int buffer(int level, int C) {
     const Geometry& g = plan.geo[level];
     auto m = std::make_unique<DevMem>();
@@ -428,9 +434,38 @@ struct PlanBuilder {
       p.m_tiles = L0.cout_pad / 128;
       // 512-pixel tiles share each weight k-block across two MMAs; fall back to
       // 256-pixel tiles (double-buffered TMEM) when that leaves SMs idle
-      const int wide = int(layers.size()) * plan.n * ((p.H * p.Wp + 511) / 512) * p.m_tiles;
+      const int per_img_units = int(layers.size()) * plan.n * p.m_tiles;  // tiles per pixel-tile index
+      const int wide = per_img_units * ((p.H * p.Wp + 511) / 512);
       p.subs = (L0.exec_k == 7 || tc3 == 3 || (tc3 == 1 && wide >= 2 * 148)) ? 2 : 1;
-      p.tiles_per_image = (p.H * p.Wp + 256 * p.subs - 1) / (256 * p.subs);
+      // Tile width: with 512-pixel tiles a C2 7x7 launch is 128 tiles on 148
+      // SMs. Narrower tiles (the second MMA shrinks, N = T - 256) trade a
+      // little per-tile weight streaming for filling the SMs: pick the width
+      // maximising (useful positions / computed positions) x (busy SM-waves).
+      // Opt-in (AVEC_TILE_FIT=1): measured -2.3% serial step time on C2 (480-px
+      // tiles) but -3.7% throughput with the server's two slots in flight, where
+      // the other stream already fills the idle SMs and only the extra per-tile
+      // weight traffic remains.
+      static const bool tile_fit = [] {
+        const char* e = std::getenv("AVEC_TILE_FIT");
+        return e && e[0] == '1';
+      }();
+      p.tile_px = 256 * p.subs;
+      if (p.subs == 2 && tile_fit) {
+        const int sms = sm_count();
+        const int pos = p.H * p.Wp;
+        double best = 0;
+        for (int T = 512; T >= 288; T -= 32) {
+          const int tpi = (pos + T - 1) / T;
+          const int tiles = per_img_units * tpi;
+          const int waves = (tiles + sms - 1) / sms;
+          const double eff = double(pos) / (double(tpi) * T) * double(tiles) / (double(waves) * sms);
+          if (eff > best * 1.01) {
+            best = eff;
+            p.tile_px = T;
+          }
+        }
+      }
+      p.tiles_per_image = (p.H * p.Wp + p.tile_px - 1) / p.tile_px;
     }
     p.n_groups = int(layers.size());
     p.total_tiles = p.n_groups * p.n_images * p.tiles_per_image * p.m_tiles;
