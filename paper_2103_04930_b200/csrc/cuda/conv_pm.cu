@@ -41,7 +41,7 @@ struct PmCfg {
   static constexpr int kWinBytes = kWinRows * 128;
   // N = 64 serves the short-K high-resolution conv1_2 (and the thin heads):
   // one more window in flight keeps its HBM reads streaming
-  static constexpr int kWinStages = N == 64 ? 3 : 2;
+  static constexpr int kWinStages = N == 64 ? 4 : N == 256 ? 2 : 3;
   static constexpr int kWgtBytes = N * 128;  // N rows x 64 bf16
   static constexpr int kAccCols = SUBS_M * N;
   static constexpr int kAccStages = 2;

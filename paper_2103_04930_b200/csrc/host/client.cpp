@@ -1,5 +1,8 @@
 #include "client.hpp"
 
+#include <algorithm>
+#include <chrono>
+
 namespace avec::client {
 
 using namespace wire;
@@ -68,17 +71,38 @@ struct VectorSink final : net::FrameSink {
 
 double Session::forward(const float* data, std::uint32_t elems, std::uint32_t width,
                         std::uint32_t height, std::vector<float>& out) {
+  return forward_timed(data, elems, width, height, out).compute_s;
+}
+
+record::CycleTiming Session::forward_timed(const float* data, std::uint32_t elems, std::uint32_t width,
+                                           std::uint32_t height, std::vector<float>& out) {
+  using clk = std::chrono::steady_clock;
+  const std::uint64_t sent0 = ch_->bytes_sent(), recv0 = ch_->bytes_received();
+  const auto t0 = clk::now();
   const auto head = frame_data_header(elems);
   ch_->send_parts(head.data(), head.size(), data, std::size_t(elems) * 4);
   ch_->send(Resolution{width, height});
   ch_->send(FrameSize{elems});
+  const auto sent_at = clk::now();
   VectorSink sink(out);
   Message m = ch_->recv(&sink);
   if (const auto* e = std::get_if<ErrorMsg>(&m)) remote(*e);
   auto* fr = std::get_if<ForwardResult>(&m);
   if (!fr) throw std::runtime_error("expected ForwardResult");
   if (!fr->data.empty()) out = std::move(fr->data);  // not streamed (small replies)
-  return fr->compute_s;
+  const auto recv_at = clk::now();
+  const double send_s = std::chrono::duration<double>(sent_at - t0).count();
+  const double wait_s = std::chrono::duration<double>(recv_at - sent_at).count();
+  record::CycleTiming t;
+  t.compute_s = fr->compute_s;
+  // the destination may start computing before sent_at is stamped: clamp so
+  // gpu + communication never exceeds the cycle
+  t.gpu_s = std::min(fr->compute_s, wait_s);
+  t.communication_s = send_s + (wait_s - t.gpu_s);
+  t.other_s = std::max(0.0, std::chrono::duration<double>(clk::now() - t0).count() - t.communication_s - t.gpu_s);
+  t.bytes_sent = ch_->bytes_sent() - sent0;
+  t.bytes_received = ch_->bytes_received() - recv0;
+  return t;
 }
 
 }  // namespace avec::client

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "channel.hpp"
+#include "record.hpp"
 #include "wire.hpp"
 
 namespace avec::client {
@@ -30,6 +31,9 @@ class Session {
   // one cycle; result floats into `out`; returns the server's compute seconds
   double forward(const float* data, std::uint32_t elems, std::uint32_t width, std::uint32_t height,
                  std::vector<float>& out);
+  // the same cycle timed like the reference client (proj/src/client.cpp:160-195)
+  record::CycleTiming forward_timed(const float* data, std::uint32_t elems, std::uint32_t width,
+                                    std::uint32_t height, std::vector<float>& out);
   void close() { ch_->close(); }
   std::uint64_t bytes_sent() const { return ch_->bytes_sent(); }
   std::uint64_t bytes_received() const { return ch_->bytes_received(); }

@@ -7,12 +7,14 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <random>
 #include <string>
 #include <thread>
 #include <vector>
 
 #include "client.hpp"
+#include "record.hpp"
 
 namespace {
 
@@ -35,6 +37,8 @@ int main(int argc, char** argv) {
   std::string endpoint = "127.0.0.1:7000", model = "posenet";
   unsigned clients = 1, steps = 20, warmup = 3, batch = 8, width = 656, height = 368;
   unsigned long elems_override = 0;  // raw FrameData size (memcpy sweep), Resolution = width x (E/width)
+  // client 0's timed cycles as a reference-format run record (record.hpp)
+  std::string record_csv, record_md, label = "b200", host = "loadgen";
   for (int i = 1; i + 1 < argc; i += 2) {
     std::string a = argv[i], v = argv[i + 1];
     if (a == "--endpoint") endpoint = v;
@@ -46,6 +50,10 @@ int main(int argc, char** argv) {
     else if (a == "--height") height = std::stoul(v);
     else if (a == "--model") model = v;
     else if (a == "--elems") elems_override = std::stoul(v);
+    else if (a == "--record-csv") record_csv = v;
+    else if (a == "--record-md") record_md = v;
+    else if (a == "--label") label = v;
+    else if (a == "--host") host = v;
     else {
       std::fprintf(stderr, "unknown option %s\n", a.c_str());
       return 2;
@@ -83,6 +91,18 @@ int main(int argc, char** argv) {
   }
   const std::uint32_t elems = std::uint32_t(frames[0].size());
 
+  record::RunMeta meta;
+  meta.label = label;
+  meta.mode = "offload";
+  meta.host = host;
+  meta.destination = endpoint;
+  meta.workload = "video:" + std::to_string(steps) + ":" + std::to_string(width) + "x" + std::to_string(height) +
+                  ":batch" + std::to_string(batch);
+  meta.model = md.name;
+  meta.output_divisor = md.output_divisor;
+  record::RunRecord rec(meta);
+  double rec_setup_s = 0, rec_loop_s = 0;
+
   std::atomic<int> ready{0};
   std::atomic<bool> go{false};
   std::vector<double> busy(clients, 0.0), compute(clients, 0.0);
@@ -91,16 +111,22 @@ int main(int argc, char** argv) {
   for (unsigned c = 0; c < clients; ++c) {
     th.emplace_back([&, c] {
       try {
+        const auto ts = std::chrono::steady_clock::now();
         auto s = client::Session::connect(endpoint, 10.0);
         s.ensure_model(md);
+        if (c == 0) rec_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
         std::vector<float> out;
         for (unsigned i = 0; i < warmup; ++i) s.forward(frames[c].data(), elems, width, height, out);
         ready++;
         while (!go) std::this_thread::yield();
         const auto t0 = std::chrono::steady_clock::now();
-        for (unsigned i = 0; i < steps; ++i)
-          compute[c] += s.forward(frames[c].data(), elems, width, height, out);
+        for (unsigned i = 0; i < steps; ++i) {
+          const record::CycleTiming t = s.forward_timed(frames[c].data(), elems, width, height, out);
+          compute[c] += t.compute_s;
+          if (c == 0) rec.record(t);
+        }
         busy[c] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (c == 0) rec_loop_s = busy[c];
         s.close();
       } catch (const std::exception& e) {
         errs[c] = e.what();
@@ -118,6 +144,19 @@ int main(int argc, char** argv) {
       std::printf("{\"ok\": false, \"error\": \"%s\"}\n", e.c_str());
       return 1;
     }
+  if (!record_csv.empty() || !record_md.empty()) {
+    // warm-up cycles are in neither the rows nor the wall time, so
+    // gpu + communication + other + setup == total_wall (profiler.cpp decomposition)
+    rec.finalize(rec_setup_s, rec_setup_s + rec_loop_s);
+    if (!record_csv.empty()) {
+      std::ofstream f(record_csv);
+      record::write_cycle_csv(rec, f);
+    }
+    if (!record_md.empty()) {
+      std::ofstream f(record_md);
+      record::write_summary_markdown(rec, f);
+    }
+  }
   double cs = 0;
   for (double v : compute) cs += v;
   const double frames_total = double(steps) * batch * clients;
