@@ -34,7 +34,7 @@ using namespace ptx;
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
 
-template <int N, int SUBS_M>
+template <int N, int SUBS_M, int NCTA>
 struct PmCfg {
   static constexpr int kTileN = 128 * SUBS_M;  // pixels per tile
   static constexpr int kWinRows = kTileN + 8;
@@ -42,7 +42,7 @@ struct PmCfg {
   // N = 64 serves the short-K high-resolution conv1_2 (and the thin heads):
   // one more window in flight keeps its HBM reads streaming
   static constexpr int kWinStages = N == 64 ? 4 : N == 256 ? 2 : 3;
-  static constexpr int kWgtBytes = N * 128;  // N rows x 64 bf16
+  static constexpr int kWgtBytes = (N / NCTA) * 128;  // this CTA's N/NCTA rows x 64 bf16
   static constexpr int kAccCols = SUBS_M * N;
   static constexpr int kAccStages = 2;
   static_assert(kAccStages * kAccCols <= 512, "TMEM budget");
@@ -83,10 +83,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int N, int SUBS_M>
+template <int N, int SUBS_M, int NCTA>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_pm_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p) {
-  using C = PmCfg<N, SUBS_M>;
+  using C = PmCfg<N, SUBS_M, NCTA>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* win = smem + C::win;
@@ -103,6 +103,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::kAccStages);
 
   const uint32_t warp = warp_id();
+  // CTA pair (NCTA == 2): rank 0 (leader) issues the M = 256 MMAs and owns the
+  // full / acc_empty barriers; both CTAs load their own window and half of
+  // every weight k-block, and run the epilogue of their own 128-row halves
+  const uint32_t rank = NCTA == 2 ? cluster_cta_rank() : 0;
+  const bool leader = rank == 0;
   if (warp == 0 && elect_one()) {
     for (int g = 0; g < p.n_groups; ++g) {
       tma_prefetch(C::kTileN == 256 ? &maps.act_big[g] : &maps.act_mid[g]);
@@ -119,13 +124,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < C::kAccStages; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], NCTA == 2 ? 8 : 128);  // pair: one arrival per epilogue warp
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (NCTA == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+    else tmem_alloc<kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (NCTA == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // see conv_tc.cu
@@ -140,30 +149,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ws = 0, wst = 0;
       uint32_t wph = 0, wtph = 0;
       const uint32_t win_tx = (C::kTileN + (k > 1 ? 8 : 0)) * 128;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      for (int t = int(blockIdx.x) / NCTA; t < p.total_tiles; t += int(gridDim.x) / NCTA) {
         const PmTile tc = pm_decode(p, t);
-        const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + tc.pt * C::kTileN;
+        const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + (tc.pt * NCTA + int(rank)) * C::kTileN;
         for (int c = 0; c < p.cin_chunks; ++c) {
           const int ch = p.in_c_off + c * 64;
           for (int r = 0; r < k; ++r) {
             mbar_wait(&win_empty[ws], wph ^ 1);
-            mbar_arrive_expect_tx(&win_full[ws], win_tx);
+            if (leader) mbar_arrive_expect_tx(&win_full[ws], NCTA * win_tx);  // both CTAs' bytes
             uint8_t* wbuf = win + ws * C::kWinBytes;
             const int wr = row0 + r * p.Wp;
             // window rows: kTileN (<= 256, one box when SUBS_M == 2) + 8-row halo
-            if (C::kTileN == 256)
-              tma_load_2d(wbuf, &maps.act_big[tc.g], &win_full[ws], ch, wr);
-            else
-              tma_load_2d(wbuf, &maps.act_mid[tc.g], &win_full[ws], ch, wr);
-            if (k > 1)
-              tma_load_2d(wbuf + C::kTileN * 128, &maps.act_small[tc.g], &win_full[ws], ch,
-                          wr + C::kTileN);
+            const CUtensorMap* wmap = C::kTileN == 256 ? &maps.act_big[tc.g] : &maps.act_mid[tc.g];
+            if constexpr (NCTA == 2) {
+              const uint32_t fb = mapa_shared(&win_full[ws], 0);
+              tma_load_2d_pair(wbuf, wmap, fb, ch, wr);
+              if (k > 1) tma_load_2d_pair(wbuf + C::kTileN * 128, &maps.act_small[tc.g], fb, ch, wr + C::kTileN);
+            } else {
+              tma_load_2d(wbuf, wmap, &win_full[ws], ch, wr);
+              if (k > 1)
+                tma_load_2d(wbuf + C::kTileN * 128, &maps.act_small[tc.g], &win_full[ws], ch, wr + C::kTileN);
+            }
             if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
             for (int s = 0; s < k; ++s) {
               mbar_wait(&w_empty[wst], wtph ^ 1);
-              mbar_arrive_expect_tx(&w_full[wst], C::kWgtBytes);
-              tma_load_2d_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], &w_full[wst],
-                               ((r * k + s) * p.cin_chunks + c) * 64, tc.nt * N, keep);
+              if (leader) mbar_arrive_expect_tx(&w_full[wst], NCTA * C::kWgtBytes);
+              const int kx = ((r * k + s) * p.cin_chunks + c) * 64;
+              const int wrow = tc.nt * N + int(rank) * (N / NCTA);  // this CTA's half of B
+              if constexpr (NCTA == 2)
+                tma_load_2d_pair_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], mapa_shared(&w_full[wst], 0), kx,
+                                      wrow, keep);
+              else
+                tma_load_2d_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], &w_full[wst], kx, wrow, keep);
               if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
             }
           }
@@ -172,12 +189,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (elect_one()) {
-      const uint32_t idesc = idesc_bf16_f32(128, N);
+    if (leader && elect_one()) {
+      const uint32_t idesc = idesc_bf16_f32(128 * NCTA, N);
       int ws = 0, wst = 0, acc = 0;
       uint32_t wph = 0, wtph = 0, aph = 0;
       const uint32_t win_base = smem_u32(win), wgt_base = smem_u32(wgt);
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t accum) {
+        if constexpr (NCTA == 2) mma_bf16_ss_pair(d, a, b, idesc, accum);
+        else mma_bf16_ss(d, a, b, idesc, accum);
+      };
+      auto commit = [&](uint64_t* bar) {
+        if constexpr (NCTA == 2) mma_commit_pair(bar);
+        else mma_commit(bar);
+      };
+      for (int t = int(blockIdx.x) / NCTA; t < p.total_tiles; t += int(gridDim.x) / NCTA) {
         mbar_wait(&acc_empty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem + acc * C::kAccCols;
@@ -197,18 +222,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < 4; ++kk) {
                   const uint64_t ad = desc_sw128(wb + (sub * 128 + s) * 128 + kk * 32);
                   const uint64_t bd = desc_sw128(bb + kk * 32);
-                  mma_bf16_ss(d0 + sub * N, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+                  mma(d0 + sub * N, ad, bd, (first && kk == 0) ? 0u : 1u);
                 }
               }
               first = false;
-              mma_commit(&w_empty[wst]);
+              commit(&w_empty[wst]);
               if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
             }
-            mma_commit(&win_empty[ws]);
+            commit(&win_empty[ws]);
             if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
           }
         }
-        mma_commit(&acc_full[acc]);
+        commit(&acc_full[acc]);
         if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
       }
     }
@@ -228,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0, stg_i = 0;
     uint32_t aph = 0;
     const int img_rows = p.Hp * p.Wp;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+    for (int t = int(blockIdx.x) / NCTA; t < p.total_tiles; t += int(gridDim.x) / NCTA) {
       const PmTile tc = pm_decode(p, t);
       const ConvGroupParams& g = p.g[tc.g];
       float* bs = sbias + acc * N;
@@ -246,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.out);
       const int c_left = g.cout - tc.nt * N;  // live channels of this tile
       for (int sub = 0; sub < SUBS_M; ++sub) {
-        const int o = tc.pt * C::kTileN + sub * 128 + int(quad) * 32 + int(lane);
+        const int o = (tc.pt * NCTA + int(rank)) * C::kTileN + sub * 128 + int(quad) * 32 + int(lane);
         const int hh = o / p.Wp;
         const int ww = o - hh * p.Wp;
         const bool valid = hh < p.H && ww < p.W;
@@ -366,39 +391,59 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&acc_empty[acc]);
+      if constexpr (NCTA == 2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(&acc_empty[acc], 0));  // the leader's barrier
+      } else {
+        mbar_arrive(&acc_empty[acc]);
+      }
       if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
     }
     if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (NCTA == 2) cluster_sync_all();  // the leader's MMAs read peer smem until the end
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem);
+    if constexpr (NCTA == 2) tmem_dealloc_pair<kTmemCols>(tmem);
+    else tmem_dealloc<kTmemCols>(tmem);
   }
 }
 
-template <int N, int SUBS_M>
-void launch_pm(const ConvMaps& maps, const ConvParams& p, int grid, cudaStream_t stream) {
+template <int N, int SUBS_M, int NCTA>
+void launch_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
+  const int pairs = sm_count / NCTA;
+  const int grid = NCTA * (p.total_tiles < pairs ? p.total_tiles : pairs);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = PmCfg<N, SUBS_M>::total + 1024;
+  cfg.dynamicSmemBytes = PmCfg<N, SUBS_M, NCTA>::total + 1024;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (NCTA == 2) {  // the pair must share a TPC
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  check_cuda(cudaLaunchKernelEx(&cfg, conv_pm_kernel<N, SUBS_M>, maps, p), "conv_pm launch");
+  cfg.numAttrs = na;
+  check_cuda(cudaLaunchKernelEx(&cfg, conv_pm_kernel<N, SUBS_M, NCTA>, maps, p), "conv_pm launch");
 }
 
-template <int N, int SUBS_M>
+template <int N, int SUBS_M, int NCTA>
 void configure_pm() {
-  check_cuda(cudaFuncSetAttribute(conv_pm_kernel<N, SUBS_M>,
+  check_cuda(cudaFuncSetAttribute(conv_pm_kernel<N, SUBS_M, NCTA>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(PmCfg<N, SUBS_M>::total + 1024)),
+                                  int(PmCfg<N, SUBS_M, NCTA>::total + 1024)),
              "conv_pm smem attribute");
 }
 
@@ -407,21 +452,29 @@ void configure_pm() {
 int conv_pm_subs(int n_tile) { return n_tile == 256 ? 1 : 2; }  // 2 acc stages fit TMEM
 
 void conv_pm_configure() {
-  configure_pm<64, 2>();
-  configure_pm<96, 2>();
-  configure_pm<128, 2>();
-  configure_pm<256, 1>();
+  configure_pm<64, 2, 1>();
+  configure_pm<96, 2, 1>();
+  configure_pm<128, 2, 1>();
+  configure_pm<256, 1, 1>();
+  configure_pm<64, 2, 2>();
+  configure_pm<96, 2, 2>();
+  configure_pm<128, 2, 2>();
+  configure_pm<256, 1, 2>();
 }
 
 int conv_pm_tile_n(int cout) { return cout <= 64 ? 64 : cout <= 96 ? 96 : cout <= 128 ? 128 : 256; }
 
 void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
-  const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
+  const bool pair = p.ncta == 2;
   switch (p.pm_n) {
-    case 64: launch_pm<64, 2>(maps, p, grid, stream); break;
-    case 96: launch_pm<96, 2>(maps, p, grid, stream); break;
-    case 128: launch_pm<128, 2>(maps, p, grid, stream); break;
-    case 256: launch_pm<256, 1>(maps, p, grid, stream); break;
+    case 64: pair ? launch_pm<64, 2, 2>(maps, p, sm_count, stream) : launch_pm<64, 2, 1>(maps, p, sm_count, stream); break;
+    case 96: pair ? launch_pm<96, 2, 2>(maps, p, sm_count, stream) : launch_pm<96, 2, 1>(maps, p, sm_count, stream); break;
+    case 128:
+      pair ? launch_pm<128, 2, 2>(maps, p, sm_count, stream) : launch_pm<128, 2, 1>(maps, p, sm_count, stream);
+      break;
+    case 256:
+      pair ? launch_pm<256, 1, 2>(maps, p, sm_count, stream) : launch_pm<256, 1, 1>(maps, p, sm_count, stream);
+      break;
     default: fail(AVEC_ERR_UNSUPPORTED, "pixel-major conv supports N tiles of 64/96/128/256");
   }
 }

@@ -77,7 +77,8 @@ struct ConvParams {
   int out_mode;        // ConvOutMode
   int subs;            // swap-AB: 1 or 2 (tile width 256 * subs pixels)
   int pixel_major;     // 1: conv_pm.cu orientation (M = pixels, N = pm_n channels)
-  int pm_n;            // pixel-major channel tile: 64, 128 or 256
+  int pm_n;            // pixel-major channel tile: 64, 96, 128 or 256
+  int ncta;            // pixel-major: 1, or 2 = CTA pair (cta_group::2, M = 256 pixels per MMA)
   int m_tiles;         // channel tiles: ceil(cout / 128), or ceil(cout / pm_n)
   int tiles_per_image; // ceil(H*Wp / pixels per tile)
   int tile_px;         // swap-AB regular tiles: pixels per tile (<= 256 * subs, multiple of 32)

@@ -428,7 +428,21 @@ struct PlanBuilder {
       p.pm_n = conv_pm_tile_n(L0.def.cout);
       p.subs = conv_pm_subs(p.pm_n);
       p.m_tiles = (L0.def.cout + p.pm_n - 1) / p.pm_n;
-      p.tiles_per_image = (p.H * p.Wp + 128 * p.subs - 1) / (128 * p.subs);
+      // CTA pairs: M = 256 MMAs whose B half is read once per SM, relieving
+      // the shared-memory operand path (tests/native/tc2_probe.cu: N = 96 runs
+      // 49 instead of 56 cycles). Measured per layer class: a win for 3x3
+      // convs with K >= 1152 and N >= 96 (C5 dense blocks -11..-22%, VGG
+      // conv2_2/conv3_x -6..-10%), a loss for the short-K ones (conv2_1 from
+      // 64 channels, the 1x1 heads: +8..+18%). AVEC_PM2: 0 off, 1 that rule
+      // (default), 2 every pixel-major layer.
+      static const int pm2 = [] {
+        const char* e = std::getenv("AVEC_PM2");
+        return e ? std::atoi(e) : 1;
+      }();
+      const bool long_k = L0.exec_k == 3 && p.cin_chunks >= 2;
+      p.ncta = (pm2 == 2 || (pm2 == 1 && p.pm_n >= 96 && long_k)) ? 2 : 1;
+      const int px = 128 * p.subs * p.ncta;
+      p.tiles_per_image = (p.H * p.Wp + px - 1) / px;
     } else {
       p.pm_n = 0;
       p.m_tiles = L0.cout_pad / 128;
@@ -512,7 +526,7 @@ struct PlanBuilder {
       op.maps.act_small[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 8);
       op.maps.act_mid[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 128);
       op.maps.wgt[g] = make_map_2d(L.w, uint64_t(L.exec_k) * L.exec_k * L.cin_pad, L.cout_pad,
-                                   p.pixel_major ? uint32_t(p.pm_n) : 128u);
+                                   p.pixel_major ? uint32_t(p.pm_n / p.ncta) : 128u);
       op.layers[g] = layers[g];
       record_io(layers[g], in[g], out[g]);
     }
