@@ -101,7 +101,11 @@ int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, 
 
 /* Debug/parity hook: run a forward like avec_forward and copy the input and
  * output activations of conv layer `layer` (weights-blob order) as unpadded
- * fp32 NHWC (input channels in the layer's own — Caffe — channel order). */
+ * fp32 NHWC (input channels in the layer's own — Caffe — channel order).
+ * Layers whose following 2x2 max-pool is fused (conv1_2, conv2_2) report the
+ * pooled output: its pyramid level comes from avec_posenet_layer_out_level. */
+int avec_posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                                 uint32_t w, int layer, int* level);
 int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                           uint32_t w, const float* in, int layer, float* layer_in,
                           uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);

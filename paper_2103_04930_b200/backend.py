@@ -190,13 +190,24 @@ class B200Backend:
                                                    *[ctypes.byref(v) for v in vals]))
         return dict(zip(["cin", "cout", "k", "level", "relu"], [v.value for v in vals]))
 
+    def layer_out_level(self, handle: ModelHandle, dims: Dims, layer: int) -> int:
+        """Pyramid level of the layer's output as the plan stores it (one more
+        than the layer's own level when its 2x2 max-pool is fused)."""
+        lv = ctypes.c_int(0)
+        _lib.check(self._L.avec_posenet_layer_out_level(self._ctx, handle.id, dims.batch, dims.channels,
+                                                        dims.height, dims.width, layer, ctypes.byref(lv)))
+        return lv.value
+
     def layer_io(self, handle: ModelHandle, frame: Frame, layer: int):
+        """(input, output) activations of conv `layer`, unpadded fp32 NHWC; the
+        output is the pooled tensor for layers with a fused max-pool."""
         info = self.layer_info(handle, layer)
         d = frame.dims
         n_img = d.batch * d.channels // 3
         hl, wl = d.height >> info["level"], d.width >> info["level"]
+        ol = self.layer_out_level(handle, d, layer)
         lin = np.empty((n_img, hl, wl, info["cin"]), np.float32)
-        lout = np.empty((n_img, hl, wl, info["cout"]), np.float32)
+        lout = np.empty((n_img, d.height >> ol, d.width >> ol, info["cout"]), np.float32)
         data = np.ascontiguousarray(frame.data, np.float32).ravel()
         _lib.check(self._L.avec_posenet_layer_io(self._ctx, handle.id, d.batch, d.channels, d.height,
                                                  d.width, data.ctypes.data, layer, lin.ctypes.data,

@@ -165,6 +165,15 @@ int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, 
   });
 }
 
+int avec_posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                                 uint32_t w, int layer, int* level) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(level, "level");
+    *level = avec::posenet_layer_out_level(ctx, handle, n, c, h, w, layer);
+  });
+}
+
 int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                           uint32_t w, const float* in, int layer, float* layer_in,
                           uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems) {

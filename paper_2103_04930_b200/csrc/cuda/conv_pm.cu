@@ -34,14 +34,16 @@ using namespace ptx;
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
 
-template <int N, int SUBS_M, int NCTA>
+template <int N, int SUBS_M, int NCTA, bool POOL>
 struct PmCfg {
+  static_assert(!POOL || SUBS_M == 2, "pooled tiles are two rows");
   static constexpr int kTileN = 128 * SUBS_M;  // pixels per tile
-  static constexpr int kWinRows = kTileN + 8;
+  // pooled tiles read four 136-row windows (input rows y-1 .. y+2) per chunk
+  static constexpr int kWinRows = POOL ? 136 : kTileN + 8;
   static constexpr int kWinBytes = kWinRows * 128;
   // N = 64 serves the short-K high-resolution conv1_2 (and the thin heads):
   // one more window in flight keeps its HBM reads streaming
-  static constexpr int kWinStages = N == 64 ? 4 : N == 256 ? 2 : 3;
+  static constexpr int kWinStages = POOL ? 6 : N == 64 ? 4 : N == 256 ? 2 : 3;
   static constexpr int kWgtBytes = (N / NCTA) * 128;  // this CTA's N/NCTA rows x 64 bf16
   static constexpr int kAccCols = SUBS_M * N;
   static constexpr int kAccStages = 2;
@@ -83,10 +85,18 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int N, int SUBS_M, int NCTA>
+// Row-pair tile of the fused-pool mode: this CTA's rows y0, y0+1 at columns
+// x0 .. x0+127 (sub-tile s = row y0 + s)
+__device__ __forceinline__ void pool_tile(const ConvParams& p, int pt, int ncta, uint32_t rank, int& y0, int& x0) {
+  const int rp = pt / p.col_blocks;
+  y0 = (rp * ncta + int(rank)) * 2;
+  x0 = (pt - rp * p.col_blocks) * 128;
+}
+
+template <int N, int SUBS_M, int NCTA, bool POOL>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_pm_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p) {
-  using C = PmCfg<N, SUBS_M, NCTA>;
+  using C = PmCfg<N, SUBS_M, NCTA, POOL>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* win = smem + C::win;
@@ -148,41 +158,62 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t keep = policy_evict_last();
       int ws = 0, wst = 0;
       uint32_t wph = 0, wtph = 0;
-      const uint32_t win_tx = (C::kTileN + (k > 1 ? 8 : 0)) * 128;
+      const uint32_t win_tx = ((POOL ? 128 : C::kTileN) + (k > 1 ? 8 : 0)) * 128;
+      auto load_window = [&](const PmTile& tc, int ch, int wr) {
+        mbar_wait(&win_empty[ws], wph ^ 1);
+        if (leader) mbar_arrive_expect_tx(&win_full[ws], NCTA * win_tx);  // both CTAs' bytes
+        uint8_t* wbuf = win + ws * C::kWinBytes;
+        constexpr int kBox = POOL ? 128 : C::kTileN;  // + 8-row halo box
+        const CUtensorMap* wmap = kBox == 256 ? &maps.act_big[tc.g] : &maps.act_mid[tc.g];
+        if constexpr (NCTA == 2) {
+          const uint32_t fb = mapa_shared(&win_full[ws], 0);
+          tma_load_2d_pair(wbuf, wmap, fb, ch, wr);
+          if (k > 1) tma_load_2d_pair(wbuf + kBox * 128, &maps.act_small[tc.g], fb, ch, wr + kBox);
+        } else {
+          tma_load_2d(wbuf, wmap, &win_full[ws], ch, wr);
+          if (k > 1) tma_load_2d(wbuf + kBox * 128, &maps.act_small[tc.g], &win_full[ws], ch, wr + kBox);
+        }
+        if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
+      };
+      auto load_weights = [&](const PmTile& tc, int c, int r) {
+        for (int s = 0; s < k; ++s) {
+          mbar_wait(&w_empty[wst], wtph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&w_full[wst], NCTA * C::kWgtBytes);
+          const int kx = ((r * k + s) * p.cin_chunks + c) * 64;
+          const int wrow = tc.nt * N + int(rank) * (N / NCTA);  // this CTA's half of B
+          if constexpr (NCTA == 2)
+            tma_load_2d_pair_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], mapa_shared(&w_full[wst], 0), kx,
+                                  wrow, keep);
+          else
+            tma_load_2d_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], &w_full[wst], kx, wrow, keep);
+          if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
+        }
+      };
       for (int t = int(blockIdx.x) / NCTA; t < p.total_tiles; t += int(gridDim.x) / NCTA) {
         const PmTile tc = pm_decode(p, t);
+        if constexpr (POOL) {
+          // windows W_j = input rows y0-1+j (j = 0..3); filter row r of the
+          // two output rows needs W_r (row y0) and W_r+1 (row y0+1), so its
+          // weights follow W_r+1
+          int y0, x0;
+          pool_tile(p, tc.pt, NCTA, rank, y0, x0);
+          const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + y0 * p.Wp + x0;
+          for (int c = 0; c < p.cin_chunks; ++c) {
+            const int ch = p.in_c_off + c * 64;
+            for (int j = 0; j <= k; ++j) {
+              load_window(tc, ch, row0 + j * p.Wp);
+              if (j > 0) load_weights(tc, c, j - 1);
+            }
+          }
+          continue;
+        }
         const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + (tc.pt * NCTA + int(rank)) * C::kTileN;
         for (int c = 0; c < p.cin_chunks; ++c) {
           const int ch = p.in_c_off + c * 64;
           for (int r = 0; r < k; ++r) {
-            mbar_wait(&win_empty[ws], wph ^ 1);
-            if (leader) mbar_arrive_expect_tx(&win_full[ws], NCTA * win_tx);  // both CTAs' bytes
-            uint8_t* wbuf = win + ws * C::kWinBytes;
-            const int wr = row0 + r * p.Wp;
             // window rows: kTileN (<= 256, one box when SUBS_M == 2) + 8-row halo
-            const CUtensorMap* wmap = C::kTileN == 256 ? &maps.act_big[tc.g] : &maps.act_mid[tc.g];
-            if constexpr (NCTA == 2) {
-              const uint32_t fb = mapa_shared(&win_full[ws], 0);
-              tma_load_2d_pair(wbuf, wmap, fb, ch, wr);
-              if (k > 1) tma_load_2d_pair(wbuf + C::kTileN * 128, &maps.act_small[tc.g], fb, ch, wr + C::kTileN);
-            } else {
-              tma_load_2d(wbuf, wmap, &win_full[ws], ch, wr);
-              if (k > 1)
-                tma_load_2d(wbuf + C::kTileN * 128, &maps.act_small[tc.g], &win_full[ws], ch, wr + C::kTileN);
-            }
-            if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
-            for (int s = 0; s < k; ++s) {
-              mbar_wait(&w_empty[wst], wtph ^ 1);
-              if (leader) mbar_arrive_expect_tx(&w_full[wst], NCTA * C::kWgtBytes);
-              const int kx = ((r * k + s) * p.cin_chunks + c) * 64;
-              const int wrow = tc.nt * N + int(rank) * (N / NCTA);  // this CTA's half of B
-              if constexpr (NCTA == 2)
-                tma_load_2d_pair_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], mapa_shared(&w_full[wst], 0), kx,
-                                      wrow, keep);
-              else
-                tma_load_2d_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], &w_full[wst], kx, wrow, keep);
-              if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
-            }
+            load_window(tc, ch, row0 + r * p.Wp);
+            load_weights(tc, c, r);
           }
         }
       }
@@ -207,6 +238,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t d0 = tmem + acc * C::kAccCols;
         bool first = true;
+        if constexpr (POOL) {
+          // sub-tile 0 (row y0) reads W_r, sub-tile 1 (row y0+1) reads W_r+1
+          for (int c = 0; c < p.cin_chunks; ++c) {
+            mbar_wait(&win_full[ws], wph);
+            tc_fence_after();
+            for (int r = 0; r < k; ++r) {
+              const int ns = ws + 1 == C::kWinStages ? 0 : ws + 1;
+              const uint32_t nph = ws + 1 == C::kWinStages ? wph ^ 1 : wph;
+              mbar_wait(&win_full[ns], nph);
+              tc_fence_after();
+              const uint32_t wb0 = win_base + ws * C::kWinBytes, wb1 = win_base + ns * C::kWinBytes;
+              for (int s = 0; s < k; ++s) {
+                mbar_wait(&w_full[wst], wtph);
+                tc_fence_after();
+                const uint32_t bb = wgt_base + wst * C::kWgtBytes;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint64_t bd = desc_sw128(bb + kk * 32);
+                  const uint32_t accum = (first && kk == 0) ? 0u : 1u;
+                  mma(d0, desc_sw128(wb0 + s * 128 + kk * 32), bd, accum);
+                  mma(d0 + N, desc_sw128(wb1 + s * 128 + kk * 32), bd, accum);
+                }
+                first = false;
+                commit(&w_empty[wst]);
+                if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
+              }
+              commit(&win_empty[ws]);  // W_r is done
+              ws = ns;
+              wph = nph;
+            }
+            commit(&win_empty[ws]);  // W_k
+            if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
+          }
+        } else {
         for (int c = 0; c < p.cin_chunks; ++c) {
           for (int r = 0; r < k; ++r) {
             mbar_wait(&win_full[ws], wph);
@@ -233,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
           }
         }
+        }  // !POOL
         commit(&acc_full[acc]);
         if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
       }
@@ -270,122 +336,181 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.out);
       const int c_left = g.cout - tc.nt * N;  // live channels of this tile
-      for (int sub = 0; sub < SUBS_M; ++sub) {
-        const int o = (tc.pt * NCTA + int(rank)) * C::kTileN + sub * 128 + int(quad) * 32 + int(lane);
-        const int hh = o / p.Wp;
-        const int ww = o - hh * p.Wp;
-        const bool valid = hh < p.H && ww < p.W;
-        const int row_in_img = p.P * p.Wp + p.P + o;  // output row of this pixel
-        const uint32_t tbase = tmem + ((quad * 32) << 16) + acc * C::kAccCols + sub * N;
-        if (p.out_mode == kOutTmaBf16) {
-          const int row_w = row_in_img - int(lane);  // the warp's first pixel
-          // one [32 px][W ch] box: TMEM -> bias/activation/bf16 -> swizzled
-          // staging (swizzle span = box row: 16-byte chunk q of row r lands at
-          // q ^ (r & 7) for 128 B rows, q ^ ((r >> 1) & 3) for 64 B,
-          // q ^ ((r >> 2) & 1) for 32 B; 16 B rows are unswizzled) -> TMA store
-          auto box = [&](auto width, auto relu_only, int c0) {
-            constexpr int W = decltype(width)::value;
-            constexpr bool kRelu = decltype(relu_only)::value;
-            uint32_t va[W < 16 ? 16 : W > 32 ? 32 : W], vb[W == 64 ? 32 : 1];
-            if constexpr (W >= 32) {
-              tmem_ld32(tbase + c0, va);
-              if constexpr (W == 64) tmem_ld32(tbase + c0 + 32, vb);
-            } else {
-              tmem_ld16(tbase + c0, va);  // c0 + 16 <= N: N is a multiple of 16
-            }
+      if constexpr (POOL) {
+        // fused 2x2/2 max-pool: TMEM lane = column x0+32q+lane, sub-tile 0/1 =
+        // rows y0/y0+1 at columns [0,N)/[N,2N). max over the four raw sums,
+        // then bias and activation: x -> bf16(act(x + b)) is monotonic for
+        // ReLU, so this equals pooling the bf16 conv outputs bit for bit.
+        int y0, x0;
+        pool_tile(p, tc.pt, NCTA, rank, y0, x0);
+        const bool pvalid = x0 + int(quad) * 32 + int(lane) < p.W;  // W even: pairs share validity
+        const uint32_t tb0 = tmem + ((quad * 32) << 16) + acc * C::kAccCols;
+        const bool relu = g.act == 1;
+        for (int c0 = 0; c0 < N; c0 += 64) {  // cout == N (host check)
+          uint8_t* buf = stg_w + (stg_i & 1) * C::kStgBox;
+          if (lane == 0) bulk_wait_read<1>();  // the store that last read `buf` is done
+          __syncwarp();
+#pragma unroll
+          for (int hlf = 0; hlf < 2; ++hlf) {
+            uint32_t va[32], vb[32];
+            tmem_ld32(tb0 + c0 + 32 * hlf, va);
+            tmem_ld32(tb0 + N + c0 + 32 * hlf, vb);
             tmem_ld_wait();
-            uint8_t* buf = stg_w + (stg_i & 1) * C::kStgBox;
-            if (lane == 0) bulk_wait_read<1>();  // the store that last read `buf` is done
-            __syncwarp();
+            uint32_t w[16];
 #pragma unroll
-            for (int q = 0; q < W / 8; ++q) {
-              uint32_t w[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int c = q * 8 + 2 * j;  // channel within the box
-                uint32_t x0, x1;
-                if constexpr (W == 64) {
-                  x0 = q < 4 ? va[c & 31] : vb[c & 31];
-                  x1 = q < 4 ? va[(c + 1) & 31] : vb[(c + 1) & 31];
-                } else {
-                  x0 = va[c];
-                  x1 = va[c + 1];
-                }
-                float a = __uint_as_float(x0) + bs[c0 + c];
-                float b = __uint_as_float(x1) + bs[c0 + c + 1];
-                if constexpr (kRelu) {
-                  a = fmaxf(a, 0.f);
-                  b = fmaxf(b, 0.f);
-                } else {  // identity (slope 1) or PReLU
-                  a = fmaxf(a, 0.f) + sl[c0 + c] * fminf(a, 0.f);
-                  b = fmaxf(b, 0.f) + sl[c0 + c + 1] * fminf(b, 0.f);
-                }
-                w[j] = valid ? pack_bf16(a, b) : 0u;
+            for (int j = 0; j < 32; j += 2) {
+              float m0 = fmaxf(__uint_as_float(va[j]), __uint_as_float(vb[j]));
+              float m1 = fmaxf(__uint_as_float(va[j + 1]), __uint_as_float(vb[j + 1]));
+              m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+              m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+              const int c = c0 + 32 * hlf + j;
+              float a = m0 + bs[c], b = m1 + bs[c + 1];
+              if (relu) {
+                a = fmaxf(a, 0.f);
+                b = fmaxf(b, 0.f);
+              } else {
+                a = fmaxf(a, 0.f) + sl[c] * fminf(a, 0.f);
+                b = fmaxf(b, 0.f) + sl[c + 1] * fminf(b, 0.f);
               }
-              uint32_t off;
-              if constexpr (W == 64) off = lane * 128 + ((q ^ (lane & 7)) << 4);
-              else if constexpr (W == 32) off = lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4);
-              else if constexpr (W == 16) off = lane * 32 + ((q ^ ((lane >> 2) & 1)) << 4);
-              else off = lane * 16;
-              *reinterpret_cast<uint4*>(buf + off) = make_uint4(w[0], w[1], w[2], w[3]);
+              w[j / 2] = pvalid ? pack_bf16(a, b) : 0u;
             }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              const CUtensorMap* m = W == 64 ? &maps.out[tc.g]
-                                     : W == 32 ? &maps.out32[tc.g]
-                                     : W == 16 ? &maps.out16[tc.g]
-                                               : &maps.out8[tc.g];
-              tma_store_3d(m, buf, g.out_c_off + tc.nt * N + c0, row_w, tc.n);
-              bulk_commit();
-            }
-            ++stg_i;
-          };
-          using I64 = std::integral_constant<int, 64>;
-          using I32 = std::integral_constant<int, 32>;
-          using I16 = std::integral_constant<int, 16>;
-          using I8 = std::integral_constant<int, 8>;
-          auto boxes = [&](auto relu_only) {
-            if (c_left >= N) {  // full tile: compile-time box sequence
+            if ((lane & 1) == 0) {  // even lanes hold pooled column (x0 + 32q + lane) / 2
+              const uint32_t row = lane >> 1;
 #pragma unroll
-              for (int c0 = 0; c0 + 64 <= N; c0 += 64) box(I64{}, relu_only, c0);
-              if constexpr (N % 64 == 32) box(I32{}, relu_only, N - 32);
-            } else {
-              // round_up(live channels, 8) in boxes of 64/32/16/8 channels; the
-              // channels past cout (zero weights, zero bias) store zeros
-              const int c_end = (c_left + 7) & ~7;
-              int c0 = 0;
-              for (; c0 + 64 <= c_end; c0 += 64) box(I64{}, relu_only, c0);
-              if (c0 + 32 <= c_end) { box(I32{}, relu_only, c0); c0 += 32; }
-              if (c0 + 16 <= c_end) { box(I16{}, relu_only, c0); c0 += 16; }
-              if (c0 + 8 <= c_end) box(I8{}, relu_only, c0);
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t qq = 4 * hlf + q;
+                *reinterpret_cast<uint4*>(buf + row * 128 + ((qq ^ (row & 7)) << 4)) =
+                    make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+              }
             }
-          };
-          if (g.act == 1) boxes(std::true_type{});
-          else boxes(std::false_type{});
-          continue;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&maps.out_pool[tc.g], buf, g.out_c_off + tc.nt * N + c0,
+                         x0 / 2 + int(quad) * 16 + p.pool_P, y0 / 2 + p.pool_P, tc.n);
+            bulk_commit();
+          }
+          ++stg_i;
         }
-        // thin heads (38/19 channels into the stage concat) and the fp32 NCHW
-        // network output: per-channel stores of valid pixels only; lanes are
-        // consecutive pixels, so NCHW stores coalesce along W
-#pragma unroll
-        for (int c0 = 0; c0 < N; c0 += 32) {
-          if (c0 >= c_left) break;
-          uint32_t v[32];
-          tmem_ld32(tbase + c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (valid && c0 + j < c_left) {
-              float a = __uint_as_float(v[j]) + bs[c0 + j];
-              a = fmaxf(a, 0.f) + sl[c0 + j] * fminf(a, 0.f);
-              const int co = tc.nt * N + c0 + j;
-              if (p.out_mode == kOutNchwF32)
-                static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
-                                                p.H + hh) * p.W + ww] = a;
-              else
-                out[(static_cast<size_t>(tc.n) * img_rows + row_in_img) * g.out_c_stride + g.out_c_off + co] =
-                    __float2bfloat16_rn(a);
+      } else {
+        for (int sub = 0; sub < SUBS_M; ++sub) {
+          const int o = (tc.pt * NCTA + int(rank)) * C::kTileN + sub * 128 + int(quad) * 32 + int(lane);
+          const int hh = o / p.Wp;
+          const int ww = o - hh * p.Wp;
+          const bool valid = hh < p.H && ww < p.W;
+          const int row_in_img = p.P * p.Wp + p.P + o;  // output row of this pixel
+          const uint32_t tbase = tmem + ((quad * 32) << 16) + acc * C::kAccCols + sub * N;
+          if (p.out_mode == kOutTmaBf16) {
+            const int row_w = row_in_img - int(lane);  // the warp's first pixel
+            // one [32 px][W ch] box: TMEM -> bias/activation/bf16 -> swizzled
+            // staging (swizzle span = box row: 16-byte chunk q of row r lands at
+            // q ^ (r & 7) for 128 B rows, q ^ ((r >> 1) & 3) for 64 B,
+            // q ^ ((r >> 2) & 1) for 32 B; 16 B rows are unswizzled) -> TMA store
+            auto box = [&](auto width, auto relu_only, int c0) {
+              constexpr int W = decltype(width)::value;
+              constexpr bool kRelu = decltype(relu_only)::value;
+              uint32_t va[W < 16 ? 16 : W > 32 ? 32 : W], vb[W == 64 ? 32 : 1];
+              if constexpr (W >= 32) {
+                tmem_ld32(tbase + c0, va);
+                if constexpr (W == 64) tmem_ld32(tbase + c0 + 32, vb);
+              } else {
+                tmem_ld16(tbase + c0, va);  // c0 + 16 <= N: N is a multiple of 16
+              }
+              tmem_ld_wait();
+              uint8_t* buf = stg_w + (stg_i & 1) * C::kStgBox;
+              if (lane == 0) bulk_wait_read<1>();  // the store that last read `buf` is done
+              __syncwarp();
+  #pragma unroll
+              for (int q = 0; q < W / 8; ++q) {
+                uint32_t w[4];
+  #pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const int c = q * 8 + 2 * j;  // channel within the box
+                  uint32_t x0, x1;
+                  if constexpr (W == 64) {
+                    x0 = q < 4 ? va[c & 31] : vb[c & 31];
+                    x1 = q < 4 ? va[(c + 1) & 31] : vb[(c + 1) & 31];
+                  } else {
+                    x0 = va[c];
+                    x1 = va[c + 1];
+                  }
+                  float a = __uint_as_float(x0) + bs[c0 + c];
+                  float b = __uint_as_float(x1) + bs[c0 + c + 1];
+                  if constexpr (kRelu) {
+                    a = fmaxf(a, 0.f);
+                    b = fmaxf(b, 0.f);
+                  } else {  // identity (slope 1) or PReLU
+                    a = fmaxf(a, 0.f) + sl[c0 + c] * fminf(a, 0.f);
+                    b = fmaxf(b, 0.f) + sl[c0 + c + 1] * fminf(b, 0.f);
+                  }
+                  w[j] = valid ? pack_bf16(a, b) : 0u;
+                }
+                uint32_t off;
+                if constexpr (W == 64) off = lane * 128 + ((q ^ (lane & 7)) << 4);
+                else if constexpr (W == 32) off = lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4);
+                else if constexpr (W == 16) off = lane * 32 + ((q ^ ((lane >> 2) & 1)) << 4);
+                else off = lane * 16;
+                *reinterpret_cast<uint4*>(buf + off) = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                const CUtensorMap* m = W == 64 ? &maps.out[tc.g]
+                                       : W == 32 ? &maps.out32[tc.g]
+                                       : W == 16 ? &maps.out16[tc.g]
+                                                 : &maps.out8[tc.g];
+                tma_store_3d(m, buf, g.out_c_off + tc.nt * N + c0, row_w, tc.n);
+                bulk_commit();
+              }
+              ++stg_i;
+            };
+            using I64 = std::integral_constant<int, 64>;
+            using I32 = std::integral_constant<int, 32>;
+            using I16 = std::integral_constant<int, 16>;
+            using I8 = std::integral_constant<int, 8>;
+            auto boxes = [&](auto relu_only) {
+              if (c_left >= N) {  // full tile: compile-time box sequence
+  #pragma unroll
+                for (int c0 = 0; c0 + 64 <= N; c0 += 64) box(I64{}, relu_only, c0);
+                if constexpr (N % 64 == 32) box(I32{}, relu_only, N - 32);
+              } else {
+                // round_up(live channels, 8) in boxes of 64/32/16/8 channels; the
+                // channels past cout (zero weights, zero bias) store zeros
+                const int c_end = (c_left + 7) & ~7;
+                int c0 = 0;
+                for (; c0 + 64 <= c_end; c0 += 64) box(I64{}, relu_only, c0);
+                if (c0 + 32 <= c_end) { box(I32{}, relu_only, c0); c0 += 32; }
+                if (c0 + 16 <= c_end) { box(I16{}, relu_only, c0); c0 += 16; }
+                if (c0 + 8 <= c_end) box(I8{}, relu_only, c0);
+              }
+            };
+            if (g.act == 1) boxes(std::true_type{});
+            else boxes(std::false_type{});
+            continue;
+          }
+          // thin heads (38/19 channels into the stage concat) and the fp32 NCHW
+          // network output: per-channel stores of valid pixels only; lanes are
+          // consecutive pixels, so NCHW stores coalesce along W
+  #pragma unroll
+          for (int c0 = 0; c0 < N; c0 += 32) {
+            if (c0 >= c_left) break;
+            uint32_t v[32];
+            tmem_ld32(tbase + c0, v);
+            tmem_ld_wait();
+  #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (valid && c0 + j < c_left) {
+                float a = __uint_as_float(v[j]) + bs[c0 + j];
+                a = fmaxf(a, 0.f) + sl[c0 + j] * fminf(a, 0.f);
+                const int co = tc.nt * N + c0 + j;
+                if (p.out_mode == kOutNchwF32)
+                  static_cast<float*>(g.out)[((static_cast<size_t>(tc.n) * g.out_c_stride + g.out_c_off + co) *
+                                                  p.H + hh) * p.W + ww] = a;
+                else
+                  out[(static_cast<size_t>(tc.n) * img_rows + row_in_img) * g.out_c_stride + g.out_c_off + co] =
+                      __float2bfloat16_rn(a);
+              }
             }
           }
         }
@@ -411,14 +536,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int N, int SUBS_M, int NCTA>
+template <int N, int SUBS_M, int NCTA, bool POOL = false>
 void launch_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
   const int pairs = sm_count / NCTA;
   const int grid = NCTA * (p.total_tiles < pairs ? p.total_tiles : pairs);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = PmCfg<N, SUBS_M, NCTA>::total + 1024;
+  cfg.dynamicSmemBytes = PmCfg<N, SUBS_M, NCTA, POOL>::total + 1024;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -436,14 +561,14 @@ void launch_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStre
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  check_cuda(cudaLaunchKernelEx(&cfg, conv_pm_kernel<N, SUBS_M, NCTA>, maps, p), "conv_pm launch");
+  check_cuda(cudaLaunchKernelEx(&cfg, conv_pm_kernel<N, SUBS_M, NCTA, POOL>, maps, p), "conv_pm launch");
 }
 
-template <int N, int SUBS_M, int NCTA>
+template <int N, int SUBS_M, int NCTA, bool POOL = false>
 void configure_pm() {
-  check_cuda(cudaFuncSetAttribute(conv_pm_kernel<N, SUBS_M, NCTA>,
+  check_cuda(cudaFuncSetAttribute(conv_pm_kernel<N, SUBS_M, NCTA, POOL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(PmCfg<N, SUBS_M, NCTA>::total + 1024)),
+                                  int(PmCfg<N, SUBS_M, NCTA, POOL>::total + 1024)),
              "conv_pm smem attribute");
 }
 
@@ -460,12 +585,26 @@ void conv_pm_configure() {
   configure_pm<96, 2, 2>();
   configure_pm<128, 2, 2>();
   configure_pm<256, 1, 2>();
+  configure_pm<64, 2, 1, true>();
+  configure_pm<128, 2, 1, true>();
+  configure_pm<64, 2, 2, true>();
+  configure_pm<128, 2, 2, true>();
 }
 
 int conv_pm_tile_n(int cout) { return cout <= 64 ? 64 : cout <= 96 ? 96 : cout <= 128 ? 128 : 256; }
 
 void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
   const bool pair = p.ncta == 2;
+  if (p.pool) {
+    if (p.pm_n == 64)
+      pair ? launch_pm<64, 2, 2, true>(maps, p, sm_count, stream) : launch_pm<64, 2, 1, true>(maps, p, sm_count, stream);
+    else if (p.pm_n == 128)
+      pair ? launch_pm<128, 2, 2, true>(maps, p, sm_count, stream)
+           : launch_pm<128, 2, 1, true>(maps, p, sm_count, stream);
+    else
+      fail(AVEC_ERR_UNSUPPORTED, "fused pooling supports 64/128-channel tiles");
+    return;
+  }
   switch (p.pm_n) {
     case 64: pair ? launch_pm<64, 2, 2>(maps, p, sm_count, stream) : launch_pm<64, 2, 1>(maps, p, sm_count, stream); break;
     case 96: pair ? launch_pm<96, 2, 2>(maps, p, sm_count, stream) : launch_pm<96, 2, 1>(maps, p, sm_count, stream); break;

@@ -79,6 +79,12 @@ struct ConvParams {
   int pixel_major;     // 1: conv_pm.cu orientation (M = pixels, N = pm_n channels)
   int pm_n;            // pixel-major channel tile: 64, 96, 128 or 256
   int ncta;            // pixel-major: 1, or 2 = CTA pair (cta_group::2, M = 256 pixels per MMA)
+  // pixel-major with a fused 2x2/2 max-pool: tiles are [2 rows x 128 columns]
+  // per CTA (sub-tile = row), the epilogue writes the pooled row through
+  // maps.out_pool into the next level's buffer (padding pool_P)
+  int pool;
+  int pool_P;
+  int col_blocks;      // pool: ceil(W / 128)
   int m_tiles;         // channel tiles: ceil(cout / 128), or ceil(cout / pm_n)
   int tiles_per_image; // ceil(H*Wp / pixels per tile)
   int tile_px;         // swap-AB regular tiles: pixels per tile (<= 256 * subs, multiple of 32)
@@ -102,6 +108,7 @@ struct ConvMaps {
   CUtensorMap out32[kConvMaxGroups];
   CUtensorMap out16[kConvMaxGroups];
   CUtensorMap out8[kConvMaxGroups];
+  CUtensorMap out_pool[kConvMaxGroups];   // 4D [N][Hp'][Wp'][C] of the pooled level, box {64, 16, 1, 1}
 };
 
 // host side

@@ -124,6 +124,21 @@ CUtensorMap make_map_3d_store(const void* base, uint64_t cols, uint64_t rows, ui
   return m;
 }
 
+// [N][Hp][Wp][C] with [16 px][64 ch] boxes along one padded row (the fused
+// pool's output rows; boxes are clipped at the row end)
+CUtensorMap make_map_4d_store(const void* base, uint64_t C, uint64_t Wp, uint64_t Hp, uint64_t n) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {C, Wp, Hp, n};
+  cuuint64_t strides[3] = {C * 2, Wp * C * 2, Hp * Wp * C * 2};
+  cuuint32_t box[4] = {64, 16, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+                           es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled (4d store) failed: " + std::to_string(int(r)));
+  return m;
+}
+
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 // ------------------------------------------------------------------ slots
@@ -299,6 +314,22 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
   return net;
 }
 
+// CTA pairs: M = 256 MMAs whose B half is read once per SM, relieving the
+// shared-memory operand path (tests/native/tc2_probe.cu: N = 96 runs 49
+// instead of 56 cycles). Measured per layer class: a win for 3x3 convs with
+// K >= 1152 and N >= 96 (C5 dense blocks -11..-22%, VGG conv2_2/conv3_x
+// -6..-10%), a loss for the short-K ones (conv2_1 from 64 channels, the 1x1
+// heads: +8..+18%). AVEC_PM2: 0 off, 1 that rule (default), 2 every
+// pixel-major layer.
+int pm_ncta(int pm_n, int exec_k, int cin_chunks) {
+  static const int pm2 = [] {
+    const char* e = std::getenv("AVEC_PM2");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool long_k = exec_k == 3 && cin_chunks >= 2;
+  return (pm2 == 2 || (pm2 == 1 && pm_n >= 96 && long_k)) ? 2 : 1;
+}
+
 struct PlanBuilder {
   Plan& plan;
   const PoseNet& net;
@@ -376,9 +407,38 @@ struct PlanBuilder {
     plan.ops.push_back(op);
   }
 
-  // one launch covering 1 or 2 conv layers (sibling branches) of equal shape
+  // A 3x3 ReLU conv writing all of a 64/128-channel buffer that only a 2x2
+  // max-pool reads: run it with the pool fused into its epilogue (conv_pm.cu
+  // POOL tiles) and skip the full-resolution tensor. AVEC_POOLFUSE=0 disables.
+  bool pool_fusable(int layer, int level) const {
+    static const bool on = [] {
+      const char* e = std::getenv("AVEC_POOLFUSE");
+      return !(e && e[0] == '0');
+    }();
+    const ConvLayerDev& L = net.layers[layer];
+    if (!on || L.exec_k != 3 || L.def.act != kActRelu || (L.def.cout != 64 && L.def.cout != 128)) return false;
+    const Geometry& g = plan.geo[level];
+    const int ncta = pm_ncta(L.def.cout, L.exec_k, L.cin_pad / 64);
+    return g.H % (2 * ncta) == 0 && g.W % 2 == 0;
+  }
+
+  // conv `layer` from `in`, then 2x2/2 max-pool into buffer `pooled` (level + 1)
+  void conv_pool(int layer, TensorView in, int pooled) {
+    const int level = in.level;
+    const int cout = net.layers[layer].def.cout;
+    if (pool_fusable(layer, level)) {
+      conv({layer}, {in}, {view(pooled, 0, cout)}, true);
+    } else {
+      const int full = buffer(level, cout);
+      conv({layer}, {in}, {view(full, 0, cout)});
+      pool(full, pooled);
+    }
+  }
+
+  // one launch covering 1 or 2 conv layers (sibling branches) of equal shape;
+  // `pool`: the single output view is the 2x2-pooled result (level + 1)
   void conv(std::initializer_list<int> layers_il, std::initializer_list<TensorView> ins,
-            std::initializer_list<TensorView> outs) {
+            std::initializer_list<TensorView> outs, bool pool = false) {
     std::vector<int> layers(layers_il);
     std::vector<TensorView> in(ins), out(outs);
     PlanOp op;
@@ -408,7 +468,7 @@ struct PlanBuilder {
       return e ? std::atoi(e) : 0;
     }();
     const bool want_tc = L0.exec_k == 7 || (tc3 && L0.exec_k == 3 && L0.def.cout == 128 && L0.cin_pad >= 128);
-    bool tc_ok = want_tc && !to_output;
+    bool tc_ok = want_tc && !to_output && !pool;
     for (size_t g = 0; g < layers.size(); ++g)
       tc_ok = tc_ok && out[g].c_off % 8 == 0 && out[g].level == in[g].level;
     p.pixel_major = tc_ok ? 0 : 1;
@@ -421,28 +481,26 @@ struct PlanBuilder {
     for (size_t g = 0; g < layers.size(); ++g) {
       const int cout = net.layers[layers[g]].def.cout;
       slab = slab && (p.pixel_major || cout % 64 == 0) && out[g].c_off % 8 == 0 &&
-             out[g].c_off + round_up(cout, 8) <= out[g].c_stride && out[g].level == in[g].level;
+             out[g].c_off + round_up(cout, 8) <= out[g].c_stride && out[g].level == in[g].level + (pool ? 1 : 0);
     }
+    if (pool && (!slab || layers.size() != 1 || !p.pixel_major))
+      fail(AVEC_ERR_UNSUPPORTED, "fused pooling needs one pixel-major slab output");
     p.out_mode = to_output ? kOutNchwF32 : slab ? kOutTmaBf16 : kOutDirectBf16;
     if (p.pixel_major) {
       p.pm_n = conv_pm_tile_n(L0.def.cout);
       p.subs = conv_pm_subs(p.pm_n);
       p.m_tiles = (L0.def.cout + p.pm_n - 1) / p.pm_n;
-      // CTA pairs: M = 256 MMAs whose B half is read once per SM, relieving
-      // the shared-memory operand path (tests/native/tc2_probe.cu: N = 96 runs
-      // 49 instead of 56 cycles). Measured per layer class: a win for 3x3
-      // convs with K >= 1152 and N >= 96 (C5 dense blocks -11..-22%, VGG
-      // conv2_2/conv3_x -6..-10%), a loss for the short-K ones (conv2_1 from
-      // 64 channels, the 1x1 heads: +8..+18%). AVEC_PM2: 0 off, 1 that rule
-      // (default), 2 every pixel-major layer.
-      static const int pm2 = [] {
-        const char* e = std::getenv("AVEC_PM2");
-        return e ? std::atoi(e) : 1;
-      }();
-      const bool long_k = L0.exec_k == 3 && p.cin_chunks >= 2;
-      p.ncta = (pm2 == 2 || (pm2 == 1 && p.pm_n >= 96 && long_k)) ? 2 : 1;
-      const int px = 128 * p.subs * p.ncta;
-      p.tiles_per_image = (p.H * p.Wp + px - 1) / px;
+      p.ncta = pm_ncta(p.pm_n, L0.exec_k, p.cin_chunks);
+      if (pool) {
+        // [2 rows x 128 columns] per CTA; the pair stacks its two row pairs
+        p.pool = 1;
+        p.pool_P = plan.geo[in[0].level + 1].P;
+        p.col_blocks = (p.W + 127) / 128;
+        p.tiles_per_image = p.H / (2 * p.ncta) * p.col_blocks;
+      } else {
+        const int px = 128 * p.subs * p.ncta;
+        p.tiles_per_image = (p.H * p.Wp + px - 1) / px;
+      }
     } else {
       p.pm_n = 0;
       p.m_tiles = L0.cout_pad / 128;
@@ -501,7 +559,11 @@ struct PlanBuilder {
       if (L.exec_k != p.k || L.cin_pad != L0.cin_pad || L.cout_pad != L0.cout_pad ||
           in[g].c_off != p.in_c_off || (out[g].buf == -1) != to_output)
         fail(AVEC_ERR_INVALID_MODEL, "grouped conv layers differ in shape");
-      if (p.out_mode == kOutTmaBf16) {
+      if (pool) {
+        const int ob = out[g].buf;
+        const Geometry& go = plan.geo[in[g].level + 1];
+        op.maps.out_pool[g] = make_map_4d_store(plan.bufs[ob]->p, plan.buf_c[ob], go.Wp(), go.Hp(), plan.n);
+      } else if (p.out_mode == kOutTmaBf16) {
         const int ob = out[g].buf;
         op.maps.out[g] = make_map_3d_store(plan.bufs[ob]->p, plan.buf_c[ob], uint64_t(gi.Hp()) * gi.Wp(),
                                            plan.n);
@@ -549,15 +611,13 @@ struct PlanBuilder {
 int build_trunk(PlanBuilder& b, Plan& plan, int cat, int trunk_off) {
   int li = 0;
   // level 0
-  const int a0 = b.buffer(0, 64), b0 = b.buffer(0, 64);
+  const int a0 = b.buffer(0, 64);
   b.first(li++, b.view(a0, 0, 64));  // conv1_1 fused with the frame conversion
-  b.conv({li++}, {b.view(a0, 0, 64)}, {b.view(b0, 0, 64)});  // conv1_2
-  const int p1 = b.buffer(1, 64), a1 = b.buffer(1, 128), b1 = b.buffer(1, 128);
-  b.pool(b0, p1);
+  const int p1 = b.buffer(1, 64), a1 = b.buffer(1, 128);
+  b.conv_pool(li++, b.view(a0, 0, 64), p1);  // conv1_2 + pool1
   b.conv({li++}, {b.view(p1, 0, 64)}, {b.view(a1, 0, 128)});   // conv2_1
-  b.conv({li++}, {b.view(a1, 0, 128)}, {b.view(b1, 0, 128)});  // conv2_2
   const int p2 = b.buffer(2, 128), a2 = b.buffer(2, 256), b2 = b.buffer(2, 256);
-  b.pool(b1, p2);
+  b.conv_pool(li++, b.view(a1, 0, 128), p2);  // conv2_2 + pool2
   b.conv({li++}, {b.view(p2, 0, 128)}, {b.view(a2, 0, 256)});  // conv3_1
   b.conv({li++}, {b.view(a2, 0, 256)}, {b.view(b2, 0, 256)});  // conv3_2
   b.conv({li++}, {b.view(b2, 0, 256)}, {b.view(a2, 0, 256)});  // conv3_3
@@ -967,11 +1027,28 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
       const double px = double(n_img) * (h >> d.level) * (w >> d.level);
       p.flops += 2.0 * px * d.cin * d.cout * d.k * d.k;
       const double in_b = op.kind == PlanOp::kFirst ? 4.0 : 2.0;  // fp32 frame or bf16 act
-      const bool final_out = plan->layer_out[op.layers[g]].buf == -1;
-      p.bytes += px * (d.cin * in_b + d.cout * (final_out ? 4.0 : 2.0));
+      const TensorView& ov = plan->layer_out[op.layers[g]];
+      const bool final_out = ov.buf == -1;
+      const double out_px = ov.level > d.level ? px / 4 : px;  // fused 2x2 pool
+      p.bytes += px * d.cin * in_b + out_px * d.cout * (final_out ? 4.0 : 2.0);
     }
   }
   return prof;
+}
+
+int posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                            int layer) {
+  const Model m = model_lookup(ctx, handle);
+  if (m.kind != AVEC_MODEL_POSENET) fail(AVEC_ERR_INVALID_ARGUMENT, "not a pose net");
+  int n_img = 0;
+  posenet_shape(m, n, c, h, w, n_img);
+  const PoseFamily& f = m.net->fam;
+  if (layer < 0 || layer >= int(f.convs.size())) fail(AVEC_ERR_INVALID_ARGUMENT, "layer index");
+  check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+  SlotLease lease(ctx);
+  Plan* plan = get_plan(ctx, lease.slot(), m, n_img, int(h), int(w));
+  const TensorView& v = plan->layer_out[layer];
+  return v.buf >= 0 ? v.level : f.convs[layer].level;
 }
 
 void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
@@ -984,15 +1061,16 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
   const PoseFamily& f = m.net->fam;
   if (layer < 0 || layer >= int(f.convs.size())) fail(AVEC_ERR_INVALID_ARGUMENT, "layer index");
   const ConvDef& d = f.convs[layer];
-  const int Hl = int(h) >> d.level, Wl = int(w) >> d.level;
-  const uint64_t need_in = uint64_t(n_img) * Hl * Wl * d.cin;
-  const uint64_t need_out = uint64_t(n_img) * Hl * Wl * d.cout;
-  if (layer_in_elems != need_in || layer_out_elems != need_out)
-    fail(AVEC_ERR_INVALID_ARGUMENT, "layer buffers have the wrong size");
   check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
   SlotLease lease(ctx);
   Slot* s = lease.slot();
   Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
+  // the output view is one level down when the layer's 2x2 pool is fused
+  const int out_level = plan->layer_out[layer].buf >= 0 ? plan->layer_out[layer].level : d.level;
+  const uint64_t need_in = uint64_t(n_img) * (int(h) >> d.level) * (int(w) >> d.level) * d.cin;
+  const uint64_t need_out = uint64_t(n_img) * (int(h) >> out_level) * (int(w) >> out_level) * d.cout;
+  if (layer_in_elems != need_in || layer_out_elems != need_out)
+    fail(AVEC_ERR_INVALID_ARGUMENT, "layer buffers have the wrong size");
   const uint64_t E = uint64_t(n) * c * h * w;
   check_cuda(cudaMemcpy(plan->in.p, in, E * 4, cudaMemcpyHostToDevice), "H2D");
   size_t last = 0;
@@ -1002,7 +1080,9 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
   check_cuda(cudaStreamSynchronize(s->stream), "layer io sync");
   // `map`: Caffe channel -> channel inside the view's window (stage inputs)
   auto fetch = [&](const TensorView& v, int cdim, float* dst, const std::vector<int>& map) {
-    const Geometry& g = plan->geo[d.level];
+    const int lv = v.buf >= 0 ? v.level : d.level;
+    const Geometry& g = plan->geo[lv];
+    const int Hl = int(h) >> lv, Wl = int(w) >> lv;
     if (v.buf == -2) {  // network input as the first layer sees it: bf16(x - 0.5), NHWC
       for (int b = 0; b < n_img; ++b)
         for (int y = 0; y < Hl; ++y)

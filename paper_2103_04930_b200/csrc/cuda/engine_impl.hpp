@@ -155,6 +155,10 @@ struct OpProfile {
 };
 std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c,
                                        uint32_t h, uint32_t w, const float* d_in, int reps);
+// pyramid level of a layer's output view: its own level, or one more when
+// the plan fuses the following 2x2 max-pool into it
+int posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                            int layer);
 void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                       uint32_t w, const float* in, int layer, float* layer_in,
                       uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);

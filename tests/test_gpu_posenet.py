@@ -48,6 +48,8 @@ def check_layer(net, i):
     w, b, sl = net["wb"][i]
     final = i in net.get("final_layers", ()) or (L.name.startswith("Mconv7") and "stage6" in L.name)
     ref = O.conv2d_nhwc(lin, w, b, relu=L.act, round_bf16=not final, slope=sl)
+    if lout.shape[1] * 2 == lin.shape[1]:  # the plan fuses this layer's 2x2 max-pool
+        ref = O.maxpool2_nhwc(ref)
     err = np.linalg.norm(lout - ref) / max(np.linalg.norm(ref), 1e-30)
     assert err <= 1e-3, (L.name, err)
     if not final:
@@ -74,9 +76,26 @@ def test_all_layers_parity(net):
 def test_maxpool_exact(net):
     be, h = net["be"], net["h"]
     for before, after in ((1, 2), (3, 4), (7, 8)):  # conv1_2->conv2_1, conv2_2->conv3_1, conv3_4->conv4_1
-        _, out_prev = be.layer_io(h, net["frame"], before)
+        lin, out_prev = be.layer_io(h, net["frame"], before)
         in_next, _ = be.layer_io(h, net["frame"], after)
-        assert np.array_equal(O.maxpool2_nhwc(out_prev), in_next)
+        if out_prev.shape[1] * 2 == lin.shape[1]:  # pool fused into the conv epilogue
+            assert np.array_equal(out_prev, in_next)
+        else:
+            assert np.array_equal(O.maxpool2_nhwc(out_prev), in_next)
+
+
+def test_fused_pool_equals_pool_of_conv(net):
+    """The fused conv+pool epilogue pools the raw sums before bias/ReLU/bf16;
+    monotonicity makes that bit-identical to pooling the unfused conv output.
+    Checked on conv1_2 / conv2_2 against the oracle conv + bf16 + maxpool."""
+    be, h = net["be"], net["h"]
+    for i in (1, 3):
+        lin, lout = be.layer_io(h, net["frame"], i)
+        assert lout.shape[1] * 2 == lin.shape[1], "pool not fused"
+        w, b, sl = net["wb"][i]
+        ref = O.maxpool2_nhwc(O.conv2d_nhwc(lin, w, b, relu=1, round_bf16=True))
+        tol = ulp_bf16(ref) + 1e-4 * float(np.abs(ref).max())
+        assert not (np.abs(lout - ref) > tol).any()
 
 
 def test_forward_output_layout_and_determinism(net):
