@@ -127,7 +127,10 @@ int avec_posenet_num_layers(avec_ctx* ctx, uint64_t handle, int* n_layers);
 int avec_posenet_synth_weights(const uint8_t* structure, size_t structure_len, float* out,
                                uint64_t* out_floats);
 
-/* Pinned (page-locked, portable) host memory for zero-copy ingest/egress. */
+/* Pinned (page-locked, portable) host memory for zero-copy ingest/egress.
+ * Blocks are pooled: a freed block is kept (up to 8 GiB) and reused by later
+ * allocations, so sessions opening and closing never call cudaFreeHost (which
+ * synchronises the device) while other sessions' cycles are in flight. */
 void* avec_host_alloc(uint64_t bytes);
 void avec_host_free(void* p);
 

@@ -3,9 +3,13 @@
 // AVEC_* code plus a thread-local message.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "engine_impl.hpp"
@@ -34,6 +38,72 @@ int guarded(F&& f) {
 
 void need(const void* p, const char* what) {
   if (!p) avec::fail(AVEC_ERR_INVALID_ARGUMENT, std::string(what) + " is NULL");
+}
+
+// Pinned host memory is pooled. cudaFreeHost synchronises the device, so a
+// session closing mid-run used to stall every other session's cycle (measured
+// 400-520 ms communication spikes through avec-server with 4 clients);
+// cudaHostAlloc of a frame-sized buffer costs milliseconds of page locking.
+// Freed blocks (2 MiB granules) are kept for reuse up to kCacheBytes and
+// handed out best-fit.
+class HostPool {
+ public:
+  static constexpr uint64_t kGranule = 2ull << 20;
+  static constexpr uint64_t kCacheBytes = 8ull << 30;
+
+  void* take(uint64_t bytes) {
+    const uint64_t sz = (std::max<uint64_t>(bytes, 1) + kGranule - 1) / kGranule * kGranule;
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      auto it = free_.lower_bound(sz);
+      if (it != free_.end() && it->first <= 2 * sz) {  // best fit, at most 2x the request
+        void* p = it->second;
+        cached_ -= it->first;
+        live_[p] = it->first;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, sz, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(m_);
+    live_[p] = sz;
+    return p;
+  }
+
+  void give(void* p) {
+    if (!p) return;
+    std::unique_lock<std::mutex> lk(m_);
+    auto it = live_.find(p);
+    if (it == live_.end()) {  // not ours: plain pinned free
+      lk.unlock();
+      cudaFreeHost(p);
+      return;
+    }
+    const uint64_t sz = it->second;
+    live_.erase(it);
+    if (cached_ + sz <= kCacheBytes) {
+      free_.emplace(sz, p);
+      cached_ += sz;
+      return;
+    }
+    lk.unlock();
+    cudaFreeHost(p);
+  }
+
+ private:
+  std::mutex m_;
+  std::multimap<uint64_t, void*> free_;
+  std::unordered_map<void*, uint64_t> live_;
+  uint64_t cached_ = 0;
+};
+
+HostPool& host_pool() {
+  static HostPool* pool = new HostPool;  // never destroyed: blocks outlive static teardown order
+  return *pool;
 }
 
 }  // namespace
@@ -248,17 +318,11 @@ int avec_posenet_synth_weights(const uint8_t* structure, size_t structure_len, f
 }
 
 void* avec_host_alloc(uint64_t bytes) {
-  void* p = nullptr;
-  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
-    cudaGetLastError();
-    g_last_error = "cudaHostAlloc failed";
-    return nullptr;
-  }
+  void* p = host_pool().take(bytes);
+  if (!p) g_last_error = "cudaHostAlloc failed";
   return p;
 }
 
-void avec_host_free(void* p) {
-  if (p) cudaFreeHost(p);
-}
+void avec_host_free(void* p) { host_pool().give(p); }
 
 }  // extern "C"

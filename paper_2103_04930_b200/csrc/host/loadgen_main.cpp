@@ -2,6 +2,7 @@
 // reporting through-the-wire frames/s (BASELINE configs C2/C4). Frames follow
 // the reference harness generator (proj/src/harness.cpp:29-42: seed_seq{lo32,
 // hi32, index} -> mt19937_64, top 24 bits / 2^24), batch folded into channels.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -106,6 +107,8 @@ int main(int argc, char** argv) {
   std::atomic<int> ready{0};
   std::atomic<bool> go{false};
   std::vector<double> busy(clients, 0.0), compute(clients, 0.0);
+  // per-cycle wall / communication / gpu seconds of every client (tail diagnostics)
+  std::vector<std::vector<double>> cyc(clients), comm(clients), gpu(clients);
   std::vector<std::string> errs(clients);
   std::vector<std::thread> th;
   for (unsigned c = 0; c < clients; ++c) {
@@ -123,6 +126,9 @@ int main(int argc, char** argv) {
         for (unsigned i = 0; i < steps; ++i) {
           const record::CycleTiming t = s.forward_timed(frames[c].data(), elems, width, height, out);
           compute[c] += t.compute_s;
+          cyc[c].push_back(t.communication_s + t.gpu_s + t.other_s);
+          comm[c].push_back(t.communication_s);
+          gpu[c].push_back(t.gpu_s);
           if (c == 0) rec.record(t);
         }
         busy[c] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -159,10 +165,26 @@ int main(int argc, char** argv) {
   }
   double cs = 0;
   for (double v : compute) cs += v;
+  std::vector<double> all, allc, allg;
+  for (unsigned c = 0; c < clients; ++c) {
+    all.insert(all.end(), cyc[c].begin(), cyc[c].end());
+    allc.insert(allc.end(), comm[c].begin(), comm[c].end());
+    allg.insert(allg.end(), gpu[c].begin(), gpu[c].end());
+  }
+  auto pct = [](std::vector<double> v, double q) {
+    if (v.empty()) return 0.0;
+    std::sort(v.begin(), v.end());
+    return v[std::min(v.size() - 1, std::size_t(q * double(v.size())))];
+  };
   const double frames_total = double(steps) * batch * clients;
   std::printf("{\"ok\": true, \"clients\": %u, \"steps\": %u, \"batch\": %u, \"frames\": %.0f, \"wall_s\": %.6f, "
-              "\"fps\": %.3f, \"ms_per_cycle\": %.4f, \"server_compute_ms\": %.4f, \"model\": \"%s\"}\n",
+              "\"fps\": %.3f, \"ms_per_cycle\": %.4f, \"server_compute_ms\": %.4f, \"model\": \"%s\", "
+              "\"cycle_ms\": {\"p50\": %.3f, \"p90\": %.3f, \"max\": %.3f}, "
+              "\"comm_ms\": {\"p50\": %.3f, \"p90\": %.3f, \"max\": %.3f}, "
+              "\"gpu_ms\": {\"p50\": %.3f, \"p90\": %.3f, \"max\": %.3f}}\n",
               clients, steps, batch, frames_total, wall, frames_total / wall, 1e3 * wall / steps,
-              1e3 * cs / (double(steps) * clients), model.c_str());
+              1e3 * cs / (double(steps) * clients), model.c_str(), 1e3 * pct(all, 0.5), 1e3 * pct(all, 0.9),
+              1e3 * pct(all, 1.0), 1e3 * pct(allc, 0.5), 1e3 * pct(allc, 0.9), 1e3 * pct(allc, 1.0),
+              1e3 * pct(allg, 0.5), 1e3 * pct(allg, 0.9), 1e3 * pct(allg, 1.0));
   return 0;
 }
