@@ -49,6 +49,14 @@ CONFIGS = {
 }
 CFG = CONFIGS["c2"]
 W, H, BATCH = CFG["width"], CFG["height"], CFG["global_batch"]  # BATCH = frames per rank per step
+# Execution slots per GPU = cycles in flight. Measured (profiles/README.md):
+# device-resident throughput saturates at 2 streams, the e2e C-ABI path gains
+# from a third slot (its H2D/D2H overlap the other two cycles' kernels: C2
+# +3.4%, C5 +4%), and through the wire 2 server slots beat 3-4 (host-side TCP
+# work per extra concurrent cycle). AVEC_SLOTS / AVEC_WIRE_SLOTS override.
+SLOTS = int(os.environ.get("AVEC_SLOTS", "3"))          # avec_ctx slots (e2e threads up to this)
+DEV_STREAMS = 2                                        # cycles in flight for the device-resident value
+WIRE_SLOTS = int(os.environ.get("AVEC_WIRE_SLOTS", "2"))
 
 
 def load_peaks() -> dict:
@@ -168,7 +176,7 @@ def wire_run(device: int, steps: int, clients: int) -> dict:
     native sessions over TCP loopback (BASELINE "through AVEC server")."""
     server = ROOT / "paper_2103_04930_b200" / "bin" / "avec-server"
     loadgen = ROOT / "paper_2103_04930_b200" / "bin" / "avec-loadgen"
-    p = subprocess.Popen([str(server), "--devices", str(device), "--slots", "2"], stdout=subprocess.PIPE,
+    p = subprocess.Popen([str(server), "--devices", str(device), "--slots", str(WIRE_SLOTS)], stdout=subprocess.PIPE,
                          stderr=subprocess.PIPE, text=True)
     try:
         line = p.stdout.readline()
@@ -180,7 +188,7 @@ def wire_run(device: int, steps: int, clients: int) -> dict:
                             "--warmup", "2", "--batch", str(BATCH), "--width", str(W), "--height", str(H),
                             "--model", model], capture_output=True, text=True, timeout=900)
         out = json.loads(r.stdout.strip().splitlines()[-1])
-        out["transport"] = "TCP loopback, native client (bin/avec-loadgen), avec-server --slots 2"
+        out["transport"] = f"TCP loopback, native client (bin/avec-loadgen), avec-server --slots {WIRE_SLOTS}"
         return out
     except Exception as e:  # noqa: BLE001
         return {"ok": False, "error": str(e)}
@@ -201,7 +209,8 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
 
     dev = local_rank
     torch.cuda.set_device(dev)
-    be = B200Backend(dev, slots=2)
+    S = DEV_STREAMS
+    be = B200Backend(dev, slots=SLOTS)
     model = make_model(CFG["family"], netspec.spec(CFG["family"]), b"", CFG["divisor"])
     h = be.register_model(model)
     dims = Dims(1, 3 * BATCH, H, W)
@@ -215,17 +224,17 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     host_frames = [(rng.integers(0, 1 << 24, E, dtype=np.int64) * (1.0 / (1 << 24))).astype(np.float32)
                    for _ in range(n_rot)]
     d_in = [torch.from_numpy(f).to(f"cuda:{dev}") for f in host_frames]
-    d_out = [torch.empty(K, dtype=torch.float32, device=f"cuda:{dev}") for _ in range(2)]
-    # two cycles in flight, like the server's two execution slots
-    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    d_out = [torch.empty(K, dtype=torch.float32, device=f"cuda:{dev}") for _ in range(S)]
+    # S cycles in flight, like the server's S execution slots per GPU
+    streams = [torch.cuda.Stream(device=dev) for _ in range(S)]
 
     if world > 1:
         dist.barrier()
 
     # ---------------- device-resident throughput (value) ----------------
     def step(i):
-        be.forward_device(h, dims, d_in[i % n_rot].data_ptr(), d_out[i % 2].data_ptr(),
-                          streams[i % 2].cuda_stream)
+        be.forward_device(h, dims, d_in[i % n_rot].data_ptr(), d_out[i % S].data_ptr(),
+                          streams[i % S].cuda_stream)
 
     for i in range(args.warmup):
         step(i)
@@ -234,14 +243,16 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev_b = torch.cuda.Event()
     with ClockSampler(dev) as clocks:
         ev0.record(streams[0])
-        streams[1].wait_event(ev0)
+        for st in streams[1:]:
+            st.wait_event(ev0)
         for i in range(args.steps):
             step(i)
-        ev_b.record(streams[1])
-        streams[0].wait_event(ev_b)
+        for st in streams[1:]:
+            ev_b = torch.cuda.Event()
+            ev_b.record(st)
+            streams[0].wait_event(ev_b)
         ev1.record(streams[0])
         torch.cuda.synchronize()
     dev_ms = ev0.elapsed_time(ev1)
@@ -255,15 +266,20 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     value = frames_total / (dev_ms / 1e3)
 
     # ---------------- e2e through avec_forward with pinned host buffers ----------------
-    pin_in = [PinnedBuffer(E) for _ in range(2)]
-    pin_out = [PinnedBuffer(K) for _ in range(2)]
-    for j in range(2):
-        pin_in[j].array[:] = host_frames[j]
+    T = SLOTS  # host threads at most, one cycle per slot
+    pin_in = [PinnedBuffer(E) for _ in range(T)]
+    pin_out = [PinnedBuffer(K) for _ in range(T)]
+    for j in range(T):
+        pin_in[j].array[:] = host_frames[j % n_rot]
     from paper_2103_04930_b200 import Frame
-    frames = [Frame(dims, pin_in[j].array) for j in range(2)]
-    for j in range(2):  # warm both slots' plans
-        be.forward(h, frames[j], out=pin_out[j].array)
-    checksum = [0.0, 0.0]
+    frames = [Frame(dims, pin_in[j].array) for j in range(T)]
+    warm = [threading.Thread(target=be.forward, args=(h, frames[j]), kwargs={"out": pin_out[j].array})
+            for j in range(T)]
+    for t in warm:  # concurrent, so every slot builds its plan
+        t.start()
+    for t in warm:
+        t.join()
+    checksum = [0.0] * T
 
     def worker(j, n):
         s = 0.0
@@ -289,8 +305,8 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
             s = float(t.item())
         return frames_total / s
 
-    # one client thread (synchronous cycles) and two (the server's two slots in flight)
-    e2e_by_threads = {1: e2e_run(1), 2: e2e_run(2)}
+    # one host thread (synchronous cycles) up to one per slot
+    e2e_by_threads = {t: e2e_run(t) for t in range(1, T + 1)}
     e2e_threads = max(e2e_by_threads, key=e2e_by_threads.get)
     e2e = e2e_by_threads[e2e_threads]
 
@@ -374,7 +390,7 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
                        "l2": "4 rotating input buffers; per-step activation working set >> 126 MB L2"},
             "e2e": {"value": round(e2e, 2), "unit": "frames/s", "h2d_bytes_per_step": E * 4,
                     "d2h_bytes_per_step": K * 4,
-                    "api": f"avec_forward (pinned host buffers), {e2e_threads} host thread(s) over 2 slots",
+                    "api": f"avec_forward (pinned host buffers), {e2e_threads} host thread(s) over {SLOTS} slots",
                     "by_threads": {str(k): round(v, 2) for k, v in e2e_by_threads.items()}},
             "wire": wire,
             "pdl": os.environ.get("AVEC_PDL", "0") == "1",
