@@ -144,3 +144,40 @@ def nms_plane(x: np.ndarray, threshold: float, max_peaks: int):
     sc = np.zeros(max_peaks, np.float32)
     n = lib().oracle_nms_plane(np.ascontiguousarray(x, np.float32), h, w, threshold, max_peaks, xy, ref, sc)
     return xy[: 2 * n].reshape(n, 2), ref[: 2 * n].reshape(n, 2), sc[:n]
+
+
+def coco_chain(frames_nchw: np.ndarray, layers, wb) -> np.ndarray:
+    """Whole COCO pose net on the oracle (bf16 rounding after every layer, as
+    the device stores activations), from NCHW fp32 frames [N,3,H,W] to the
+    wire output [N][19 heat | 38 PAF][H/8][W/8] flattened."""
+    x = bf16_round(frames_nchw.transpose(0, 2, 3, 1) - 0.5)
+
+    def conv(t, idx, final=False):
+        w, b, _ = wb[idx]
+        return conv2d_nhwc(t, w, b, relu=layers[idx].act, round_bf16=not final)
+
+    cur = conv(x, 0)
+    cur = maxpool2_nhwc(conv(cur, 1))
+    cur = conv(cur, 2)
+    cur = maxpool2_nhwc(conv(cur, 3))
+    for j in (4, 5, 6, 7):
+        cur = conv(cur, j)
+    cur = maxpool2_nhwc(cur)
+    for j in (8, 9, 10, 11):
+        cur = conv(cur, j)
+    trunk = l1 = l2 = cur
+    for j in range(12, 17):
+        l1 = conv(l1, j)
+    for j in range(17, 22):
+        l2 = conv(l2, j)
+    idx = 22
+    for t in range(2, 7):
+        cat = np.concatenate([l1, l2, trunk], axis=3)
+        a, b_ = cat, cat
+        for j in range(7):
+            a = conv(a, idx + j, final=(t == 6 and j == 6))
+        for j in range(7):
+            b_ = conv(b_, idx + 7 + j, final=(t == 6 and j == 6))
+        l1, l2 = a, b_
+        idx += 14
+    return np.concatenate([l2, l1], axis=3).transpose(0, 3, 1, 2).ravel()

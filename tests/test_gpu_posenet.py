@@ -126,40 +126,7 @@ def test_inline_weights_equal_seeded(net):
 def test_end_to_end_against_oracle_chain(net):
     """Whole net on the oracle from the raw frame (bf16 rounding at every layer).
     Rounding flips propagate, so the tolerance is 2e-2 relative on the net output."""
-    from paper_2103_04930_b200 import netspec
-    layers, wb = net["layers"], net["wb"]
-    x = O.bf16_round(net["frame"].data.reshape(NB, 3, H, W).transpose(0, 2, 3, 1) - 0.5)
-    acts = {}
-    cur = x
-    i = 0
-    def conv(t, idx, final=False):
-        w, b, _ = wb[idx]
-        return O.conv2d_nhwc(t, w, b, relu=layers[idx].act, round_bf16=not final)
-    cur = conv(cur, 0); cur = conv(cur, 1); cur = O.maxpool2_nhwc(cur)
-    cur = conv(cur, 2); cur = conv(cur, 3); cur = O.maxpool2_nhwc(cur)
-    for j in (4, 5, 6, 7):
-        cur = conv(cur, j)
-    cur = O.maxpool2_nhwc(cur)
-    for j in (8, 9, 10, 11):
-        cur = conv(cur, j)
-    trunk = cur
-    l1 = trunk
-    for j in range(12, 17):
-        l1 = conv(l1, j)
-    l2 = trunk
-    for j in range(17, 22):
-        l2 = conv(l2, j)
-    idx = 22
-    for t in range(2, 7):
-        cat = np.concatenate([l1, l2, trunk], axis=3)
-        a, b_ = cat, cat
-        for j in range(7):
-            a = conv(a, idx + j, final=(t == 6 and j == 6))
-        for j in range(7):
-            b_ = conv(b_, idx + 7 + j, final=(t == 6 and j == 6))
-        l1, l2 = a, b_
-        idx += 14
-    want = np.concatenate([l2, l1], axis=3).transpose(0, 3, 1, 2).ravel()
+    want = O.coco_chain(net["frame"].data.reshape(NB, 3, H, W), net["layers"], net["wb"])
     got = net["be"].forward(net["h"], net["frame"]).data
     err = np.linalg.norm(got - want) / np.linalg.norm(want)
     assert err < 2e-2, err

@@ -84,6 +84,56 @@ def test_posenet_over_the_wire_equals_c_abi(server, tmp_path):
     be.close()
 
 
+def test_c1_reference_client_posenet_368(server, tmp_path):
+    """BASELINE configs[0] (C1): the unmodified reference client drives the COCO
+    pose net through our server, one 368x368 frame, batch 1. The wire reply is
+    the C-ABI result bit for bit and matches the CPU oracle chain within 2e-2
+    (bf16 rounding flips propagate through 92 layers); the NMS peaks of its
+    upsampled heatmaps are bit-exact against the oracle NMS."""
+    import torch
+    from paper_2103_04930_b200 import B200Backend, Dims, Frame, make_model, netspec, synth_posenet_weights
+    spec = tmp_path / "spec.txt"
+    spec.write_bytes(netspec.spec())
+    h = w = 368
+    rc, out = ref_client(server.endpoint, "--structure", str(spec), "--divisor", repr(netspec.COCO_DIVISOR),
+                         "--width", str(w), "--height", str(h), "--batch", "1", "--frames", "1",
+                         "--dump", str(tmp_path / "heat.bin"), "--name", "openpose_coco")
+    assert rc == 0 and out["ok"] and out["byte_account_bad"] == 0
+    wire_out = np.fromfile(tmp_path / "heat.bin", dtype=np.float32)
+    assert wire_out.size == 57 * 46 * 46 == 120612  # SURVEY §8(a) a1: K at C1
+    frame = O.batched_frame(w, h, 1, seed=7)
+    be = B200Backend(0)
+    hd = be.register_model(make_model("openpose_coco", netspec.spec(), b"", netspec.COCO_DIVISOR))
+    local = be.forward(hd, Frame(Dims(1, 3, h, w), frame)).data
+    assert wire_out.tobytes() == local.tobytes()
+    layers = netspec.coco_layers()
+    wb = [(O.bf16_round(wt), b, sl) for wt, b, sl in netspec.split_weights(layers, synth_posenet_weights(netspec.spec()))]
+    want = O.coco_chain(frame.reshape(1, 3, h, w), layers, wb)
+    err = np.linalg.norm(local - want) / np.linalg.norm(want)
+    assert err < 2e-2, err
+    # keypoint candidates: x8 upsample + 3x3 NMS on the 18 part heatmaps
+    planes = np.ascontiguousarray(local.reshape(57, 46, 46)[:18])
+    d_in = torch.from_numpy(planes).cuda()
+    d_up = torch.empty((18, h, w), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    be.upsample_device(d_in.data_ptr(), 18, 46, 46, 8, d_up.data_ptr())
+    up = d_up.cpu().numpy()
+    thr = float(np.quantile(up, 0.5))
+    maxp = 96
+    d_cnt = torch.zeros(18, dtype=torch.int32, device="cuda")
+    d_pk = torch.zeros((18, maxp, 5), dtype=torch.float32, device="cuda")
+    be.nms_device(d_up.data_ptr(), 18, h, w, thr, maxp, d_cnt.data_ptr(), d_pk.data_ptr())
+    cnt, pk = d_cnt.cpu().numpy(), d_pk.cpu().numpy()
+    for p in range(18):
+        assert up[p].tobytes() == O.upsample_plane(planes[p], 8).tobytes(), p
+        xy, ref, sc = O.nms_plane(up[p], thr, maxp)
+        n = len(sc)
+        assert cnt[p] == n
+        assert np.array_equal(pk[p, :n, 0:2].astype(np.int32), xy)
+        assert pk[p, :n, 2:4].tobytes() == ref.tobytes() and pk[p, :n, 4].tobytes() == sc.tobytes()
+    be.close()
+
+
 def test_posenet_bad_resolution_is_internal_error(server, tmp_path):
     from paper_2103_04930_b200 import netspec
     s = netspec.spec()
