@@ -106,13 +106,19 @@ int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, 
  * pooled output: its pyramid level comes from avec_posenet_layer_out_level. */
 int avec_posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                                  uint32_t w, int layer, int* level);
+/* How the plan of this shape executes `layer`: *kind 0 plain, 1 output pooled
+ * (fused 2x2 max-pool), 2 fused into the next layer (Mconv6 of a fused head:
+ * avec_posenet_layer_io rejects it with AVEC_ERR_UNSUPPORTED), 3 second layer
+ * of a fused head, whose layer_io input is the input of layer *in_layer. */
+int avec_posenet_layer_fusion(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
+                              uint32_t w, int layer, int* kind, int* in_layer);
 int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                           uint32_t w, const float* in, int layer, float* layer_in,
                           uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);
 /* Profiling hook (bench.py roofline): replays the plan of this shape op by op
  * with CUDA events on the slot stream, `reps` times, after one warm graph run.
  * Per op i < *n_ops: kind (0 = fused first layer, 1 = pixel-major tcgen05 conv,
- * 2 = max-pool, 3 = swap-AB tcgen05 conv), algorithmic FLOPs and bytes of the
+ * 2 = max-pool, 3 = swap-AB tcgen05 conv, 4 = fused Mconv6+Mconv7 head), algorithmic FLOPs and bytes of the
  * launch, mean duration (ms). */
 int avec_posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                          uint32_t w, const float* d_in, int reps, int max_ops, int* n_ops,

@@ -198,6 +198,15 @@ class B200Backend:
                                                         dims.height, dims.width, layer, ctypes.byref(lv)))
         return lv.value
 
+    def layer_fusion(self, handle: ModelHandle, dims: Dims, layer: int):
+        """(kind, in_layer): 0 plain, 1 pooled output, 2 fused into the next
+        layer (no output of its own), 3 second layer of a fused head whose
+        input is layer `in_layer`'s input (avec_posenet_layer_fusion)."""
+        kind, src = ctypes.c_int(0), ctypes.c_int(0)
+        _lib.check(self._L.avec_posenet_layer_fusion(self._ctx, handle.id, dims.batch, dims.channels, dims.height,
+                                                     dims.width, layer, ctypes.byref(kind), ctypes.byref(src)))
+        return kind.value, src.value
+
     def layer_io(self, handle: ModelHandle, frame: Frame, layer: int):
         """(input, output) activations of conv `layer`, unpadded fp32 NHWC; the
         output is the pooled tensor for layers with a fused max-pool."""
@@ -206,7 +215,9 @@ class B200Backend:
         n_img = d.batch * d.channels // 3
         hl, wl = d.height >> info["level"], d.width >> info["level"]
         ol = self.layer_out_level(handle, d, layer)
-        lin = np.empty((n_img, hl, wl, info["cin"]), np.float32)
+        _, src = self.layer_fusion(handle, d, layer)
+        cin = self.layer_info(handle, src)["cin"]
+        lin = np.empty((n_img, hl, wl, cin), np.float32)
         lout = np.empty((n_img, d.height >> ol, d.width >> ol, info["cout"]), np.float32)
         data = np.ascontiguousarray(frame.data, np.float32).ravel()
         _lib.check(self._L.avec_posenet_layer_io(self._ctx, handle.id, d.batch, d.channels, d.height,
@@ -226,7 +237,7 @@ class B200Backend:
             self._ctx, handle.id, dims.batch, dims.channels, dims.height, dims.width, d_in, reps, cap,
             ctypes.byref(n), kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), flops.ctypes.data,
             nbytes.ctypes.data, ms.ctypes.data))
-        names = {0: "conv_first", 1: "conv_pm", 2: "maxpool", 3: "conv_tc"}
+        names = {0: "conv_first", 1: "conv_pm", 2: "maxpool", 3: "conv_tc", 4: "conv_head"}
         return [dict(kind=names[int(kind[i])], flops=float(flops[i]), bytes=float(nbytes[i]),
                      ms=float(ms[i])) for i in range(n.value)]
 

@@ -235,6 +235,16 @@ int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, 
   });
 }
 
+int avec_posenet_layer_fusion(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                              int layer, int* kind, int* in_layer) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(kind, "kind");
+    need(in_layer, "in_layer");
+    avec::posenet_layer_fusion(ctx, handle, n, c, h, w, layer, kind, in_layer);
+  });
+}
+
 int avec_posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                                  uint32_t w, int layer, int* level) {
   return guarded([&] {

@@ -1,0 +1,359 @@
+// Fused stage head: Mconv6 (1x1, c6 channels, ReLU/PReLU) followed by Mconv7
+// (1x1, c7 <= 64 channels, no activation) in one tcgen05 kernel (sm_100a).
+//
+// The c6-channel intermediate never reaches HBM: per 128-pixel tile,
+//   MMA1  acc1[128 px x NB] = X[128 px x cin] * W6[block]^T      (TMEM cols 0..NB)
+//   epi1  acc1 -> bias6, act6 -> bf16 -> Y block in smem (SW128 K-major)
+//   MMA2  acc2[128 px x 64] += Y * W7[:, block]^T                 (TMEM cols 256..319)
+// for each NB-wide block of c6 (NB = min(c6, 256)), then
+//   epi2  acc2 -> bias7 -> the stage concat (bf16, 32/16/8-channel TMA boxes)
+//         and/or the fp32 NCHW network output.
+// On BODY_25 (c6 = 512 at 1312x736 x 32 frames) this removes a 495 MB write
+// and read per stage and one launch; on COCO (c6 = 128) mostly the launch.
+// Warp roles as in conv_pm.cu: warp 0 TMA producer, warp 1 TMEM owner + MMA
+// issuer, warps 2-5 both epilogues. Persistent over (branch, image, tile).
+#include <cuda_bf16.h>
+
+#include <type_traits>
+
+#include "conv_tc.cuh"
+#include "engine.hpp"
+#include "ptx.cuh"
+
+namespace avec {
+
+namespace {
+
+using namespace ptx;
+
+constexpr int kHThreads = 192;
+constexpr uint32_t kHTmemCols = 512;
+constexpr int kAcc2Col = 256;  // acc2 lives at TMEM columns 256..319
+constexpr int kXStages = 3;
+constexpr int kW6Stages = 2;
+constexpr int kW7Stages = 2;
+
+struct HeadSmem {
+  static constexpr int x = 0;                          // kXStages x [128 px][64 ch]
+  static constexpr int w6 = x + kXStages * 16384;      // kW6Stages x [256 rows][64]
+  static constexpr int y = w6 + kW6Stages * 32768;     // [128 px][256 ch] as 4 SW128 chunks
+  static constexpr int w7 = y + 4 * 16384;             // kW7Stages x [64 rows][64]
+  static constexpr int stg = w7 + kW7Stages * 8192;    // 4 warps x [32 px][<=64 ch]
+  static constexpr int bias = stg + 4 * 4096;          // b6/s6 block (2 x 256) + b7 (64)
+  static constexpr int bars = bias + (2 * 256 + 64) * 4;
+  static constexpr int total = bars + 256;
+  static_assert(total + 1024 <= 232448, "smem budget");
+};
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void head_decode(const HeadParams& p, int t, int& g, int& n, int& pt) {
+  const int per_group = p.n_images * p.tiles_per_image;
+  g = t / per_group;
+  const int rem = t - g * per_group;
+  n = rem / p.tiles_per_image;
+  pt = rem - n * p.tiles_per_image;
+}
+
+__global__ void __launch_bounds__(kHThreads, 1)
+    conv_head_kernel(const __grid_constant__ HeadMaps maps, const __grid_constant__ HeadParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_align1024(smem_raw);
+  uint8_t* sx = smem + HeadSmem::x;
+  uint8_t* sw6 = smem + HeadSmem::w6;
+  uint8_t* sy = smem + HeadSmem::y;
+  uint8_t* sw7 = smem + HeadSmem::w7;
+  uint8_t* stg = smem + HeadSmem::stg;
+  float* sb6 = reinterpret_cast<float*>(smem + HeadSmem::bias);
+  float* ss6 = sb6 + 256;
+  float* sb7 = ss6 + 256;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + HeadSmem::bars);
+  uint64_t* x_full = bars;
+  uint64_t* x_empty = x_full + kXStages;
+  uint64_t* w6_full = x_empty + kXStages;
+  uint64_t* w6_empty = w6_full + kW6Stages;
+  uint64_t* w7_full = w6_empty + kW6Stages;
+  uint64_t* w7_empty = w7_full + kW7Stages;
+  uint64_t* a1_full = w7_empty + kW7Stages;
+  uint64_t* y_full = a1_full + 1;
+  uint64_t* y_empty = y_full + 1;
+  uint64_t* a2_full = y_empty + 1;
+  uint64_t* a2_empty = a2_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
+
+  const uint32_t warp = warp_id();
+  const int NB = p.nb;
+  const int kc_per_block = NB / 64;
+  if (warp == 0 && elect_one()) {
+    for (int g = 0; g < p.n_groups; ++g) {
+      tma_prefetch(&maps.x[g]);
+      tma_prefetch(&maps.w6[g]);
+      tma_prefetch(&maps.w7[g]);
+    }
+    for (int i = 0; i < kXStages; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < kW6Stages; ++i) { mbar_init(&w6_full[i], 1); mbar_init(&w6_empty[i], 1); }
+    for (int i = 0; i < kW7Stages; ++i) { mbar_init(&w7_full[i], 1); mbar_init(&w7_empty[i], 1); }
+    mbar_init(a1_full, 1);
+    mbar_init(y_full, 128);
+    mbar_init(y_empty, 1);
+    mbar_init(a2_full, 1);
+    mbar_init(a2_empty, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kHTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      const uint64_t keep = policy_evict_last();
+      int xs = 0, w6s = 0, w7s = 0;
+      uint32_t xph = 0, w6ph = 0, w7ph = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        int g, n, pt;
+        head_decode(p, t, g, n, pt);
+        const int row0 = n * p.Hp * p.Wp + p.P * (p.Wp + 1) + pt * 128;
+        for (int j = 0; j < p.blocks; ++j) {
+          for (int c = 0; c < p.cin_chunks; ++c) {
+            mbar_wait(&x_empty[xs], xph ^ 1);
+            mbar_arrive_expect_tx(&x_full[xs], 16384);
+            tma_load_2d(sx + xs * 16384, &maps.x[g], &x_full[xs], p.in_c_off + c * 64, row0);
+            if (++xs == kXStages) { xs = 0; xph ^= 1; }
+            mbar_wait(&w6_empty[w6s], w6ph ^ 1);
+            mbar_arrive_expect_tx(&w6_full[w6s], NB * 128);
+            tma_load_2d_hint(sw6 + w6s * 32768, &maps.w6[g], &w6_full[w6s], c * 64, j * NB, keep);
+            if (++w6s == kW6Stages) { w6s = 0; w6ph ^= 1; }
+          }
+          for (int kc = 0; kc < kc_per_block; ++kc) {
+            mbar_wait(&w7_empty[w7s], w7ph ^ 1);
+            mbar_arrive_expect_tx(&w7_full[w7s], 8192);
+            tma_load_2d_hint(sw7 + w7s * 8192, &maps.w7[g], &w7_full[w7s], j * NB + kc * 64, 0, keep);
+            if (++w7s == kW7Stages) { w7s = 0; w7ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc1 = idesc_bf16_f32(128, uint32_t(NB));
+      const uint32_t idesc2 = idesc_bf16_f32(128, 64);
+      int xs = 0, w6s = 0, w7s = 0;
+      uint32_t xph = 0, w6ph = 0, w7ph = 0, yfph = 0, a2eph = 0;
+      const uint32_t x_base = smem_u32(sx), w6_base = smem_u32(sw6), y_base = smem_u32(sy),
+                     w7_base = smem_u32(sw7);
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        for (int j = 0; j < p.blocks; ++j) {
+          // acc1 is free: the epilogue signalled y_full for block j-1 (waited
+          // below before MMA2 of j-1) after its last read of acc1
+          for (int c = 0; c < p.cin_chunks; ++c) {
+            mbar_wait(&x_full[xs], xph);
+            mbar_wait(&w6_full[w6s], w6ph);
+            tc_fence_after();
+            const uint32_t xa = x_base + xs * 16384, wb = w6_base + w6s * 32768;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss(tmem, desc_sw128(xa + kk * 32), desc_sw128(wb + kk * 32), idesc1,
+                          (c == 0 && kk == 0) ? 0u : 1u);
+            mma_commit(&x_empty[xs]);
+            mma_commit(&w6_empty[w6s]);
+            if (++xs == kXStages) { xs = 0; xph ^= 1; }
+            if (++w6s == kW6Stages) { w6s = 0; w6ph ^= 1; }
+          }
+          mma_commit(a1_full);
+          mbar_wait(y_full, yfph);  // Y block j written (and acc1 drained)
+          yfph ^= 1;
+          if (j == 0) {  // acc2 drained by the previous tile's epilogue
+            mbar_wait(a2_empty, a2eph ^ 1);
+            a2eph ^= 1;
+          }
+          tc_fence_after();
+          for (int kc = 0; kc < kc_per_block; ++kc) {
+            mbar_wait(&w7_full[w7s], w7ph);
+            tc_fence_after();
+            const uint32_t ya = y_base + kc * 16384, wb = w7_base + w7s * 8192;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss(tmem + kAcc2Col, desc_sw128(ya + kk * 32), desc_sw128(wb + kk * 32), idesc2,
+                          (j == 0 && kc == 0 && kk == 0) ? 0u : 1u);
+            mma_commit(&w7_empty[w7s]);
+            if (++w7s == kW7Stages) { w7s = 0; w7ph ^= 1; }
+          }
+          mma_commit(y_empty);
+        }
+        mma_commit(a2_full);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogues
+    const uint32_t quad = warp & 3;
+    const uint32_t lane = lane_id();
+    const int ep = int(threadIdx.x) - 64;  // 0..127, loader index for the bias slices
+    // warp q may only touch TMEM lanes 32q..32q+31: this thread's pixel (and
+    // its TMEM lane, and its row of Y) is 32q + lane
+    const int px = int(quad) * 32 + int(lane);
+    const uint32_t lane_base = (quad * 32) << 16;
+    uint8_t* stg_w = stg + quad * 4096;
+    uint8_t* yrow = sy + px * 128;  // this pixel's row in every 16 KB Y chunk
+    uint32_t a1ph = 0, yeph = 0, a2fph = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      int gi, n, pt;
+      head_decode(p, t, gi, n, pt);
+      const HeadGroup& g = p.g[gi];
+      const int o = pt * 128 + px;  // padded-width output position of this pixel
+      const int hh = o / p.Wp;
+      const int ww = o - hh * p.Wp;
+      const bool valid = hh < p.H && ww < p.W;
+      for (int j = 0; j < p.blocks; ++j) {
+        // this block's bias / slope: every epilogue warp is done with the
+        // previous block's (and the previous tile's b7) before they change
+        named_bar_sync(1, 128);
+        for (int i = ep; i < NB; i += 128) {
+          const int co = j * NB + i;
+          sb6[i] = g.bias6[co];
+          ss6[i] = g.act6 == 1 ? 0.f : g.act6 == 2 ? g.slope6[co] : 1.f;
+        }
+        if (j == 0 && ep < 64) sb7[ep] = ep < g.c7 ? g.bias7[ep] : 0.f;
+        named_bar_sync(1, 128);
+        mbar_wait(y_empty, yeph ^ 1);  // MMA2 of the previous block released Y
+        yeph ^= 1;
+        mbar_wait(a1_full, a1ph);
+        a1ph ^= 1;
+        tc_fence_after();
+        for (int c0 = 0; c0 < NB; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem + lane_base + c0, v);
+          tmem_ld_wait();
+          uint8_t* chunk = yrow + (c0 >> 6) * 16384;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int c = c0 + q * 8 + 2 * jj;
+              float a = __uint_as_float(v[q * 8 + 2 * jj]) + sb6[c];
+              float b = __uint_as_float(v[q * 8 + 2 * jj + 1]) + sb6[c + 1];
+              a = fmaxf(a, 0.f) + ss6[c] * fminf(a, 0.f);
+              b = fmaxf(b, 0.f) + ss6[c + 1] * fminf(b, 0.f);
+              w[jj] = pack2(a, b);
+            }
+            const uint32_t qq = ((c0 & 63) >> 3) + q;  // 16-byte chunk within the 128-byte row
+            *reinterpret_cast<uint4*>(chunk + ((qq ^ (uint32_t(px) & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(y_full);
+      }
+      // ---- epilogue 2: acc2 (+ b7) -> outputs
+      mbar_wait(a2_full, a2fph);
+      a2fph ^= 1;
+      tc_fence_after();
+      uint32_t v0[32], v1[32];
+      tmem_ld32(tmem + lane_base + kAcc2Col, v0);
+      tmem_ld32(tmem + lane_base + kAcc2Col + 32, v1);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(a2_empty);
+      float zf[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) zf[c] = __uint_as_float(c < 32 ? v0[c] : v1[c - 32]) + sb7[c];
+      if (g.out2 != nullptr && valid) {  // fp32 NCHW copy for the wire
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (c < g.c7)
+            g.out2[((static_cast<size_t>(n) * g.out2_c_stride + g.out2_c_off + c) * p.H + hh) * p.W + ww] = zf[c];
+      }
+      if (g.out_mode == kOutNchwF32) {
+        if (valid) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (c < g.c7)
+              static_cast<float*>(g.out)[((static_cast<size_t>(n) * g.out_c_stride + g.out_c_off + c) * p.H + hh) *
+                                             p.W + ww] = zf[c];
+        }
+        continue;
+      }
+      // bf16 into the stage concat: round_up(c7, 8) channels as 32/16/8-channel
+      // boxes of this warp's 32 pixels (channels past c7 carry zero weights and
+      // bias, so they store zeros)
+      uint32_t packed[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) packed[i] = valid ? pack2(zf[2 * i], zf[2 * i + 1]) : 0u;
+      const int row_w = p.P * p.Wp + p.P + pt * 128 + int(quad) * 32;
+      const int c_end = (g.c7 + 7) & ~7;
+      auto box = [&](auto width, auto first) {
+        constexpr int W = decltype(width)::value;
+        constexpr int c0 = decltype(first)::value;
+        if (lane == 0) bulk_wait_read<0>();  // this warp's previous store has read the staging box
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < W / 8; ++q) {
+          const int w0 = (c0 >> 1) + q * 4;  // packed word of channel c0 + 8q
+          uint32_t w[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) w[jj] = packed[w0 + jj];
+          uint32_t off;
+          if constexpr (W == 32) off = lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4);
+          else if constexpr (W == 16) off = lane * 32 + ((q ^ ((lane >> 2) & 1)) << 4);
+          else off = lane * 16;
+          *reinterpret_cast<uint4*>(stg_w + off) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const CUtensorMap* m = W == 32 ? &maps.out32[gi] : W == 16 ? &maps.out16[gi] : &maps.out8[gi];
+          tma_store_3d(m, stg_w, g.out_c_off + c0, row_w, n);
+          bulk_commit();
+        }
+      };
+      // c_end in {8, 16, ..., 64}: 32-channel boxes, then 16 and 8 tails
+      using I0 = std::integral_constant<int, 0>;
+      using I16 = std::integral_constant<int, 16>;
+      using I32 = std::integral_constant<int, 32>;
+      using I48 = std::integral_constant<int, 48>;
+      using B8 = std::integral_constant<int, 8>;
+      using B16 = std::integral_constant<int, 16>;
+      using B32 = std::integral_constant<int, 32>;
+      switch (c_end) {
+        case 8: box(B8{}, I0{}); break;
+        case 16: box(B16{}, I0{}); break;
+        case 24: box(B16{}, I0{}); box(B8{}, I16{}); break;
+        case 32: box(B32{}, I0{}); break;
+        case 40: box(B32{}, I0{}); box(B8{}, I32{}); break;
+        case 48: box(B32{}, I0{}); box(B16{}, I32{}); break;
+        case 56: box(B32{}, I0{}); box(B16{}, I32{}); box(B8{}, I48{}); break;
+        default: box(B32{}, I0{}); box(B32{}, I32{}); break;
+      }
+    }
+    if (lane_id() == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kHTmemCols>(tmem);
+  }
+}
+
+}  // namespace
+
+void conv_head_configure() {
+  check_cuda(cudaFuncSetAttribute(conv_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  HeadSmem::total + 1024),
+             "conv_head smem attribute");
+}
+
+void launch_conv_head(const HeadMaps& maps, const HeadParams& p, int sm_count, cudaStream_t stream) {
+  const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
+  conv_head_kernel<<<grid, kHThreads, HeadSmem::total + 1024, stream>>>(maps, p);
+  check_cuda(cudaGetLastError(), "conv_head launch");
+}
+
+}  // namespace avec

@@ -111,6 +111,36 @@ struct ConvMaps {
   CUtensorMap out_pool[kConvMaxGroups];   // 4D [N][Hp'][Wp'][C] of the pooled level, box {64, 16, 1, 1}
 };
 
+// Fused stage head (conv_head.cu): Mconv6 (1x1 -> c6, act6) then Mconv7
+// (1x1 -> c7 <= 64, no activation) per 128-pixel tile, c6 in NB-wide blocks.
+struct HeadGroup {
+  const float* bias6;
+  const float* slope6;
+  int act6;
+  const float* bias7;
+  int c7;
+  void* out;            // bf16 padded-flat slab (kOutTmaBf16) or fp32 NCHW (kOutNchwF32)
+  int out_mode;
+  int out_c_off, out_c_stride;
+  float* out2;          // optional second destination: fp32 NCHW (BODY_25's last PAF stage)
+  int out2_c_off, out2_c_stride;
+};
+
+struct HeadParams {
+  int n_images, H, W, Hp, Wp, P;
+  int in_c_off, cin_chunks;
+  int nb, blocks;       // c6 = nb * blocks, nb in {64, 128, 256}
+  int tiles_per_image, total_tiles, n_groups;
+  HeadGroup g[kConvMaxGroups];
+};
+
+struct HeadMaps {
+  CUtensorMap x[kConvMaxGroups];    // input, box {64 ch, 128 rows}
+  CUtensorMap w6[kConvMaxGroups];   // [c6_pad][cin_pad], box {64, nb rows}
+  CUtensorMap w7[kConvMaxGroups];   // [c7_pad][c6], box {64, 64 rows}
+  CUtensorMap out32[kConvMaxGroups], out16[kConvMaxGroups], out8[kConvMaxGroups];
+};
+
 // host side
 // per device, before the first launch (sets the dynamic smem limits)
 void conv_configure();
@@ -123,6 +153,8 @@ void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cud
 // first layer fused with the input conversion (conv_first.cu): fp32 NCHW frames
 // -> 3x3x3 taps built in smem -> tcgen05 -> 64-channel padded-flat NHWC output
 void conv_first_configure();
+void conv_head_configure();
+void launch_conv_head(const HeadMaps& maps, const HeadParams& p, int sm_count, cudaStream_t stream);
 void launch_conv_first(const ConvMaps& maps, const ConvParams& p, const float* frames, int sm_count,
                        cudaStream_t stream);
 

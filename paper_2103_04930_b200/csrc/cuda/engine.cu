@@ -428,11 +428,105 @@ struct PlanBuilder {
     const int cout = net.layers[layer].def.cout;
     if (pool_fusable(layer, level)) {
       conv({layer}, {in}, {view(pooled, 0, cout)}, true);
+      plan.layer_fusion[layer] = 1;
     } else {
       const int full = buffer(level, cout);
       conv({layer}, {in}, {view(full, 0, cout)});
       pool(full, pooled);
     }
+  }
+
+  // Mconv6 -> Mconv7 of each branch as one fused launch (conv_head.cu) when the
+  // shapes allow; otherwise two conv launches through the `mid` buffers.
+  // outs2: optional fp32 NCHW second destinations (BODY_25's last PAF stage).
+  // AVEC_HEADFUSE=0 disables.
+  void head(std::vector<int> l6, std::vector<int> l7, std::vector<TensorView> in, std::vector<TensorView> mid,
+            std::vector<TensorView> out, std::vector<TensorView> out2 = {}) {
+    static const bool on = [] {
+      const char* e = std::getenv("AVEC_HEADFUSE");
+      return !(e && e[0] == '0');
+    }();
+    bool ok = on;
+    for (size_t g = 0; g < l6.size(); ++g) {
+      const ConvLayerDev& A = net.layers[l6[g]];
+      const ConvLayerDev& B = net.layers[l7[g]];
+      const int c6 = A.def.cout;
+      ok = ok && A.exec_k == 1 && B.exec_k == 1 && (c6 == 128 || c6 == 256 || c6 == 512) && B.def.cout <= 64 &&
+           B.def.cin == c6 && B.def.cin_map.empty() && B.cin_pad == c6 && B.def.act == kActNone &&
+           in[g].level == 3;
+      const TensorView& o = out[g];
+      ok = ok && (o.buf == -1 || (o.c_off % 8 == 0 && o.c_off + round_up(B.def.cout, 8) <= o.c_stride &&
+                                  o.level == in[g].level));
+      if (!out2.empty()) ok = ok && out2[g].buf == -1 && o.buf != -1;
+    }
+    if (!ok) {
+      std::vector<int> a(l6), b(l7);
+      if (a.size() == 1) {
+        conv({a[0]}, {in[0]}, {mid[0]});
+        conv({b[0]}, {mid[0]}, {out[0]});
+        if (!out2.empty()) conv({b[0]}, {mid[0]}, {out2[0]});
+      } else {
+        conv({a[0], a[1]}, {in[0], in[1]}, {mid[0], mid[1]});
+        conv({b[0], b[1]}, {mid[0], mid[1]}, {out[0], out[1]});
+      }
+      return;
+    }
+    PlanOp op;
+    op.kind = PlanOp::kHead;
+    HeadParams& p = op.hp;
+    const Geometry& gi = plan.geo[in[0].level];
+    const ConvLayerDev& A0 = net.layers[l6[0]];
+    p.n_images = plan.n;
+    p.H = gi.H;
+    p.W = gi.W;
+    p.Hp = gi.Hp();
+    p.Wp = gi.Wp();
+    p.P = gi.P;
+    p.in_c_off = in[0].c_off;
+    p.cin_chunks = A0.cin_pad / 64;
+    p.nb = A0.def.cout < 256 ? A0.def.cout : 256;
+    p.blocks = A0.def.cout / p.nb;
+    p.tiles_per_image = (p.H * p.Wp + 127) / 128;
+    p.n_groups = int(l6.size());
+    p.total_tiles = p.n_groups * p.n_images * p.tiles_per_image;
+    const uint64_t rows = uint64_t(plan.n) * gi.Hp() * gi.Wp();
+    for (size_t g = 0; g < l6.size(); ++g) {
+      const ConvLayerDev& A = net.layers[l6[g]];
+      const ConvLayerDev& B = net.layers[l7[g]];
+      if (A.cin_pad != A0.cin_pad || A.def.cout != A0.def.cout || in[g].c_off != p.in_c_off)
+        fail(AVEC_ERR_INVALID_MODEL, "grouped head layers differ in shape");
+      HeadGroup& hg = p.g[g];
+      hg.bias6 = A.bias;
+      hg.slope6 = A.slope;
+      hg.act6 = A.def.act;
+      hg.bias7 = B.bias;
+      hg.c7 = B.def.cout;
+      const TensorView& o = out[g];
+      hg.out = o.buf == -1 ? static_cast<void*>(plan.out.p) : plan.bufs[o.buf]->p;
+      hg.out_mode = o.buf == -1 ? kOutNchwF32 : kOutTmaBf16;
+      hg.out_c_off = o.c_off;
+      hg.out_c_stride = o.c_stride;
+      hg.out2 = out2.empty() ? nullptr : plan.out.as<float>();
+      hg.out2_c_off = out2.empty() ? 0 : out2[g].c_off;
+      hg.out2_c_stride = out2.empty() ? 0 : out2[g].c_stride;
+      const int ib = in[g].buf;
+      op.hm.x[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 128);
+      op.hm.w6[g] = make_map_2d(A.w, A.cin_pad, A.cout_pad, uint32_t(p.nb));
+      op.hm.w7[g] = make_map_2d(B.w, B.cin_pad, B.cout_pad, 64);
+      if (o.buf != -1) {
+        op.hm.out32[g] = make_map_3d_store(plan.bufs[o.buf]->p, plan.buf_c[o.buf], uint64_t(gi.Hp()) * gi.Wp(), plan.n, 32);
+        op.hm.out16[g] = make_map_3d_store(plan.bufs[o.buf]->p, plan.buf_c[o.buf], uint64_t(gi.Hp()) * gi.Wp(), plan.n, 16);
+        op.hm.out8[g] = make_map_3d_store(plan.bufs[o.buf]->p, plan.buf_c[o.buf], uint64_t(gi.Hp()) * gi.Wp(), plan.n, 8);
+      }
+      op.layers[g] = l7[g];
+      op.head_l6[g] = l6[g];
+      // the parity hook shows the fp32 copy when there is one (as the unfused plan did)
+      record_io(l7[g], in[g], out2.empty() ? out[g] : out2[g]);
+      plan.layer_fusion[l6[g]] = 2;
+      plan.layer_fusion[l7[g]] = 3;
+      plan.layer_in_from[l7[g]] = l6[g];
+    }
+    plan.ops.push_back(op);
   }
 
   // one launch covering 1 or 2 conv layers (sibling branches) of equal shape;
@@ -639,6 +733,9 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
   const int nl = int(f.convs.size());
   plan.layer_in.assign(nl, TensorView{});
   plan.layer_out.assign(nl, TensorView{});
+  plan.layer_fusion.assign(nl, 0);
+  plan.layer_in_from.resize(nl);
+  for (int i = 0; i < nl; ++i) plan.layer_in_from[i] = i;
   const int cat = b.buffer(3, kCocoCatChannels);  // [trunk | L1 at kCocoPaf | L2 at kCocoHeat]
   int li = build_trunk(b, plan, cat, 0);
   const int T = f.trunk_channels, C1 = f.paf_channels, C2 = f.heat_channels;  // T == kCocoPaf
@@ -649,9 +746,8 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
   b.conv({s1 + 0, s1 + 5}, {b.view(cat, 0, T), b.view(cat, 0, T)}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
   b.conv({s1 + 1, s1 + 6}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)}, {b.view(l1b, 0, 128), b.view(l2b, 0, 128)});
   b.conv({s1 + 2, s1 + 7}, {b.view(l1b, 0, 128), b.view(l2b, 0, 128)}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
-  b.conv({s1 + 3, s1 + 8}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)}, {b.view(l1x, 0, 512), b.view(l2x, 0, 512)});
-  b.conv({s1 + 4, s1 + 9}, {b.view(l1x, 0, 512), b.view(l2x, 0, 512)},
-         {b.view(cat, kCocoPaf, C1), b.view(cat, kCocoHeat, C2)});
+  b.head({s1 + 3, s1 + 8}, {s1 + 4, s1 + 9}, {b.view(l1a, 0, 128), b.view(l2a, 0, 128)},
+         {b.view(l1x, 0, 512), b.view(l2x, 0, 512)}, {b.view(cat, kCocoPaf, C1), b.view(cat, kCocoHeat, C2)});
   li += 10;
   for (int t = 2; t <= f.stages; ++t) {
     const int s = li;  // L1: s..s+6, L2: s+7..s+13
@@ -659,19 +755,17 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
     b.conv({s + 0, s + 7}, {b.view(cat, 0, catc), b.view(cat, 0, catc)},
            {b.view(l1a, 0, 128), b.view(l2a, 0, 128)});
     int x = l1a, y = l1b, u = l2a, v = l2b;
-    for (int i = 1; i <= 5; ++i) {  // Mconv2..5 (7x7) then Mconv6 (1x1)
+    for (int i = 1; i <= 4; ++i) {  // Mconv2..5 (7x7)
       b.conv({s + i, s + 7 + i}, {b.view(x, 0, 128), b.view(u, 0, 128)}, {b.view(y, 0, 128), b.view(v, 0, 128)});
       std::swap(x, y);
       std::swap(u, v);
     }
-    if (t == f.stages) {
-      // wire output: [n][heat 19 | paf 38][H/8][W/8] fp32
-      b.conv({s + 6, s + 13}, {b.view(x, 0, 128), b.view(u, 0, 128)},
-             {b.view(-1, C2, C1), b.view(-1, 0, C2)});
-    } else {
-      b.conv({s + 6, s + 13}, {b.view(x, 0, 128), b.view(u, 0, 128)},
-             {b.view(cat, kCocoPaf, C1), b.view(cat, kCocoHeat, C2)});
-    }
+    // Mconv6 (1x1, ReLU) + Mconv7 (1x1) per branch, fused
+    const std::vector<TensorView> outs =
+        t == f.stages ? std::vector<TensorView>{b.view(-1, C2, C1), b.view(-1, 0, C2)}  // wire: [heat | paf] fp32
+                      : std::vector<TensorView>{b.view(cat, kCocoPaf, C1), b.view(cat, kCocoHeat, C2)};
+    b.head({s + 5, s + 12}, {s + 6, s + 13}, {b.view(x, 0, 128), b.view(u, 0, 128)},
+           {b.view(y, 0, 128), b.view(v, 0, 128)}, outs);
     li += 14;
   }
   if (li != nl) fail(AVEC_ERR_INVALID_MODEL, "plan/layer table mismatch");
@@ -686,6 +780,9 @@ void build_body25_plan(Plan& plan, const PoseNet& net, int device) {
   const int nl = int(f.convs.size());
   plan.layer_in.assign(nl, TensorView{});
   plan.layer_out.assign(nl, TensorView{});
+  plan.layer_fusion.assign(nl, 0);
+  plan.layer_in_from.resize(nl);
+  for (int i = 0; i < nl; ++i) plan.layer_in_from[i] = i;
   const int cat = b.buffer(3, kB25CatChannels);
   int li = build_trunk(b, plan, cat, kB25Trunk);
   const int X0 = b.buffer(3, 384), Y0 = b.buffer(3, 384), m6 = b.buffer(3, 512);
@@ -698,9 +795,10 @@ void build_body25_plan(Plan& plan, const PoseNet& net, int device) {
       b.conv({li++}, {b.view(Y, w, w)}, {b.view(Y, 2 * w, w)});
       std::swap(X, Y);
     }
-    b.conv({li++}, {b.view(X, 0, 3 * w)}, {b.view(m6, 0, c6)});  // Mconv6
-    const int head = li++;
-    for (const TensorView& o : heads) b.conv({head}, {b.view(m6, 0, c6)}, {o});  // Mconv7
+    const int l6 = li++, l7 = li++;  // Mconv6 (1x1, PReLU) + Mconv7 (1x1), fused
+    std::vector<TensorView> out2;
+    if (heads.size() > 1) out2.push_back(heads[1]);
+    b.head({l6}, {l7}, {b.view(X, 0, 3 * w)}, {b.view(m6, 0, c6)}, {heads[0]}, out2);
   };
   // PAF stage 0 reads the trunk; stages 1..3 read [PAF | trunk] = window [32, 224)
   stage(b.view(cat, kB25Trunk, 128), 96, 256, {b.view(cat, kB25Paf, P)});
@@ -721,6 +819,9 @@ void run_ops(avec_ctx* ctx, const Plan& plan, const PoseNet& net, size_t first, 
     switch (op.kind) {
       case PlanOp::kFirst:
         launch_conv_first(op.maps, op.cp, plan.in.as<float>(), ctx->sms, st);
+        break;
+      case PlanOp::kHead:
+        launch_conv_head(op.hm, op.hp, ctx->sms, st);
         break;
       case PlanOp::kConv:
         if (op.cp.pixel_major)
@@ -809,6 +910,7 @@ void ctx_init(avec_ctx* ctx, int device, int slots) {
   conv_configure();
   conv_pm_configure();
   conv_first_configure();
+  conv_head_configure();
   if (slots <= 0) slots = 2;
   for (int i = 0; i < slots; ++i) {
     auto s = std::make_unique<Slot>();
@@ -1020,6 +1122,19 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
       p.bytes = double(n_img) * g.H * g.W * op.C * 2 * 1.25;  // read 4, write 1 bf16 per window
       continue;
     }
+    if (op.kind == PlanOp::kHead) {  // Mconv6 + Mconv7: both layers' FLOPs, input + head output bytes
+      p.kind = 4;
+      for (int g = 0; g < 2; ++g) {
+        if (op.layers[g] < 0) continue;
+        const ConvDef& d6 = f.convs[op.head_l6[g]];
+        const ConvDef& d7 = f.convs[op.layers[g]];
+        const double px = double(n_img) * (h >> d6.level) * (w >> d6.level);
+        p.flops += 2.0 * px * (double(d6.cin) * d6.cout + double(d7.cin) * d7.cout);
+        const bool final_out = plan->layer_out[op.layers[g]].buf == -1;
+        p.bytes += px * (d6.cin * 2.0 + d7.cout * (final_out ? 4.0 : 2.0));
+      }
+      continue;
+    }
     p.kind = op.kind == PlanOp::kFirst ? 0 : op.cp.pixel_major ? 1 : 3;
     for (int g = 0; g < 2; ++g) {
       if (op.layers[g] < 0) continue;
@@ -1034,6 +1149,20 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
     }
   }
   return prof;
+}
+
+void posenet_layer_fusion(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                          int layer, int* kind, int* in_layer) {
+  const Model m = model_lookup(ctx, handle);
+  if (m.kind != AVEC_MODEL_POSENET) fail(AVEC_ERR_INVALID_ARGUMENT, "not a pose net");
+  int n_img = 0;
+  posenet_shape(m, n, c, h, w, n_img);
+  if (layer < 0 || layer >= int(m.net->fam.convs.size())) fail(AVEC_ERR_INVALID_ARGUMENT, "layer index");
+  check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+  SlotLease lease(ctx);
+  Plan* plan = get_plan(ctx, lease.slot(), m, n_img, int(h), int(w));
+  *kind = plan->layer_fusion[layer];
+  *in_layer = plan->layer_in_from[layer];
 }
 
 int posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
@@ -1065,9 +1194,13 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
   SlotLease lease(ctx);
   Slot* s = lease.slot();
   Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
+  if (plan->layer_fusion[layer] == 2)
+    fail(AVEC_ERR_UNSUPPORTED, d.name + " is fused into the next layer: its output never leaves the SM");
+  // a fused head's second layer sees the head's input (the first layer's input)
+  const ConvDef& din = f.convs[plan->layer_in_from[layer]];
   // the output view is one level down when the layer's 2x2 pool is fused
   const int out_level = plan->layer_out[layer].buf >= 0 ? plan->layer_out[layer].level : d.level;
-  const uint64_t need_in = uint64_t(n_img) * (int(h) >> d.level) * (int(w) >> d.level) * d.cin;
+  const uint64_t need_in = uint64_t(n_img) * (int(h) >> d.level) * (int(w) >> d.level) * din.cin;
   const uint64_t need_out = uint64_t(n_img) * (int(h) >> out_level) * (int(w) >> out_level) * d.cout;
   if (layer_in_elems != need_in || layer_out_elems != need_out)
     fail(AVEC_ERR_INVALID_ARGUMENT, "layer buffers have the wrong size");
@@ -1119,7 +1252,7 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
         dst[p * cdim + ch] = hostv[p * grab + src_ch];
       }
   };
-  fetch(plan->layer_in[layer], d.cin, layer_in, layer == 0 ? std::vector<int>{} : d.cin_map);
+  fetch(plan->layer_in[layer], din.cin, layer_in, layer == 0 ? std::vector<int>{} : din.cin_map);
   fetch(plan->layer_out[layer], d.cout, layer_out, {});
 }
 

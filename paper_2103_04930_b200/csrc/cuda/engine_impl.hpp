@@ -73,9 +73,12 @@ struct TensorView {
 };
 
 struct PlanOp {
-  enum Kind { kFirst, kConv, kPool } kind = kConv;
+  enum Kind { kFirst, kConv, kPool, kHead } kind = kConv;
   ConvParams cp{};
   ConvMaps maps{};
+  HeadParams hp{};  // kHead: fused Mconv6 + Mconv7 (layers[] = the Mconv7 layers)
+  HeadMaps hm{};
+  int head_l6[2] = {-1, -1};
   int layers[2] = {-1, -1};
   int src = -1, dst = -1, level = 0, C = 0;  // pool: src/dst buffers
 };
@@ -87,6 +90,10 @@ struct Plan {
   std::vector<int> buf_level, buf_c;
   std::vector<PlanOp> ops;
   std::vector<TensorView> layer_in, layer_out;
+  // parity-hook view of each layer: 0 plain, 1 output 2x2-pooled (level + 1),
+  // 2 fused into the next layer (no output of its own), 3 second layer of a
+  // fused head (its input view is the head's input, described by layer_in_from)
+  std::vector<int> layer_fusion, layer_in_from;
   DevMem in, out;  // fp32 NCHW frames in, fp32 NCHW net output
   uint64_t in_elems = 0, out_elems = 0;
   cudaGraphExec_t graph = nullptr;
@@ -157,6 +164,11 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
                                        uint32_t h, uint32_t w, const float* d_in, int reps);
 // pyramid level of a layer's output view: its own level, or one more when
 // the plan fuses the following 2x2 max-pool into it
+// parity-hook view of a layer in the plan of this shape: kind 0 plain,
+// 1 pooled output, 2 fused into the next layer, 3 second layer of a fused
+// head whose input is `in_layer`'s input
+void posenet_layer_fusion(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                          int layer, int* kind, int* in_layer);
 int posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                             int layer);
 void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,

@@ -47,15 +47,22 @@ def test_all_layers_parity(b25):
     be, h, layers = b25["be"], b25["h"], b25["layers"]
     finals = {i for i, L in enumerate(layers) if L.name in ("Mconv7_stage3_L2", "Mconv7_stage1_L1")}
     for i, L in enumerate(layers):
+        kind, src = be.layer_fusion(h, b25["frame"].dims, i)
+        if kind == 2:  # Mconv6 of a fused head: checked through its Mconv7
+            continue
         lin, lout = be.layer_io(h, b25["frame"], i)
         w, b, sl = b25["wb"][i]
         final = i in finals
-        ref = O.conv2d_nhwc(lin, w, b, relu=L.act, round_bf16=not final, slope=sl)
-        if lout.shape[1] * 2 == lin.shape[1]:  # the plan fuses this layer's 2x2 max-pool
+        x = lin
+        if kind == 3:  # fused head: chain Mconv6 (bf16 intermediate) from the head input
+            w6, b6, s6 = b25["wb"][src]
+            x = O.conv2d_nhwc(lin, w6, b6, relu=layers[src].act, round_bf16=True, slope=s6)
+        ref = O.conv2d_nhwc(x, w, b, relu=L.act, round_bf16=not final, slope=sl)
+        if kind == 1:  # the plan fuses this layer's 2x2 max-pool
             ref = O.maxpool2_nhwc(ref)
         err = np.linalg.norm(lout - ref) / max(np.linalg.norm(ref), 1e-30)
         assert err <= 1e-3, (L.name, err)
-        if not final:
+        if not final and kind != 3:
             tol = ulp_bf16(ref) + 1e-4 * float(np.abs(ref).max())
             assert not (np.abs(lout - ref) > tol).any(), L.name
 

@@ -41,18 +41,35 @@ def ulp_bf16(x):
     return np.exp2(e - 7)
 
 
+def layer_reference(net, i, lin, final):
+    """Oracle output of layer i as the plan executes it: a fused head's second
+    layer (kind 3) chains the first layer (bf16 intermediate) from the head's
+    input; a pooled layer (kind 1) pools its output."""
+    layers, wb = net["layers"], net["wb"]
+    kind, src = net["be"].layer_fusion(net["h"], net["frame"].dims, i)
+    x = lin
+    if kind == 3:
+        w6, b6, s6 = wb[src]
+        x = O.conv2d_nhwc(lin, w6, b6, relu=layers[src].act, round_bf16=True, slope=s6)
+    w, b, sl = wb[i]
+    ref = O.conv2d_nhwc(x, w, b, relu=layers[i].act, round_bf16=not final, slope=sl)
+    if kind == 1:
+        ref = O.maxpool2_nhwc(ref)
+    return kind, ref
+
+
 def check_layer(net, i):
     be, h = net["be"], net["h"]
     L = net["layers"][i]
+    kind, _ = be.layer_fusion(h, net["frame"].dims, i)
+    if kind == 2:  # Mconv6 of a fused head: checked through its Mconv7
+        return None
     lin, lout = be.layer_io(h, net["frame"], i)
-    w, b, sl = net["wb"][i]
     final = i in net.get("final_layers", ()) or (L.name.startswith("Mconv7") and "stage6" in L.name)
-    ref = O.conv2d_nhwc(lin, w, b, relu=L.act, round_bf16=not final, slope=sl)
-    if lout.shape[1] * 2 == lin.shape[1]:  # the plan fuses this layer's 2x2 max-pool
-        ref = O.maxpool2_nhwc(ref)
+    kind, ref = layer_reference(net, i, lin, final)
     err = np.linalg.norm(lout - ref) / max(np.linalg.norm(ref), 1e-30)
     assert err <= 1e-3, (L.name, err)
-    if not final:
+    if not final and kind != 3:  # element bound: one rounding; a chained head has two
         tol = ulp_bf16(ref) + 1e-4 * float(np.abs(ref).max())
         bad = np.abs(lout - ref) > tol
         assert not bad.any(), (L.name, int(bad.sum()), float(np.abs(lout - ref).max()))
@@ -82,6 +99,20 @@ def test_maxpool_exact(net):
             assert np.array_equal(out_prev, in_next)
         else:
             assert np.array_equal(O.maxpool2_nhwc(out_prev), in_next)
+
+
+def test_fused_heads_present(net):
+    """conv5_4/5_5 and every stage's Mconv6/Mconv7 run as fused heads."""
+    be, h = net["be"], net["h"]
+    names = [L.name for L in net["layers"]]
+    for i, n in enumerate(names):
+        kind, src = be.layer_fusion(h, net["frame"].dims, i)
+        if n.startswith("Mconv6") or n.startswith("conv5_4"):
+            assert kind == 2, n
+        if n.startswith("Mconv7") or n.startswith("conv5_5"):
+            assert kind == 3 and src == i - 1, n
+    with pytest.raises(Exception):
+        be.layer_io(h, net["frame"], names.index("Mconv6_stage2_L1"))
 
 
 def test_fused_pool_equals_pool_of_conv(net):
