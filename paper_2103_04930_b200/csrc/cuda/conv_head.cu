@@ -2,10 +2,11 @@
 // (1x1, c7 <= 64 channels, no activation) in one tcgen05 kernel (sm_100a).
 //
 // The c6-channel intermediate never reaches HBM: per 128-pixel tile,
-//   MMA1  acc1[128 px x NB] = X[128 px x cin] * W6[block]^T      (TMEM cols 0..NB)
-//   epi1  acc1 -> bias6, act6 -> bf16 -> Y block in smem (SW128 K-major)
-//   MMA2  acc2[128 px x 64] += Y * W7[:, block]^T                 (TMEM cols 256..319)
-// for each NB-wide block of c6 (NB = min(c6, 256)), then
+//   MMA1  acc1[b] = X[128 px x cin] * W6[block]^T   (128 cols, b = block & 1)
+//   epi1  acc1[b] -> bias6, act6 -> bf16 -> Y[b] in smem (SW128 K-major)
+//   MMA2  acc2[128 px x 64] += Y[b] * W7[:, block]^T  (TMEM cols 256..319)
+// for each 128-wide block of c6, double-buffered so MMA1 of block j+1 runs
+// while the epilogue converts block j, then
 //   epi2  acc2 -> bias7 -> the stage concat (bf16, 32/16/8-channel TMA boxes)
 //         and/or the fp32 NCHW network output.
 // On BODY_25 (c6 = 512 at 1312x736 x 32 frames) this removes a 495 MB write
@@ -29,18 +30,19 @@ using namespace ptx;
 constexpr int kHThreads = 192;
 constexpr uint32_t kHTmemCols = 512;
 constexpr int kAcc2Col = 256;  // acc2 lives at TMEM columns 256..319
+constexpr int kNB = 128;        // c6 block width (MMA1 N)
 constexpr int kXStages = 3;
-constexpr int kW6Stages = 2;
+constexpr int kW6Stages = 3;
 constexpr int kW7Stages = 2;
 
 struct HeadSmem {
   static constexpr int x = 0;                          // kXStages x [128 px][64 ch]
-  static constexpr int w6 = x + kXStages * 16384;      // kW6Stages x [256 rows][64]
-  static constexpr int y = w6 + kW6Stages * 32768;     // [128 px][256 ch] as 4 SW128 chunks
-  static constexpr int w7 = y + 4 * 16384;             // kW7Stages x [64 rows][64]
+  static constexpr int w6 = x + kXStages * 16384;      // kW6Stages x [128 rows][64]
+  static constexpr int y = w6 + kW6Stages * 16384;     // 2 x [128 px][128 ch] as 2 SW128 chunks each
+  static constexpr int w7 = y + 2 * 32768;             // kW7Stages x [64 rows][64]
   static constexpr int stg = w7 + kW7Stages * 8192;    // 4 warps x [32 px][<=64 ch]
-  static constexpr int bias = stg + 4 * 4096;          // b6/s6 block (2 x 256) + b7 (64)
-  static constexpr int bars = bias + (2 * 256 + 64) * 4;
+  static constexpr int bias = stg + 4 * 4096;          // b6/s6 per Y buffer (2 x 2 x 128) + b7 (64)
+  static constexpr int bars = bias + (4 * kNB + 64) * 4;
   static constexpr int total = bars + 256;
   static_assert(total + 1024 <= 232448, "smem budget");
 };
@@ -67,9 +69,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
   uint8_t* sy = smem + HeadSmem::y;
   uint8_t* sw7 = smem + HeadSmem::w7;
   uint8_t* stg = smem + HeadSmem::stg;
-  float* sb6 = reinterpret_cast<float*>(smem + HeadSmem::bias);
-  float* ss6 = sb6 + 256;
-  float* sb7 = ss6 + 256;
+  float* sb6 = reinterpret_cast<float*>(smem + HeadSmem::bias);  // [2][128]
+  float* ss6 = sb6 + 2 * kNB;                                     // [2][128]
+  float* sb7 = ss6 + 2 * kNB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + HeadSmem::bars);
   uint64_t* x_full = bars;
   uint64_t* x_empty = x_full + kXStages;
@@ -77,16 +79,16 @@ __global__ void __launch_bounds__(kHThreads, 1)
   uint64_t* w6_empty = w6_full + kW6Stages;
   uint64_t* w7_full = w6_empty + kW6Stages;
   uint64_t* w7_empty = w7_full + kW7Stages;
-  uint64_t* a1_full = w7_empty + kW7Stages;
-  uint64_t* y_full = a1_full + 1;
-  uint64_t* y_empty = y_full + 1;
-  uint64_t* a2_full = y_empty + 1;
+  uint64_t* a1_full = w7_empty + kW7Stages;  // [2]
+  uint64_t* y_full = a1_full + 2;             // [2]
+  uint64_t* y_empty = y_full + 2;             // [2]
+  uint64_t* a2_full = y_empty + 2;
   uint64_t* a2_empty = a2_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
 
   const uint32_t warp = warp_id();
-  const int NB = p.nb;
-  const int kc_per_block = NB / 64;
+  constexpr int NB = kNB;
+  constexpr int kc_per_block = NB / 64;
   if (warp == 0 && elect_one()) {
     for (int g = 0; g < p.n_groups; ++g) {
       tma_prefetch(&maps.x[g]);
@@ -96,9 +98,11 @@ __global__ void __launch_bounds__(kHThreads, 1)
     for (int i = 0; i < kXStages; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
     for (int i = 0; i < kW6Stages; ++i) { mbar_init(&w6_full[i], 1); mbar_init(&w6_empty[i], 1); }
     for (int i = 0; i < kW7Stages; ++i) { mbar_init(&w7_full[i], 1); mbar_init(&w7_empty[i], 1); }
-    mbar_init(a1_full, 1);
-    mbar_init(y_full, 128);
-    mbar_init(y_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a1_full[i], 1);
+      mbar_init(&y_full[i], 128);
+      mbar_init(&y_empty[i], 1);
+    }
     mbar_init(a2_full, 1);
     mbar_init(a2_empty, 128);
     fence_barrier_init();
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
             if (++xs == kXStages) { xs = 0; xph ^= 1; }
             mbar_wait(&w6_empty[w6s], w6ph ^ 1);
             mbar_arrive_expect_tx(&w6_full[w6s], NB * 128);
-            tma_load_2d_hint(sw6 + w6s * 32768, &maps.w6[g], &w6_full[w6s], c * 64, j * NB, keep);
+            tma_load_2d_hint(sw6 + w6s * 16384, &maps.w6[g], &w6_full[w6s], c * 64, j * NB, keep);
             if (++w6s == kW6Stages) { w6s = 0; w6ph ^= 1; }
           }
           for (int kc = 0; kc < kc_per_block; ++kc) {
@@ -142,51 +146,60 @@ __global__ void __launch_bounds__(kHThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
-      const uint32_t idesc1 = idesc_bf16_f32(128, uint32_t(NB));
+      const uint32_t idesc1 = idesc_bf16_f32(128, NB);
       const uint32_t idesc2 = idesc_bf16_f32(128, 64);
       int xs = 0, w6s = 0, w7s = 0;
-      uint32_t xph = 0, w6ph = 0, w7ph = 0, yfph = 0, a2eph = 0;
+      uint32_t xph = 0, w6ph = 0, w7ph = 0, a2eph = 0;
+      uint32_t yfph[2] = {0, 0};
+      int bc = 0;  // running block counter: Y / acc1 buffer = bc & 1
       const uint32_t x_base = smem_u32(sx), w6_base = smem_u32(sw6), y_base = smem_u32(sy),
                      w7_base = smem_u32(sw7);
+      // MMA2 of one block: acc2 (+)= Y[b] * W7[:, block]^T
+      auto mma2 = [&](int jb, int b, bool first_of_tile) {
+        mbar_wait(&y_full[b], yfph[b]);  // Y[b] written (and acc1[b] drained)
+        yfph[b] ^= 1;
+        if (first_of_tile) {  // acc2 drained by the previous tile's epilogue
+          mbar_wait(a2_empty, a2eph ^ 1);
+          a2eph ^= 1;
+        }
+        tc_fence_after();
+        for (int kc = 0; kc < kc_per_block; ++kc) {
+          mbar_wait(&w7_full[w7s], w7ph);
+          tc_fence_after();
+          const uint32_t ya = y_base + b * 32768 + kc * 16384, wb = w7_base + w7s * 8192;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16_ss(tmem + kAcc2Col, desc_sw128(ya + kk * 32), desc_sw128(wb + kk * 32), idesc2,
+                        (first_of_tile && kc == 0 && kk == 0) ? 0u : 1u);
+          mma_commit(&w7_empty[w7s]);
+          if (++w7s == kW7Stages) { w7s = 0; w7ph ^= 1; }
+        }
+        mma_commit(&y_empty[b]);
+        (void)jb;
+      };
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-        for (int j = 0; j < p.blocks; ++j) {
-          // acc1 is free: the epilogue signalled y_full for block j-1 (waited
-          // below before MMA2 of j-1) after its last read of acc1
+        for (int j = 0; j < p.blocks; ++j, ++bc) {
+          const int b = bc & 1;
+          // acc1[b] is free: its previous block's y_full was waited in the
+          // MMA2 issued before this point
           for (int c = 0; c < p.cin_chunks; ++c) {
             mbar_wait(&x_full[xs], xph);
             mbar_wait(&w6_full[w6s], w6ph);
             tc_fence_after();
-            const uint32_t xa = x_base + xs * 16384, wb = w6_base + w6s * 32768;
+            const uint32_t xa = x_base + xs * 16384, wb = w6_base + w6s * 16384;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ss(tmem, desc_sw128(xa + kk * 32), desc_sw128(wb + kk * 32), idesc1,
+              mma_bf16_ss(tmem + b * NB, desc_sw128(xa + kk * 32), desc_sw128(wb + kk * 32), idesc1,
                           (c == 0 && kk == 0) ? 0u : 1u);
             mma_commit(&x_empty[xs]);
             mma_commit(&w6_empty[w6s]);
             if (++xs == kXStages) { xs = 0; xph ^= 1; }
             if (++w6s == kW6Stages) { w6s = 0; w6ph ^= 1; }
           }
-          mma_commit(a1_full);
-          mbar_wait(y_full, yfph);  // Y block j written (and acc1 drained)
-          yfph ^= 1;
-          if (j == 0) {  // acc2 drained by the previous tile's epilogue
-            mbar_wait(a2_empty, a2eph ^ 1);
-            a2eph ^= 1;
-          }
-          tc_fence_after();
-          for (int kc = 0; kc < kc_per_block; ++kc) {
-            mbar_wait(&w7_full[w7s], w7ph);
-            tc_fence_after();
-            const uint32_t ya = y_base + kc * 16384, wb = w7_base + w7s * 8192;
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ss(tmem + kAcc2Col, desc_sw128(ya + kk * 32), desc_sw128(wb + kk * 32), idesc2,
-                          (j == 0 && kc == 0 && kk == 0) ? 0u : 1u);
-            mma_commit(&w7_empty[w7s]);
-            if (++w7s == kW7Stages) { w7s = 0; w7ph ^= 1; }
-          }
-          mma_commit(y_empty);
+          mma_commit(&a1_full[b]);
+          if (j > 0) mma2(j - 1, b ^ 1, j == 1);  // the previous block, converted meanwhile
         }
+        mma2(p.blocks - 1, (bc - 1) & 1, p.blocks == 1);
         mma_commit(a2_full);
       }
     }
@@ -201,7 +214,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
     const uint32_t lane_base = (quad * 32) << 16;
     uint8_t* stg_w = stg + quad * 4096;
     uint8_t* yrow = sy + px * 128;  // this pixel's row in every 16 KB Y chunk
-    uint32_t a1ph = 0, yeph = 0, a2fph = 0;
+    uint32_t a1ph[2] = {0, 0}, yeph[2] = {0, 0}, a2fph = 0;
+    int bc = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       int gi, n, pt;
       head_decode(p, t, gi, n, pt);
@@ -210,38 +224,42 @@ __global__ void __launch_bounds__(kHThreads, 1)
       const int hh = o / p.Wp;
       const int ww = o - hh * p.Wp;
       const bool valid = hh < p.H && ww < p.W;
-      for (int j = 0; j < p.blocks; ++j) {
+      for (int j = 0; j < p.blocks; ++j, ++bc) {
+        const int b = bc & 1;
+        float* bs = sb6 + b * NB;
+        float* ss = ss6 + b * NB;
         // this block's bias / slope: every epilogue warp is done with the
-        // previous block's (and the previous tile's b7) before they change
+        // slices' previous block (and the previous tile's b7) before they change
         named_bar_sync(1, 128);
-        for (int i = ep; i < NB; i += 128) {
-          const int co = j * NB + i;
-          sb6[i] = g.bias6[co];
-          ss6[i] = g.act6 == 1 ? 0.f : g.act6 == 2 ? g.slope6[co] : 1.f;
+        {
+          const int co = j * NB + ep;  // NB == 128 == epilogue threads
+          bs[ep] = g.bias6[co];
+          ss[ep] = g.act6 == 1 ? 0.f : g.act6 == 2 ? g.slope6[co] : 1.f;
         }
         if (j == 0 && ep < 64) sb7[ep] = ep < g.c7 ? g.bias7[ep] : 0.f;
         named_bar_sync(1, 128);
-        mbar_wait(y_empty, yeph ^ 1);  // MMA2 of the previous block released Y
-        yeph ^= 1;
-        mbar_wait(a1_full, a1ph);
-        a1ph ^= 1;
+        mbar_wait(&y_empty[b], yeph[b] ^ 1);  // MMA2 of this buffer's previous block released Y[b]
+        yeph[b] ^= 1;
+        mbar_wait(&a1_full[b], a1ph[b]);
+        a1ph[b] ^= 1;
         tc_fence_after();
+#pragma unroll
         for (int c0 = 0; c0 < NB; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tmem + lane_base + c0, v);
+          tmem_ld32(tmem + lane_base + b * NB + c0, v);
           tmem_ld_wait();
-          uint8_t* chunk = yrow + (c0 >> 6) * 16384;
+          uint8_t* chunk = yrow + b * 32768 + (c0 >> 6) * 16384;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint32_t w[4];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
               const int c = c0 + q * 8 + 2 * jj;
-              float a = __uint_as_float(v[q * 8 + 2 * jj]) + sb6[c];
-              float b = __uint_as_float(v[q * 8 + 2 * jj + 1]) + sb6[c + 1];
-              a = fmaxf(a, 0.f) + ss6[c] * fminf(a, 0.f);
-              b = fmaxf(b, 0.f) + ss6[c + 1] * fminf(b, 0.f);
-              w[jj] = pack2(a, b);
+              float x0 = __uint_as_float(v[q * 8 + 2 * jj]) + bs[c];
+              float x1 = __uint_as_float(v[q * 8 + 2 * jj + 1]) + bs[c + 1];
+              x0 = fmaxf(x0, 0.f) + ss[c] * fminf(x0, 0.f);
+              x1 = fmaxf(x1, 0.f) + ss[c + 1] * fminf(x1, 0.f);
+              w[jj] = pack2(x0, x1);
             }
             const uint32_t qq = ((c0 & 63) >> 3) + q;  // 16-byte chunk within the 128-byte row
             *reinterpret_cast<uint4*>(chunk + ((qq ^ (uint32_t(px) & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -249,7 +267,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         }
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(y_full);
+        mbar_arrive(&y_full[b]);
       }
       // ---- epilogue 2: acc2 (+ b7) -> outputs
       mbar_wait(a2_full, a2fph);

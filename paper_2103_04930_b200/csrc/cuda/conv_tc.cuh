@@ -129,14 +129,14 @@ struct HeadGroup {
 struct HeadParams {
   int n_images, H, W, Hp, Wp, P;
   int in_c_off, cin_chunks;
-  int nb, blocks;       // c6 = nb * blocks, nb in {64, 128, 256}
+  int nb, blocks;       // c6 = nb * blocks, nb = 128
   int tiles_per_image, total_tiles, n_groups;
   HeadGroup g[kConvMaxGroups];
 };
 
 struct HeadMaps {
   CUtensorMap x[kConvMaxGroups];    // input, box {64 ch, 128 rows}
-  CUtensorMap w6[kConvMaxGroups];   // [c6_pad][cin_pad], box {64, nb rows}
+  CUtensorMap w6[kConvMaxGroups];   // [c6_pad][cin_pad], box {64, 128 rows}
   CUtensorMap w7[kConvMaxGroups];   // [c7_pad][c6], box {64, 64 rows}
   CUtensorMap out32[kConvMaxGroups], out16[kConvMaxGroups], out8[kConvMaxGroups];
 };

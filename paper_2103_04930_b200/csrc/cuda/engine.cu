@@ -484,7 +484,7 @@ struct PlanBuilder {
     p.P = gi.P;
     p.in_c_off = in[0].c_off;
     p.cin_chunks = A0.cin_pad / 64;
-    p.nb = A0.def.cout < 256 ? A0.def.cout : 256;
+    p.nb = 128;
     p.blocks = A0.def.cout / p.nb;
     p.tiles_per_image = (p.H * p.Wp + 127) / 128;
     p.n_groups = int(l6.size());
@@ -511,7 +511,7 @@ struct PlanBuilder {
       hg.out2_c_stride = out2.empty() ? 0 : out2[g].c_stride;
       const int ib = in[g].buf;
       op.hm.x[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 128);
-      op.hm.w6[g] = make_map_2d(A.w, A.cin_pad, A.cout_pad, uint32_t(p.nb));
+      op.hm.w6[g] = make_map_2d(A.w, A.cin_pad, A.cout_pad, 128);
       op.hm.w7[g] = make_map_2d(B.w, B.cin_pad, B.cout_pad, 64);
       if (o.buf != -1) {
         op.hm.out32[g] = make_map_3d_store(plan.bufs[o.buf]->p, plan.buf_c[o.buf], uint64_t(gi.Hp()) * gi.Wp(), plan.n, 32);
