@@ -59,7 +59,8 @@ build/avec_stub_server: tests/native/stub_server.cpp $(LIB)/libavec_host.so
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -I$(HOST_DIR) -o $@ $< -L$(LIB) -lavec_host -lavec_cuda -Wl,-rpath,'$$ORIGIN/../$(LIB)' -lpthread
 
-oracle:
+# the reference drivers include ref_b200_server, which links libavec_cuda.so
+oracle: $(LIB)/libavec_cuda.so
 	$(MAKE) -C oracle oracle
 	@if [ -d /root/reference/proj ]; then $(MAKE) -C oracle ref; else echo "no /root/reference: using prebuilt oracle/_ref"; fi
 
