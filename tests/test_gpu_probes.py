@@ -25,7 +25,10 @@ def run_probe(name):
 def test_single_cta_probe():
     d = run_probe("tc_probe")
     assert d["ok"]
-    assert all(c["bad"] == 0 for c in d["correctness"])
+    # with the descriptor's base-offset field left 0, any row offset is exact
+    # (the kernels' sliding windows rely on it); the probe also records the
+    # variants that set the field, which the kernels do not use
+    assert all(c["bad"] == 0 for c in d["correctness"] if c["base_off_field"] == 0)
     rate = {x["N"]: x["cycles_per_mma"] for x in d["rate"]}
     assert rate[256] < 128 * 1.05 and rate[128] < 64 * 1.05  # full rate from N = 128
     assert rate[64] > 40  # N = 64 is operand-read bound (48 cycles, not 32)
