@@ -49,12 +49,13 @@ CONFIGS = {
 }
 CFG = CONFIGS["c2"]
 W, H, BATCH = CFG["width"], CFG["height"], CFG["global_batch"]  # BATCH = frames per rank per step
-# Execution slots per GPU = cycles in flight. Measured (profiles/README.md):
-# device-resident throughput saturates at 2 streams, the e2e C-ABI path gains
-# from a third slot (its H2D/D2H overlap the other two cycles' kernels: C2
-# +3.4%, C5 +4%), and through the wire 2 server slots beat 3-4 (host-side TCP
-# work per extra concurrent cycle). AVEC_SLOTS / AVEC_WIRE_SLOTS override.
-SLOTS = int(os.environ.get("AVEC_SLOTS", "3"))          # avec_ctx slots (e2e threads up to this)
+# Execution slots per GPU = cycles in flight. Measured (tools/ab_slots.sh):
+# device-resident throughput saturates at 2 streams; the e2e C-ABI path gains
+# from third and fourth slots (their H2D/D2H overlap the other cycles'
+# kernels: 2 -> 3 -> 4 slots C2 2525 -> 2611 -> 2623, C5 840 -> 870 -> 889);
+# through the wire 2 server slots beat 3-4 (host-side TCP work per extra
+# concurrent cycle). AVEC_SLOTS / AVEC_WIRE_SLOTS override.
+SLOTS = int(os.environ.get("AVEC_SLOTS", "4"))          # avec_ctx slots (e2e threads up to this)
 DEV_STREAMS = 2                                        # cycles in flight for the device-resident value
 WIRE_SLOTS = int(os.environ.get("AVEC_WIRE_SLOTS", "2"))
 
