@@ -1,6 +1,7 @@
 // Pose-net post-processing: heatmap/PAF bilinear upsample and 3x3 peak NMS.
 // Arithmetic uses explicit _rn intrinsics in the exact order of the CPU oracle
 // (oracle/post_oracle.c, compiled with -ffp-contract=off): bit-exact parity.
+#include <algorithm>
 #include <cstdint>
 
 #include "engine.hpp"
@@ -52,6 +53,101 @@ __global__ void upsample_kernel(const float* __restrict__ in, int planes, int h,
       make_float4(r[0], r[1], r[2], r[3]);
 }
 
+// Power-of-two scales (the pose net's x8): (o + 0.5) / scale is exact as a
+// multiply by 1/scale, so the coordinates match src_coord bit for bit without
+// the division.
+__device__ __forceinline__ float src_coord_pow2(int o, float inv_scale, int n, int& i0, int& i1) {
+  float f = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(o), 0.5f), inv_scale), 0.5f);
+  if (f < 0.0f) f = 0.0f;
+  int a = static_cast<int>(f);
+  if (a > n - 1) a = n - 1;
+  i0 = a;
+  i1 = (a + 1 < n) ? a + 1 : n - 1;
+  return __fsub_rn(f, static_cast<float>(a));
+}
+
+// one thread per 8 consecutive outputs of a row (two float4 stores). Their
+// source columns span at most 3 consecutive inputs per source row, loaded
+// once and selected per output.
+// x8 interior groups (1 <= g < w - 1): outputs 8g+j sit at f = g - 1 + (j + 4.5) / 8
+// (j < 4: between source columns g-1, g; j >= 4: between g, g+1). Every step
+// of src_coord is exact in fp32 there, so lx is the constant (j + 4.5) / 8 mod 1
+// and the result equals the general kernel's bit for bit.
+__global__ void upsample8_interior_kernel(const float* __restrict__ in, int h, int w, float* __restrict__ out) {
+  const int wo = w * 8, ho = h * 8;
+  const int g = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= w - 1) return;
+  const int oy = blockIdx.y;
+  const int pl = blockIdx.z;
+  const float* src = in + static_cast<size_t>(pl) * h * w;
+  int y0, y1;
+  const float ly = src_coord_pow2(oy, 0.125f, h, y0, y1);
+  const float* r0 = src + static_cast<size_t>(y0) * w + (g - 1);
+  const float* r1 = src + static_cast<size_t>(y1) * w + (g - 1);
+  const float a0 = __ldg(r0), a1 = __ldg(r0 + 1), a2 = __ldg(r0 + 2);
+  const float b0 = __ldg(r1), b1 = __ldg(r1 + 1), b2 = __ldg(r1 + 2);
+  constexpr float kLx[8] = {0.5625f, 0.6875f, 0.8125f, 0.9375f, 0.0625f, 0.1875f, 0.3125f, 0.4375f};
+  float r[8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) r[j] = lerp2(lerp2(a0, a1, kLx[j]), lerp2(b0, b1, kLx[j]), ly);
+#pragma unroll
+  for (int j = 4; j < 8; ++j) r[j] = lerp2(lerp2(a1, a2, kLx[j]), lerp2(b1, b2, kLx[j]), ly);
+  float4* o4 = reinterpret_cast<float4*>(out + (static_cast<size_t>(pl) * ho + oy) * wo) + 2 * g;
+  o4[0] = make_float4(r[0], r[1], r[2], r[3]);
+  o4[1] = make_float4(r[4], r[5], r[6], r[7]);
+}
+
+// one 8-output group: the general path of the pow2 kernels
+__device__ __forceinline__ void upsample_group(const float* __restrict__ in, int h, int w, int scale, float inv_scale,
+                                               float* __restrict__ out, int pl, int oy, int g) {
+  const int wo = w * scale, ho = h * scale;
+  const float* src = in + static_cast<size_t>(pl) * h * w;
+  int y0, y1;
+  const float ly = src_coord_pow2(oy, inv_scale, h, y0, y1);
+  int c0, c0b;
+  src_coord_pow2(g * 8, inv_scale, w, c0, c0b);  // first output's left source column
+  const int c1 = c0 + 1 < w ? c0 + 1 : w - 1, c2 = c0 + 2 < w ? c0 + 2 : w - 1;
+  const float* r0 = src + static_cast<size_t>(y0) * w;
+  const float* r1 = src + static_cast<size_t>(y1) * w;
+  const float a0 = __ldg(r0 + c0), a1 = __ldg(r0 + c1), a2 = __ldg(r0 + c2);
+  const float b0 = __ldg(r1 + c0), b1 = __ldg(r1 + c1), b2 = __ldg(r1 + c2);
+  float r[8];
+  float4* o4 = reinterpret_cast<float4*>(out + (static_cast<size_t>(pl) * ho + oy) * wo) + 2 * g;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    int x0, x1;
+    const float lx = src_coord_pow2(g * 8 + j, inv_scale, w, x0, x1);
+    // x0 - c0 and x1 - c0 are in {0, 1, 2} (clamped columns alias)
+    const int d0 = x0 - c0, d1 = x1 - c0;
+    const float ta = d0 == 0 ? a0 : d0 == 1 ? a1 : a2, tb = d1 == 0 ? a0 : d1 == 1 ? a1 : a2;
+    const float ba = d0 == 0 ? b0 : d0 == 1 ? b1 : b2, bb = d1 == 0 ? b0 : d1 == 1 ? b1 : b2;
+    const float top = lerp2(ta, tb, lx);
+    const float bot = lerp2(ba, bb, lx);
+    r[j] = lerp2(top, bot, ly);
+  }
+  o4[0] = make_float4(r[0], r[1], r[2], r[3]);
+  o4[1] = make_float4(r[4], r[5], r[6], r[7]);
+}
+
+// grid (column groups, output rows, planes): no integer division per thread
+__global__ void upsample_pow2_kernel(const float* __restrict__ in, int planes, int h, int w, int scale,
+                                     float inv_scale, float* __restrict__ out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= w * scale / 8) return;
+  upsample_group(in, h, w, scale, inv_scale, out, blockIdx.z, blockIdx.y, g);
+}
+
+// the two border groups (0 and w - 1) of every x8 output row, one per thread
+__global__ void upsample8_border_kernel(const float* __restrict__ in, int planes, int h, int w,
+                                        float* __restrict__ out) {
+  const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned ho = static_cast<unsigned>(h) * 8;
+  if (idx >= 2u * ho * static_cast<unsigned>(planes)) return;
+  const unsigned rest = idx >> 1;
+  const int oy = static_cast<int>(rest % ho), pl = static_cast<int>(rest / ho);
+  upsample_group(in, h, w, 8, 0.125f, out, pl, oy, (idx & 1u) ? w - 1 : 0);
+}
+
 // Peak test for the pixel this lane owns in row y; neighbours come from the
 // lanes on either side (warp shuffles) and rows y-1 / y+1 loaded per lane.
 __device__ __forceinline__ bool lane_peak(const float* __restrict__ pl, int H, int W, int y, int x,
@@ -83,6 +179,135 @@ __device__ __forceinline__ bool lane_peak(const float* __restrict__ pl, int H, i
   if (!inb || !(v > threshold)) return false;
   // out-of-plane neighbours are -inf, so "strictly greater" ignores them
   return v > lv && v > lu && v > ld && v > rv && v > ru && v > rd && v > up && v > dn;
+}
+
+// ---- tiled variant (W % 4 == 0): a block stages rows y0-1 .. y0+R of one
+// plane in shared memory with coalesced float4 loads (many in flight), then
+// each thread tests four columns per row from the tile. Rows and columns
+// outside the plane read as -inf, so "strictly greater" ignores them.
+constexpr int kNmsRows = 8;
+
+__device__ __forceinline__ void nms_stage_tile(float* tile, const float* __restrict__ p, int H, int W, int y0,
+                                               int rows) {
+  const float NEG = -__int_as_float(0x7f800000);
+  const int W4 = W >> 2;
+  const int n = (rows + 2) * W4;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int rr = i / W4, c4 = i - rr * W4;
+    const int y = y0 - 1 + rr;
+    const float4 v = (y >= 0 && y < H) ? __ldg(reinterpret_cast<const float4*>(p + static_cast<size_t>(y) * W) + c4)
+                                       : make_float4(NEG, NEG, NEG, NEG);
+    reinterpret_cast<float4*>(tile + rr * W)[c4] = v;
+  }
+}
+
+// peak mask of columns 4*x4 .. 4*x4+3 of tile row r+1 (= image row y0 + r)
+__device__ __forceinline__ unsigned nms_tile_peaks(const float* tile, int W, int r, int x4, float threshold,
+                                                   float (&mid)[4]) {
+  const float NEG = -__int_as_float(0x7f800000);
+  if (x4 >= (W >> 2)) return 0u;
+  float row[3][6];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float* t = tile + (r + k) * W + 4 * x4;
+    const float4 c = reinterpret_cast<const float4*>(t)[0];
+    row[k][0] = x4 > 0 ? t[-1] : NEG;
+    row[k][1] = c.x; row[k][2] = c.y; row[k][3] = c.z; row[k][4] = c.w;
+    row[k][5] = 4 * x4 + 4 < W ? t[4] : NEG;
+  }
+  unsigned m = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float v = row[1][i + 1];
+    mid[i] = v;
+    const bool pk = v > threshold && v > row[0][i] && v > row[0][i + 1] && v > row[0][i + 2] && v > row[1][i] &&
+                    v > row[1][i + 2] && v > row[2][i] && v > row[2][i + 1] && v > row[2][i + 2];
+    m |= pk ? (1u << i) : 0u;
+  }
+  return m;
+}
+
+__global__ void nms4_count_kernel(const float* __restrict__ in, int H, int W, float threshold,
+                                  int* __restrict__ row_counts) {
+  extern __shared__ __align__(16) float tile[];
+  __shared__ int rows_cnt[kNmsRows];
+  const int y0 = blockIdx.x * kNmsRows, pl = blockIdx.y;
+  const int rows = y0 + kNmsRows < H ? kNmsRows : H - y0;
+  const float* p = in + static_cast<size_t>(pl) * H * W;
+  if (threadIdx.x < kNmsRows) rows_cnt[threadIdx.x] = 0;
+  nms_stage_tile(tile, p, H, W, y0, rows);
+  __syncthreads();
+  for (int r = 0; r < rows; ++r) {
+    int cnt = 0;
+    for (int x4 = threadIdx.x; x4 < (W >> 2); x4 += blockDim.x) {
+      float mid[4];
+      cnt += __popc(nms_tile_peaks(tile, W, r, x4, threshold, mid));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&rows_cnt[r], cnt);
+  }
+  __syncthreads();
+  if (threadIdx.x < rows) row_counts[static_cast<size_t>(pl) * H + y0 + threadIdx.x] = rows_cnt[threadIdx.x];
+}
+
+// one pass over a row per iteration: blockDim covers W / 4 columns
+__global__ void nms4_write_kernel(const float* __restrict__ in, int H, int W, float threshold, int max_peaks,
+                                  const int* __restrict__ row_offsets, float* __restrict__ peaks) {
+  extern __shared__ __align__(16) float tile[];
+  __shared__ int warp_cnt[32];
+  const int y0 = blockIdx.x * kNmsRows, pl = blockIdx.y;
+  const int rows = y0 + kNmsRows < H ? kNmsRows : H - y0;
+  const float* p = in + static_cast<size_t>(pl) * H * W;
+  if (row_offsets[static_cast<size_t>(pl) * H + y0] >= max_peaks) return;
+  nms_stage_tile(tile, p, H, W, y0, rows);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int x4 = threadIdx.x;
+  for (int r = 0; r < rows; ++r) {
+    const int y = y0 + r;
+    const int base = row_offsets[static_cast<size_t>(pl) * H + y];
+    if (base >= max_peaks) return;  // uniform: later rows start later
+    float mid[4];
+    const unsigned m = nms_tile_peaks(tile, W, r, x4, threshold, mid);
+    // raster rank: peaks of earlier lanes / warps, then earlier columns of this thread
+    const int mine = __popc(m);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_cnt[wid] = incl;
+    __syncthreads();
+    int before = 0;
+    for (int i = 0; i < wid; ++i) before += warp_cnt[i];
+    int idx = base + before + incl - mine;
+    for (int i = 0; i < 4; ++i) {
+      if (!((m >> i) & 1u)) continue;
+      if (idx < max_peaks) {
+        const int x = 4 * x4 + i;
+        float sw = 0.0f, sx = 0.0f, sy = 0.0f;
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int yy = y + dy, xx = x + dx;
+            if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+            const float sv = tile[(r + 1 + dy) * W + xx];
+            sw = __fadd_rn(sw, sv);
+            sx = __fadd_rn(sx, __fmul_rn(static_cast<float>(xx), sv));
+            sy = __fadd_rn(sy, __fmul_rn(static_cast<float>(yy), sv));
+          }
+        float* o = peaks + (static_cast<size_t>(pl) * max_peaks + idx) * 5;
+        o[0] = static_cast<float>(x);
+        o[1] = static_cast<float>(y);
+        o[2] = __fdiv_rn(sx, sw);
+        o[3] = __fdiv_rn(sy, sw);
+        o[4] = mid[i];
+      }
+      ++idx;
+    }
+    __syncthreads();  // warp_cnt is rewritten for the next row
+  }
 }
 
 // pass 1: per (plane, row) peak counts
@@ -175,6 +400,24 @@ __global__ void nms_write_kernel(const float* __restrict__ in, int H, int W, flo
 
 void launch_upsample(const float* d_in, int planes, int h, int w, int scale, float* d_out,
                      cudaStream_t stream) {
+  const bool pow2 = scale >= 8 && scale <= 64 && (scale & (scale - 1)) == 0;
+  if (pow2 && h * scale <= 65535 && planes <= 65535) {  // 8 outputs per thread: <= 3 source columns each side
+    const int wg = w * scale / 8;
+    const float inv = 1.0f / static_cast<float>(scale);
+    if (scale == 8 && w >= 3) {  // interior groups on the fast kernel, the two border groups apart
+      const int n = w - 2;
+      const int tpb = n >= 128 ? 128 : (n + 31) / 32 * 32;
+      upsample8_interior_kernel<<<dim3((n + tpb - 1) / tpb, h * 8, planes), tpb, 0, stream>>>(d_in, h, w, d_out);
+      const unsigned nb = 2u * static_cast<unsigned>(h) * 8u * static_cast<unsigned>(planes);
+      upsample8_border_kernel<<<(nb + 255) / 256, 256, 0, stream>>>(d_in, planes, h, w, d_out);
+    } else {
+      const int tpb = wg >= 128 ? 128 : (wg + 31) / 32 * 32;
+      upsample_pow2_kernel<<<dim3((wg + tpb - 1) / tpb, h * scale, planes), tpb, 0, stream>>>(
+          d_in, planes, h, w, scale, inv, d_out);
+    }
+    check_cuda(cudaGetLastError(), "upsample launch");
+    return;
+  }
   if ((w * scale) % 4 != 0) fail(AVEC_ERR_UNSUPPORTED, "upsample needs output width % 4 == 0");
   const long long total = static_cast<long long>(planes) * h * scale * (w * scale / 4);
   upsample_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(
@@ -194,6 +437,23 @@ void launch_nms(const float* d_in, int planes, int H, int W, float threshold, in
   int* row_counts = static_cast<int*>(d_scratch);
   int* row_offsets = row_counts + static_cast<size_t>(planes) * H;
   dim3 grid(H, planes);
+  if (W % 4 == 0 && W <= 4096) {  // row tiles in smem, four columns per thread
+    const int threads = ((W / 4) + 31) / 32 * 32;
+    const size_t tile_bytes = static_cast<size_t>(kNmsRows + 2) * W * sizeof(float);
+    if (tile_bytes > 48 * 1024) {  // wide planes (C5's 1312 columns): opt in to the larger carve-out
+      check_cuda(cudaFuncSetAttribute(nms4_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(tile_bytes)), "nms smem");
+      check_cuda(cudaFuncSetAttribute(nms4_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(tile_bytes)), "nms smem");
+    }
+    dim3 grid4((H + kNmsRows - 1) / kNmsRows, planes);
+    nms4_count_kernel<<<grid4, threads, tile_bytes, stream>>>(d_in, H, W, threshold, row_counts);
+    nms_scan_kernel<<<planes, 32, 0, stream>>>(row_counts, H, max_peaks, row_offsets, d_counts);
+    nms4_write_kernel<<<grid4, threads, tile_bytes, stream>>>(d_in, H, W, threshold, max_peaks, row_offsets,
+                                                              d_peaks);
+    check_cuda(cudaGetLastError(), "nms launch");
+    return;
+  }
   nms_count_kernel<<<grid, 256, 0, stream>>>(d_in, H, W, threshold, row_counts);
   nms_scan_kernel<<<planes, 32, 0, stream>>>(row_counts, H, max_peaks, row_offsets, d_counts);
   nms_write_kernel<<<grid, 256, 0, stream>>>(d_in, H, W, threshold, max_peaks, row_offsets,
