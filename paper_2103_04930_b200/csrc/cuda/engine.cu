@@ -126,11 +126,12 @@ CUtensorMap make_map_3d_store(const void* base, uint64_t cols, uint64_t rows, ui
 
 // [N][Hp][Wp][C] with [16 px][64 ch] boxes along one padded row (the fused
 // pool's output rows; boxes are clipped at the row end)
-CUtensorMap make_map_4d_store(const void* base, uint64_t C, uint64_t Wp, uint64_t Hp, uint64_t n) {
+CUtensorMap make_map_4d_store(const void* base, uint64_t C, uint64_t Wp, uint64_t Hp, uint64_t n,
+                              uint32_t box_px = 16) {
   CUtensorMap m;
   cuuint64_t dims[4] = {C, Wp, Hp, n};
   cuuint64_t strides[3] = {C * 2, Wp * C * 2, Hp * Wp * C * 2};
-  cuuint32_t box[4] = {64, 16, 1, 1};
+  cuuint32_t box[4] = {64, box_px, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

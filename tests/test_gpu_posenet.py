@@ -223,3 +223,22 @@ def test_nms_synthetic_peaks_and_edges(net):
         assert np.array_equal(p[i, :c[i], :2].astype(np.int32), xy)
         assert p[i, :c[i], 2:4].tobytes() == ref.tobytes()
     assert c[0] == 3 and c[1] == 0 and c[2] == maxp
+
+
+def test_first_layers_wide_frame(net):
+    """conv1_1 (row tiles of 128 columns, 4D stores clipped at the row end) and
+    conv1_2 (+ fused pool) on a frame whose width is not a multiple of 128."""
+    from paper_2103_04930_b200 import Dims, Frame
+    be, h = net["be"], net["h"]
+    w, hgt = 200, 48
+    frame = Frame(Dims(1, 3, hgt, w), O.batched_frame(w, hgt, 1, seed=11))
+    for i in (0, 1):
+        lin, lout = be.layer_io(h, frame, i)
+        wt, b, sl = net["wb"][i]
+        ref = O.conv2d_nhwc(lin, wt, b, relu=net["layers"][i].act, round_bf16=True, slope=sl)
+        if lout.shape[1] * 2 == lin.shape[1]:
+            ref = O.maxpool2_nhwc(ref)
+        err = np.linalg.norm(lout - ref) / np.linalg.norm(ref)
+        assert err <= 1e-3, (i, err)
+        tol = ulp_bf16(ref) + 1e-4 * float(np.abs(ref).max())
+        assert not (np.abs(lout - ref) > tol).any(), i
