@@ -1,22 +1,31 @@
-// Pixel-major tcgen05 implicit-GEMM convolution (sm_100a) for the VGG front
-// end and the other short-K layers.
+// Pixel-major tcgen05 implicit-GEMM convolution (sm_100a): every conv of the
+// pose nets except conv1_1 (conv_first.cu), the COCO 7x7 stage convs
+// (conv_tc.cu) and the fused Mconv6+Mconv7 heads (conv_head.cu).
 //
 // Same padded-flat activation layout, window-reuse trick and warp roles as the
 // swap-AB kernel (conv_tc.cu), with the GEMM oriented the other way:
 //   M = 128 output pixels (activation window = operand A),
-//   N = 64/128/256 output channels (weights = operand B), K = 64 per k-block.
+//   N = 64/96/128/256 output channels (weights = operand B), K = 64 per k-block.
 // The accumulator row of a pixel sits in one TMEM lane, so each epilogue
-// thread holds 32 consecutive channels of ITS pixel per tcgen05.ld and writes
-// them as 16-byte vectors straight into the pixel's NHWC row: no transpose, no
-// shared-memory staging, no barriers. That is what the high-resolution layers
-// need — their K is short (conv1_1: 64, conv1_2: 576), so the epilogue, not
-// the MMA, bounds them.
+// thread holds consecutive channels of ITS pixel per tcgen05.ld; it converts
+// them (bias, ReLU/PReLU, zero outside the image, bf16) into its warp's
+// swizzled [32 px][W ch] staging box and one lane issues a TMA store per box
+// (W = 64/32/16/8, so 52/38/26/19-channel heads need no scalar stores).
 //
 // Tile = 128 * SUBS_M pixels x N channels; TMEM holds 2 accumulator stages
 // (2 * SUBS_M * N <= 512 columns) so the epilogue of tile i overlaps the
 // mainloop of tile i+1. Positions outside the image (padded-width columns,
 // rows past H) are written as zeros, keeping the output's border valid
-// padding; rows past the image's padded extent are not written.
+// padding; rows past the image's padded extent are clipped by the store map.
+//
+// Variants (template parameters):
+//  * NCTA = 2: a CTA pair on one TPC (cta_group::2). The leader issues
+//    M = 256 MMAs; each CTA loads its own window and half of every weight
+//    k-block (N/2 rows), so the B operand is read once per SM.
+//  * POOL: conv + 2x2/2 max-pool. A CTA's two sub-tiles are output rows y0 and
+//    y0+1 at columns x0..x0+127 (four 136-row windows per chunk); the epilogue
+//    takes the max of the four raw sums, then bias / ReLU / bf16, and stores
+//    the pooled row through a 4D [N][Hp][Wp][C] map.
 #include <cuda_bf16.h>
 
 #include <type_traits>
