@@ -23,8 +23,9 @@
 //    columns. Used for large-K layers (7x7 stages) where the mainloop dwarfs
 //    the epilogue.
 //  * SUBS = 1: 128 x 256 with TWO accumulator stages in TMEM, so the epilogue
-//    of tile i overlaps the mainloop of tile i+1. Used for the small-K,
-//    high-resolution VGG layers where the epilogue is a large share.
+//    of tile i overlaps the mainloop of tile i+1. Only reachable through the
+//    AVEC_TC3 experiment (3x3 layers on this kernel); the short-K layers run
+//    on the pixel-major kernel (conv_pm.cu).
 //
 // Activation reuse: for each (channel chunk, filter row r) the producer loads
 // ONE window of 256*SUBS + 8 rows; the k taps s = 0..k-1 are MMA descriptors
@@ -32,7 +33,7 @@
 // address bits, validated by tests/native/tc_probe.cu), so a 7x7 conv reads
 // its input 7x, not 49x, from L2.
 //
-// Epilogue: TMEM -> registers (bias, ReLU, zero outside the image, bf16) ->
+// Epilogue: TMEM -> registers (bias, ReLU/PReLU, zero outside the image, bf16) ->
 // 128B-swizzled smem staging -> TMA bulk-tensor store of [32 px][64 ch] boxes
 // into the output's 3D view [N][Hp*Wp][C] (rows past the image are clipped by
 // the tensor bounds). Outputs that are not 64-channel slabs (the 38/19-channel
