@@ -843,8 +843,26 @@ void run_ops(avec_ctx* ctx, const Plan& plan, const PoseNet& net, size_t first, 
 Plan* get_plan(avec_ctx* ctx, Slot* slot, const Model& m, int n_img, int H, int W) {
   auto key = std::make_tuple(m.id, n_img, H, W);
   auto it = slot->plans.find(key);
-  if (it != slot->plans.end()) return it->second.get();
+  if (it != slot->plans.end()) {
+    it->second->last_use = ++slot->use_clock;
+    return it->second.get();
+  }
+  static const size_t max_plans = [] {
+    const char* e = std::getenv("AVEC_PLANS_PER_SLOT");
+    const int v = e ? std::atoi(e) : 4;
+    return size_t(v > 0 ? v : 1);
+  }();
+  if (slot->plans.size() >= max_plans) {
+    // the slot is leased to this caller; its last work may still be in flight
+    check_cuda(cudaStreamSynchronize(slot->stream), "plan eviction sync");
+    if (slot->pending) check_cuda(cudaEventSynchronize(slot->done), "plan eviction sync");
+    auto lru = slot->plans.begin();
+    for (auto p = slot->plans.begin(); p != slot->plans.end(); ++p)
+      if (p->second->last_use < lru->second->last_use) lru = p;
+    slot->plans.erase(lru);
+  }
   auto plan = std::make_unique<Plan>();
+  plan->last_use = ++slot->use_clock;
   plan->n = n_img;
   plan->H = H;
   plan->W = W;

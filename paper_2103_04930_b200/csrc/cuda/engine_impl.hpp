@@ -97,6 +97,7 @@ struct Plan {
   DevMem in, out;  // fp32 NCHW frames in, fp32 NCHW net output
   uint64_t in_elems = 0, out_elems = 0;
   cudaGraphExec_t graph = nullptr;
+  uint64_t last_use = 0;  // slot-local LRU clock
   ~Plan();
 };
 
@@ -109,7 +110,11 @@ struct Slot {
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   PinnedMem stage[2];
   DevMem d_in, d_out;  // segment-mean path
+  // cached plans (activation buffers + CUDA graph) per (model, frames, H, W),
+  // least recently used evicted beyond AVEC_PLANS_PER_SLOT (default 4): a
+  // long-lived server seeing many resolutions must not grow without bound
   std::map<std::tuple<uint64_t, int, int, int>, std::unique_ptr<Plan>> plans;
+  uint64_t use_clock = 0;
 };
 
 struct Model {

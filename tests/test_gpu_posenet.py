@@ -242,3 +242,20 @@ def test_first_layers_wide_frame(net):
         assert err <= 1e-3, (i, err)
         tol = ulp_bf16(ref) + 1e-4 * float(np.abs(ref).max())
         assert not (np.abs(lout - ref) > tol).any(), i
+
+
+def test_plan_cache_eviction_keeps_results():
+    """A slot keeps at most AVEC_PLANS_PER_SLOT (default 4) shape plans; the
+    least recently used one is evicted and rebuilt on demand, bit-identically."""
+    from paper_2103_04930_b200 import B200Backend, Dims, Frame, make_model, netspec
+    be = B200Backend(0, slots=1)
+    h = be.register_model(make_model("openpose", netspec.spec(), b"", netspec.COCO_DIVISOR))
+    shapes = [(64, 96), (64, 104), (72, 96), (64, 112), (80, 96), (64, 120)]
+    first = {}
+    for (hh, ww) in shapes:
+        f = Frame(Dims(1, 3, hh, ww), O.batched_frame(ww, hh, 1, seed=hh + ww))
+        first[(hh, ww)] = (f, be.forward(h, f).data.copy())
+    for (hh, ww) in shapes[:3]:  # evicted by now: rebuilt
+        f, ref = first[(hh, ww)]
+        assert be.forward(h, f).data.tobytes() == ref.tobytes()
+    be.close()
