@@ -99,6 +99,26 @@ int avec_upsample_device(avec_ctx* ctx, const float* d_in, int planes, int h, in
 int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, float threshold,
                     int max_peaks, int* d_counts, float* d_peaks, void* cuda_stream);
 
+/* Bottom-up person assembly (OpenPose parsing; SURVEY.md §8 f rank 4, not in
+ * the reference). Peaks come from avec_nms_device on the part heatmaps
+ * ([n_parts][max_peaks][5] = x, y, refined x, refined y, score); `d_paf` holds
+ * the (upsampled) PAF planes. avec_paf_candidates_device scores every
+ * candidate limb: d_cand [n_limbs][max_peaks][max_peaks][2] = (score, valid),
+ * limb l joining parts limb_parts[2l] -> limb_parts[2l+1] along PAF planes
+ * limb_paf[2l] (x), limb_paf[2l+1] (y) (host arrays, n_limbs <= 32).
+ * avec_assemble_people (host buffers) matches limbs greedily and merges them
+ * into people: people [max_people][n_parts] peak index (-1 none), people_score
+ * [max_people][2] = (total score, parts). Limb types >= new_row_limbs only
+ * extend people. avec_coco_limbs fills the 19 COCO limb types (parts 0..17,
+ * PAF planes 0..37 of the 38-plane PAF block; new_row_limbs = 17). */
+int avec_paf_candidates_device(avec_ctx* ctx, const float* d_paf, int H, int W, const int* d_counts,
+                               const float* d_peaks, int max_peaks, const int* limb_parts, const int* limb_paf,
+                               int n_limbs, float paf_threshold, float* d_cand, void* cuda_stream);
+int avec_assemble_people(const int* counts, const float* peaks, int n_parts, int max_peaks, const float* cand,
+                         const int* limb_parts, int n_limbs, int new_row_limbs, int max_people, int* people,
+                         float* people_score, int* n_people);
+int avec_coco_limbs(int* limb_parts, int* limb_paf, int* n_limbs, int* new_row_limbs);
+
 /* Debug/parity hook: run a forward like avec_forward and copy the input and
  * output activations of conv layer `layer` (weights-blob order) as unpadded
  * fp32 NHWC (input channels in the layer's own — Caffe — channel order).

@@ -54,6 +54,13 @@ void oracle_upsample_plane(const float* in, int h, int w, int scale, float* out)
 /* 3x3 NMS on one plane: a peak is > threshold and strictly > its 8 neighbours
  * (out-of-plane neighbours ignored). Writes up to max_peaks (x, y, score) in
  * raster order plus 3x3 weighted-average refined coordinates. Returns count. */
+/* PAF candidate scores [n_limbs][max_peaks][max_peaks][2] = (score, valid)
+ * and person assembly (oracle/paf_oracle.c). */
+void oracle_paf_candidates(const float* paf, int H, int W, const int* counts, const float* peaks, int max_peaks,
+                           const int* limb_parts, const int* limb_paf, int n_limbs, float paf_thr, float* cand);
+int oracle_assemble_people(const int* counts, const float* peaks, int n_parts, int max_peaks, const float* cand,
+                           const int* limb_parts, int n_limbs, int new_row_limbs, int max_people, int* people,
+                           float* people_score);
 int oracle_nms_plane(const float* in, int h, int w, float threshold, int max_peaks,
                      int* peak_xy, float* peak_refined_xy, float* peak_score);
 

@@ -32,6 +32,7 @@ EXPORTS = [
     "avec_output_elems", "avec_forward", "avec_forward_device", "avec_upsample_device",
     "avec_nms_device", "avec_posenet_layer_io", "avec_posenet_layer_out_level", "avec_posenet_layer_fusion", "avec_posenet_layer_info",
     "avec_posenet_num_layers", "avec_posenet_profile", "avec_posenet_synth_weights", "avec_host_alloc", "avec_host_free",
+    "avec_paf_candidates_device", "avec_assemble_people", "avec_coco_limbs",
 ]
 
 _lib = None
@@ -71,6 +72,9 @@ def load() -> ctypes.CDLL:
         "avec_posenet_layer_io": (i, [vp, u64, u32, u32, u32, u32, vp, i, vp, u64, vp, u64]),
         "avec_posenet_layer_out_level": (i, [vp, u64, u32, u32, u32, u32, i, c.POINTER(i)]),
         "avec_posenet_layer_fusion": (i, [vp, u64, u32, u32, u32, u32, i, c.POINTER(i), c.POINTER(i)]),
+        "avec_paf_candidates_device": (i, [vp, vp, i, i, vp, vp, i, vp, vp, i, c.c_float, vp, vp]),
+        "avec_assemble_people": (i, [vp, vp, i, i, vp, vp, i, i, i, vp, vp, c.POINTER(i)]),
+        "avec_coco_limbs": (i, [vp, vp, c.POINTER(i), c.POINTER(i)]),
         "avec_posenet_layer_info": (i, [vp, u64, i] + [c.POINTER(i)] * 5),
         "avec_posenet_num_layers": (i, [vp, u64, c.POINTER(i)]),
         "avec_posenet_profile": (i, [vp, u64, u32, u32, u32, u32, vp, i, i, c.POINTER(i), vp, vp, vp, vp]),

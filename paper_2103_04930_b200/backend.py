@@ -246,11 +246,49 @@ class B200Backend:
         _lib.check(self._L.avec_upsample_device(self._ctx, d_in, planes, h, w, scale, d_out,
                                                 ctypes.c_void_p(stream) if stream else None))
 
+    def paf_candidates_device(self, d_paf: int, h: int, w: int, d_counts: int, d_peaks: int, max_peaks: int,
+                              limb_parts: np.ndarray, limb_paf: np.ndarray, threshold: float, d_cand: int,
+                              stream: int = 0) -> None:
+        """Score every candidate limb on the device (avec_paf_candidates_device)."""
+        lp = np.ascontiguousarray(limb_parts, np.int32)
+        lf = np.ascontiguousarray(limb_paf, np.int32)
+        _lib.check(self._L.avec_paf_candidates_device(self._ctx, d_paf, h, w, d_counts, d_peaks, max_peaks,
+                                                      lp.ctypes.data, lf.ctypes.data, lp.shape[0], threshold, d_cand,
+                                                      ctypes.c_void_p(stream) if stream else None))
+
     def nms_device(self, d_in: int, planes: int, h: int, w: int, threshold: float, max_peaks: int,
                    d_counts: int, d_peaks: int, stream: int = 0) -> None:
         _lib.check(self._L.avec_nms_device(self._ctx, d_in, planes, h, w, threshold, max_peaks,
                                            d_counts, d_peaks,
                                            ctypes.c_void_p(stream) if stream else None))
+
+
+def coco_limbs():
+    """OpenPose COCO limb types: (limb_parts [19,2], limb_paf [19,2], new_row_limbs)."""
+    L = _lib.load()
+    parts = np.zeros((19, 2), np.int32)
+    paf = np.zeros((19, 2), np.int32)
+    n, new_rows = ctypes.c_int(0), ctypes.c_int(0)
+    _lib.check(L.avec_coco_limbs(parts.ctypes.data, paf.ctypes.data, ctypes.byref(n), ctypes.byref(new_rows)))
+    return parts, paf, new_rows.value
+
+
+def assemble_people(counts: np.ndarray, peaks: np.ndarray, cand: np.ndarray, limb_parts: np.ndarray,
+                    new_row_limbs: int, max_people: int = 64):
+    """Host person assembly (avec_assemble_people) -> (people [n][parts], scores [n][2])."""
+    L = _lib.load()
+    counts = np.ascontiguousarray(counts, np.int32)
+    peaks = np.ascontiguousarray(peaks, np.float32)
+    cand = np.ascontiguousarray(cand, np.float32)
+    limb_parts = np.ascontiguousarray(limb_parts, np.int32)
+    n_parts, max_peaks = peaks.shape[0], peaks.shape[1]
+    people = np.full((max_people, n_parts), -1, np.int32)
+    score = np.zeros((max_people, 2), np.float32)
+    n = ctypes.c_int(0)
+    _lib.check(L.avec_assemble_people(counts.ctypes.data, peaks.ctypes.data, n_parts, max_peaks, cand.ctypes.data,
+                                      limb_parts.ctypes.data, limb_parts.shape[0], new_row_limbs, max_people,
+                                      people.ctypes.data, score.ctypes.data, ctypes.byref(n)))
+    return people[:n.value], score[:n.value]
 
 
 def synth_posenet_weights(structure: bytes) -> np.ndarray:

@@ -235,6 +235,62 @@ int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, 
   });
 }
 
+int avec_paf_candidates_device(avec_ctx* ctx, const float* d_paf, int H, int W, const int* d_counts,
+                               const float* d_peaks, int max_peaks, const int* limb_parts, const int* limb_paf,
+                               int n_limbs, float paf_threshold, float* d_cand, void* cuda_stream) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(d_paf, "d_paf");
+    need(d_counts, "d_counts");
+    need(d_peaks, "d_peaks");
+    need(limb_parts, "limb_parts");
+    need(limb_paf, "limb_paf");
+    need(d_cand, "d_cand");
+    avec::check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    avec::launch_paf_candidates(d_paf, H, W, d_counts, d_peaks, max_peaks, limb_parts, limb_paf, n_limbs,
+                                paf_threshold, d_cand, st);
+    avec::check_cuda(cudaStreamSynchronize(st), "paf candidates sync");
+  });
+}
+
+int avec_assemble_people(const int* counts, const float* peaks, int n_parts, int max_peaks, const float* cand,
+                         const int* limb_parts, int n_limbs, int new_row_limbs, int max_people, int* people,
+                         float* people_score, int* n_people) {
+  return guarded([&] {
+    need(counts, "counts");
+    need(peaks, "peaks");
+    need(cand, "cand");
+    need(limb_parts, "limb_parts");
+    need(people, "people");
+    need(people_score, "people_score");
+    need(n_people, "n_people");
+    *n_people = avec::assemble_people(counts, peaks, n_parts, max_peaks, cand, limb_parts, n_limbs, new_row_limbs,
+                                      max_people, people, people_score);
+  });
+}
+
+int avec_coco_limbs(int* limb_parts, int* limb_paf, int* n_limbs, int* new_row_limbs) {
+  return guarded([&] {
+    need(n_limbs, "n_limbs");
+    // OpenPose COCO limb sequence (1-based parts) and the PAF channel pairs of
+    // its 57-channel output, re-based to parts 0..17 and the 38 PAF planes
+    static const int seq[19][2] = {{2, 3},   {2, 6},   {3, 4},  {4, 5},   {6, 7},   {7, 8},  {2, 9},
+                                   {9, 10},  {10, 11}, {2, 12}, {12, 13}, {13, 14}, {2, 1},  {1, 15},
+                                   {15, 17}, {1, 16},  {16, 18}, {3, 17}, {6, 18}};
+    static const int map[19][2] = {{31, 32}, {39, 40}, {33, 34}, {35, 36}, {41, 42}, {43, 44}, {19, 20},
+                                   {21, 22}, {23, 24}, {25, 26}, {27, 28}, {29, 30}, {47, 48}, {49, 50},
+                                   {53, 54}, {51, 52}, {55, 56}, {37, 38}, {45, 46}};
+    *n_limbs = 19;
+    if (new_row_limbs) *new_row_limbs = 17;
+    for (int l = 0; l < 19; ++l)
+      for (int k = 0; k < 2; ++k) {
+        if (limb_parts) limb_parts[2 * l + k] = seq[l][k] - 1;
+        if (limb_paf) limb_paf[2 * l + k] = map[l][k] - 19;
+      }
+  });
+}
+
 int avec_posenet_layer_fusion(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                               int layer, int* kind, int* in_layer) {
   return guarded([&] {

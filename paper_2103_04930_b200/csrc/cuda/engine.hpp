@@ -33,6 +33,16 @@ bool pdl_enabled();
 void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K,
                           cudaStream_t stream);
 
+// PAF candidate scores [n_limbs][max_peaks][max_peaks][2] = (score, valid)
+// for the peaks of avec_nms_device (paf.cu), and the host person assembly
+// over them (people.cpp); returns the number of people written
+void launch_paf_candidates(const float* d_paf, int H, int W, const int* d_counts, const float* d_peaks, int max_peaks,
+                           const int* limb_parts, const int* limb_paf, int n_limbs, float thr, float* d_cand,
+                           cudaStream_t stream);
+int assemble_people(const int* counts, const float* peaks, int n_parts, int max_peaks, const float* cand,
+                    const int* limb_parts, int n_limbs, int new_row_limbs, int max_people, int* people,
+                    float* people_score);
+
 // 2x2/2 max pool, padded-flat NHWC bf16 -> padded-flat NHWC bf16
 void launch_maxpool2(const void* d_in, int n, int H, int W, int P_in, int C, void* d_out,
                      int P_out, cudaStream_t stream);

@@ -42,6 +42,9 @@ def lib():
         L.oracle_upsample_plane.argtypes = [f32p, i, i, i, f32p]
         L.oracle_nms_plane.argtypes = [f32p, i, i, ctypes.c_float, i, i32p, f32p, f32p]
         L.oracle_nms_plane.restype = i
+        L.oracle_paf_candidates.argtypes = [f32p, i, i, i32p, f32p, i, i32p, i32p, i, ctypes.c_float, f32p]
+        L.oracle_assemble_people.argtypes = [i32p, f32p, i, i, f32p, i32p, i, i, i, i32p, f32p]
+        L.oracle_assemble_people.restype = i
         _LIB = L
     return _LIB
 
@@ -181,3 +184,29 @@ def coco_chain(frames_nchw: np.ndarray, layers, wb) -> np.ndarray:
         l1, l2 = a, b_
         idx += 14
     return np.concatenate([l2, l1], axis=3).transpose(0, 3, 1, 2).ravel()
+
+
+def paf_candidates(paf, counts, peaks, limb_parts, limb_paf, thr):
+    """Oracle candidate scores [n_limbs][max_peaks][max_peaks][2] (oracle/paf_oracle.c)."""
+    paf = np.ascontiguousarray(paf, np.float32)
+    counts = np.ascontiguousarray(counts, np.int32)
+    peaks = np.ascontiguousarray(peaks, np.float32)
+    lp = np.ascontiguousarray(limb_parts, np.int32)
+    lf = np.ascontiguousarray(limb_paf, np.int32)
+    max_peaks = peaks.shape[1]
+    cand = np.zeros((lp.shape[0], max_peaks, max_peaks, 2), np.float32)
+    lib().oracle_paf_candidates(paf, paf.shape[1], paf.shape[2], counts, peaks, max_peaks, lp, lf, lp.shape[0],
+                                thr, cand)
+    return cand
+
+
+def assemble_people(counts, peaks, cand, limb_parts, new_row_limbs, max_people=64):
+    counts = np.ascontiguousarray(counts, np.int32)
+    peaks = np.ascontiguousarray(peaks, np.float32)
+    cand = np.ascontiguousarray(cand, np.float32)
+    lp = np.ascontiguousarray(limb_parts, np.int32)
+    people = np.full((max_people, peaks.shape[0]), -1, np.int32)
+    score = np.zeros((max_people, 2), np.float32)
+    n = lib().oracle_assemble_people(counts, peaks, peaks.shape[0], peaks.shape[1], cand, lp, lp.shape[0],
+                                     new_row_limbs, max_people, people, score)
+    return people[:n], score[:n]
