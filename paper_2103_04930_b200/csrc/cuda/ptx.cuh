@@ -182,9 +182,13 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
-// arrive on an mbarrier given by its shared::cluster address (possibly remote)
+// arrive on an mbarrier given by its shared::cluster address (possibly remote).
+// Default semantics (release at CTA scope), as CUTLASS's ClusterBarrier: the
+// arrivals we send only publish completed tcgen05.ld reads (the caller fences
+// with tcgen05.fence::before_thread_sync); a cluster-scope release added a
+// MEMBAR + ERRBAR per tile that was the pair kernels' top stall site.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load into this CTA's smem, completing bytes on an mbarrier that may live
 // in the peer CTA of the pair (the leader's full barrier)
