@@ -853,9 +853,11 @@ Plan* get_plan(avec_ctx* ctx, Slot* slot, const Model& m, int n_img, int H, int 
     return size_t(v > 0 ? v : 1);
   }();
   if (slot->plans.size() >= max_plans) {
-    // the slot is leased to this caller; its last work may still be in flight
+    // the slot is leased to this caller, but its previous forward may still
+    // run on the slot stream or on a caller stream (marked by `done`, whose
+    // pending flag the lease may already have cleared)
     check_cuda(cudaStreamSynchronize(slot->stream), "plan eviction sync");
-    if (slot->pending) check_cuda(cudaEventSynchronize(slot->done), "plan eviction sync");
+    check_cuda(cudaEventSynchronize(slot->done), "plan eviction sync");
     auto lru = slot->plans.begin();
     for (auto p = slot->plans.begin(); p != slot->plans.end(); ++p)
       if (p->second->last_use < lru->second->last_use) lru = p;
