@@ -64,11 +64,14 @@ oracle: $(LIB)/libavec_cuda.so
 	$(MAKE) -C oracle oracle
 	@if [ -d /root/reference/proj ]; then $(MAKE) -C oracle ref; else echo "no /root/reference: using prebuilt oracle/_ref"; fi
 
-probe: build/tc_probe build/tc2_probe
+probe: build/tc_probe build/tc2_probe build/tma3d_probe
 build/tc_probe: tests/native/tc_probe.cu $(CUDA_DIR)/ptx.cuh
 	@mkdir -p build
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -o $@ $<
 build/tc2_probe: tests/native/tc2_probe.cu $(CUDA_DIR)/ptx.cuh
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -o $@ $<
+build/tma3d_probe: tests/native/tma3d_probe.cu $(CUDA_DIR)/ptx.cuh
 	@mkdir -p build
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -o $@ $<
 

@@ -333,7 +333,7 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     dom_fl = sum(p["flops"] for p in dom) / max(len(dom), 1)   # per launch
     dom_ms = sum(p["ms"] for p in dom) / max(len(dom), 1)      # mean launch duration
     dom_tf = dom_fl / (dom_ms / 1e3) / 1e12
-    allc = [p for p in prof if p["kind"] in ("conv_tc", "conv_pm", "conv_first", "conv_head")]  # every conv launch
+    allc = [p for p in prof if p["kind"] in ("conv_tc", "conv_pm", "conv_first", "conv_head", "conv12")]  # every conv launch
     all_fl, all_ms = sum(p["flops"] for p in allc), sum(p["ms"] for p in allc)
     traffic = None
     tp = ROOT / "profiles" / "conv_traffic.json"

@@ -138,7 +138,8 @@ int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c
 /* Profiling hook (bench.py roofline): replays the plan of this shape op by op
  * with CUDA events on the slot stream, `reps` times, after one warm graph run.
  * Per op i < *n_ops: kind (0 = fused first layer, 1 = pixel-major tcgen05 conv,
- * 2 = max-pool, 3 = swap-AB tcgen05 conv, 4 = fused Mconv6+Mconv7 head), algorithmic FLOPs and bytes of the
+ * 2 = max-pool, 3 = swap-AB tcgen05 conv, 4 = fused Mconv6+Mconv7 head, 5 = fused conv1_1+conv1_2+pool1),
+ * algorithmic FLOPs and bytes of the
  * launch, mean duration (ms). */
 int avec_posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                          uint32_t w, const float* d_in, int reps, int max_ops, int* n_ops,

@@ -237,7 +237,7 @@ class B200Backend:
             self._ctx, handle.id, dims.batch, dims.channels, dims.height, dims.width, d_in, reps, cap,
             ctypes.byref(n), kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), flops.ctypes.data,
             nbytes.ctypes.data, ms.ctypes.data))
-        names = {0: "conv_first", 1: "conv_pm", 2: "maxpool", 3: "conv_tc", 4: "conv_head"}
+        names = {0: "conv_first", 1: "conv_pm", 2: "maxpool", 3: "conv_tc", 4: "conv_head", 5: "conv12"}
         return [dict(kind=names[int(kind[i])], flops=float(flops[i]), bytes=float(nbytes[i]),
                      ms=float(ms[i])) for i in range(n.value)]
 

@@ -1,0 +1,398 @@
+// conv1_1 + conv1_2 + pool1 in one tcgen05 kernel (sm_100a): the 64-channel
+// full-resolution conv1_1 activation never reaches HBM.
+//
+// Tile = output rows y0, y0+1 (y0 even) at columns x0 .. x0+125 (x0 = 126 cb):
+// conv1_2 needs conv1_1 at rows y0-1 .. y0+2 and padded columns x0 .. x0+127,
+// i.e. four 128-position windows — exactly one M = 128 MMA each.
+//   producer  TMA of the fp32 frame patch [3 ch][rows y0-2..y0+3][132 cols from
+//             (x0-2) & ~3] (zero-filled outside the frame; a TMA inner
+//             coordinate must be 16-byte aligned — an unaligned one is an
+//             illegal instruction, tests/native/tma3d_probe.cu), conv1_1 weights once, conv1_2
+//             weights per tap (9 x 64x64 per tile, from L2)
+//   epilogue  A: im2col of the 27 taps per window position (x - 0.5, 0 outside
+//                the frame) into a K = 32 SW64 im2col buffer
+//   MMA       conv1_1: 4 windows x 2 MMAs (M128 N64 K16) -> acc1[4] in TMEM
+//   epilogue  B: acc1 -> bias, ReLU, 0 outside the image, bf16 -> overwrites
+//                the window (it is now conv1_2's A operand, SW128 K-major)
+//   MMA       conv1_2: 9 taps x 4 K16 x 2 rows (sub-tile 0 reads window r,
+//             sub-tile 1 window r+1, shifted by s rows) -> acc2[stage]
+//   epilogue  C: 2x2 max of the raw sums, bias, ReLU, bf16 -> pooled row
+//             y0/2, columns x0/2 .. x0/2+62 through a 4D TMA map (the 127th/
+//             128th positions read past their window and are never stored)
+// Windows are double-buffered and the MMA warp issues conv1_1(t+1) before
+// conv1_2(t), so the im2col of tile t+2, the conv1_1 epilogue of tile t+1 and
+// the pooled epilogue of tile t-1 all overlap conv1_2 of tile t. Bit-identical to the
+// separate conv_first + pooled conv1_2 path (same bf16 operands, K order and
+// MMA shapes).
+#include <cuda_bf16.h>
+
+#include "conv_tc.cuh"
+#include "engine.hpp"
+#include "ptx.cuh"
+
+namespace avec {
+
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 320;  // producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant)
+constexpr int kEpi = 256;
+constexpr uint32_t kTmemCols = 512;
+constexpr int kTileCols = 126;  // output columns per tile (even: whole pooled columns)
+constexpr int kPatchCols = 132;
+constexpr int kPatchRows = 6;
+constexpr int kPatchBytes = 3 * kPatchRows * kPatchCols * 4;  // 9504
+constexpr int kW12Stages = 3;
+constexpr int kAcc2Col = 256;  // acc2[2 stages] at 256..383, 384..511 (2 rows x 64 each)
+
+struct Smem12 {
+  static constexpr int win = 0;                          // 2 buffers x 4 windows x [128][64] bf16 SW128
+  static constexpr int imc = win + 2 * 4 * 16384;        // 4 windows x [128][32] bf16 SW64 (im2col)
+  static constexpr int w12 = imc + 4 * 8192;             // kW12Stages x [64 cout][64 K]
+  static constexpr int w11 = w12 + kW12Stages * 8192;    // [64 cout][64 K] (K 27 used)
+  static constexpr int patch = w11 + 8192;               // 2 x [3][6][132] fp32
+  static constexpr int stg = patch + 2 * 9728;           // 4 warps x [16 px][64 ch] (pooled box)
+  static constexpr int bias = stg + 4 * 2048;            // b11, b12 (64 each)
+  static constexpr int bars = bias + 2 * 64 * 4;
+  static constexpr int total = bars + 256;
+  static_assert(total + 1024 <= 232448, "smem budget");
+};
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void tile_of(const ConvParams& p, int t, int& n, int& y0, int& x0) {
+  n = t / p.tiles_per_image;
+  const int rem = t - n * p.tiles_per_image;
+  const int rp = rem / p.col_blocks;
+  y0 = 2 * rp;
+  x0 = (rem - rp * p.col_blocks) * kTileCols;
+}
+
+// maps.act_big[0]: fp32 frames [N*3][H][W], box {132, 6, 3}; maps.wgt[0]:
+// conv1_2 weights, maps.wgt[1]: conv1_1 weights (box {64, 64}); maps.out_pool[0]
+// / [1]: pooled 4D stores with 16 / 15-column boxes. p.g[0] = conv1_2, p.g[1] = conv1_1.
+__global__ void __launch_bounds__(kThreads, 1)
+    conv12_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_align1024(smem_raw);
+  uint8_t* win = smem + Smem12::win;
+  uint8_t* imc = smem + Smem12::imc;
+  uint8_t* w12 = smem + Smem12::w12;
+  uint8_t* w11 = smem + Smem12::w11;
+  float* patch = reinterpret_cast<float*>(smem + Smem12::patch);
+  uint8_t* stg = smem + Smem12::stg;
+  float* b11 = reinterpret_cast<float*>(smem + Smem12::bias);
+  float* b12 = b11 + 64;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem12::bars);
+  uint64_t* patch_full = bars;             // [2]
+  uint64_t* patch_empty = patch_full + 2;  // [2] 128 arrivals
+  uint64_t* w11_full = patch_empty + 2;
+  uint64_t* w12_full = w11_full + 1;       // [kW12Stages]
+  uint64_t* w12_empty = w12_full + kW12Stages;
+  uint64_t* imc_full = w12_empty + kW12Stages;  // 128 arrivals: im2col written
+  uint64_t* a1_full = imc_full + 1;             // conv1_1 MMAs done (acc1 ready, im2col free)
+  uint64_t* win_full = a1_full + 1;             // [2] 128 arrivals: conv1_1 output written, acc1 drained
+  uint64_t* win_empty = win_full + 2;           // [2] conv1_2 MMAs done with the windows
+  uint64_t* acc2_full = win_empty + 2;          // [2]
+  uint64_t* acc2_empty = acc2_full + 2;         // [2] 128 arrivals
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc2_empty + 2);
+
+  const uint32_t warp = warp_id();
+  if (warp == 0 && elect_one()) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&patch_full[i], 1);
+      mbar_init(&patch_empty[i], kEpi);
+      mbar_init(&win_full[i], kEpi);
+      mbar_init(&win_empty[i], 1);
+      mbar_init(&acc2_full[i], 1);
+      mbar_init(&acc2_empty[i], kEpi);
+    }
+    mbar_init(w11_full, 1);
+    mbar_init(imc_full, kEpi);
+    mbar_init(a1_full, 1);
+    for (int i = 0; i < kW12Stages; ++i) {
+      mbar_init(&w12_full[i], 1);
+      mbar_init(&w12_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      const uint64_t keep = policy_evict_last();
+      mbar_arrive_expect_tx(w11_full, 8192);
+      tma_load_2d(w11, &maps.wgt[1], w11_full, 0, 0);
+      int ws = 0;
+      uint32_t wph = 0;
+      // the frame patch runs one tile ahead of the weights (the im2col of
+      // tile t+1 precedes conv1_2 of tile t)
+      auto load_patch = [&](int t, int it) {
+        int n, y0, x0;
+        tile_of(p, t, n, y0, x0);
+        const int pb = it & 1;
+        mbar_wait(&patch_empty[pb], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&patch_full[pb], kPatchBytes);
+        tma_load_3d(patch + pb * (9728 / 4), &maps.act_big[0], &patch_full[pb], (x0 - 2) & ~3, y0 - 2, n * 3);
+      };
+      if (int(blockIdx.x) < p.total_tiles) load_patch(blockIdx.x, 0);
+      int it = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+        if (t + int(gridDim.x) < p.total_tiles) load_patch(t + gridDim.x, it + 1);
+        for (int tap = 0; tap < 9; ++tap) {
+          mbar_wait(&w12_empty[ws], wph ^ 1);
+          mbar_arrive_expect_tx(&w12_full[ws], 8192);
+          tma_load_2d_hint(w12 + ws * 8192, &maps.wgt[0], &w12_full[ws], tap * 64, 0, keep);
+          if (++ws == kW12Stages) { ws = 0; wph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // order per tile t: conv1_1(t+1) (once act11(t) drained acc1 and the
+    // im2col of t+1 is written), then conv1_2(t) — the tensor pipe runs them
+    // in issue order, so act11(t+1) overlaps conv1_2(t)
+    if (elect_one()) {
+      const uint32_t idesc = idesc_bf16_f32(128, 64);
+      const uint32_t win_base = smem_u32(win), imc_base = smem_u32(imc);
+      const uint32_t w12_base = smem_u32(w12), w11_base = smem_u32(w11);
+      auto conv11 = [&](uint32_t ph) {
+        mbar_wait(imc_full, ph);
+        tc_fence_after();
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)  // K = 32 covers the 27 taps
+            mma_bf16_ss(tmem + j * 64, desc_sw64(imc_base + j * 8192 + kk * 32), desc_sw128(w11_base + kk * 32),
+                        idesc, kk ? 1u : 0u);
+        mma_commit(a1_full);
+      };
+      int ws = 0;
+      uint32_t wph = 0;
+      mbar_wait(w11_full, 0);
+      if (int(blockIdx.x) < p.total_tiles) conv11(0);
+      int it = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+        const int b = it & 1;  // window buffer, also the acc2 stage
+        const uint32_t bph = (it >> 1) & 1;
+        const uint32_t wb = win_base + b * 4 * 16384;
+        mbar_wait(&win_full[b], bph);
+        if (t + int(gridDim.x) < p.total_tiles) conv11((it + 1) & 1);
+        mbar_wait(&acc2_empty[b], bph ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + kAcc2Col + b * 128;
+        for (int r = 0; r < 3; ++r)
+          for (int s = 0; s < 3; ++s) {
+            mbar_wait(&w12_full[ws], wph);
+            tc_fence_after();
+            const uint32_t bb = w12_base + ws * 8192;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t bd = desc_sw128(bb + kk * 32);
+              const uint32_t accum = (r == 0 && s == 0 && kk == 0) ? 0u : 1u;
+              mma_bf16_ss(d0, desc_sw128(wb + r * 16384 + s * 128 + kk * 32), bd, idesc, accum);
+              mma_bf16_ss(d0 + 64, desc_sw128(wb + (r + 1) * 16384 + s * 128 + kk * 32), bd, idesc, accum);
+            }
+            mma_commit(&w12_empty[ws]);
+            if (++ws == kW12Stages) { ws = 0; wph ^= 1; }
+          }
+        mma_commit(&win_empty[b]);
+        mma_commit(&acc2_full[b]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue group
+    // warps 2..9: quad = TMEM lane quadrant (warp % 4), sub = which half of
+    // the windows (im2col, conv1_1 epilogue) or channels (pooled) it handles
+    const uint32_t quad = warp & 3;
+    const int sub = (int(warp) - 2) >> 2;
+    const uint32_t lane = lane_id();
+    const int px = int(quad) * 32 + int(lane);  // window position / TMEM lane of this thread
+    const int ep = int(threadIdx.x) - 64;
+    const uint32_t lane_base = (quad * 32) << 16;
+    if (ep < 64) {
+      const ConvGroupParams& g2 = p.g[0];
+      const ConvGroupParams& g1 = p.g[1];
+      b12[ep] = g2.bias[ep];
+      b11[ep] = g1.bias[ep];
+    }
+    named_bar_sync(1, kEpi);
+    // A: im2col of tile (t, it) into the SW64 im2col buffer (free once conv1_1
+    // of the previous tile completed)
+    auto im2col = [&](int t, int it) {
+      int n, y0, x0;
+      tile_of(p, t, n, y0, x0);
+      const int b = it & 1;
+      mbar_wait(&patch_full[b], (it >> 1) & 1);
+      const float* pp = patch + b * (9728 / 4);
+      const int C = x0 + px - 1;  // image column of this window position
+      // the patch starts at column (x0 - 2) & ~3: TMA needs 16-byte aligned inner coordinates
+      const float* ppx = pp + px + ((x0 - 2) & 3);
+      uint8_t* wrow = imc + px * 64;
+#pragma unroll
+      for (int jw = 0; jw < 2; ++jw) {
+        const int j = 2 * sub + jw;
+        const int R = y0 - 1 + j;  // conv1_1 output row of window j
+        float xs[32];
+#pragma unroll
+        for (int i = 27; i < 32; ++i) xs[i] = 0.f;
+#pragma unroll
+        for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            const int yy = R + r - 1;
+            const bool rv = yy >= 0 && yy < p.H;
+#pragma unroll
+            for (int sx = 0; sx < 3; ++sx) {
+              const int xx = C + sx - 1;
+              const bool v = rv && xx >= 0 && xx < p.W;
+              // patch row j + r = image row y0 - 2 + j + r; image col x0 - 2 + px + sx
+              xs[ci * 9 + r * 3 + sx] = v ? ppx[(ci * kPatchRows + j + r) * kPatchCols + sx] - 0.5f : 0.f;
+            }
+          }
+        uint32_t packed[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) packed[i] = pack2(xs[2 * i], xs[2 * i + 1]);
+        uint8_t* row = wrow + j * 8192;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(row + ((q ^ ((px >> 1) & 3)) << 4)) =
+              make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&patch_empty[b]);
+      mbar_arrive(imc_full);
+    };
+    // B: conv1_1 accumulators -> bias, ReLU, zero outside the image, bf16 ->
+    // the tile's window buffer (conv1_2's A operand, SW128 K-major)
+    auto act11 = [&](int t, int it) {
+      int n, y0, x0;
+      tile_of(p, t, n, y0, x0);
+      const int b = it & 1;
+      mbar_wait(&win_empty[b], ((it >> 1) & 1) ^ 1);  // conv1_2 two tiles back is done with the buffer
+      const int C = x0 + px - 1;
+      uint8_t* wrow = win + b * 4 * 16384 + px * 128;
+#pragma unroll
+      for (int jw = 0; jw < 2; ++jw) {
+        const int j = 2 * sub + jw;
+        const int R = y0 - 1 + j;
+        const bool valid = R >= 0 && R < p.H && C >= 0 && C < p.W;
+        uint32_t va[32], vb[32];
+        tmem_ld32(tmem + lane_base + j * 64, va);
+        tmem_ld32(tmem + lane_base + j * 64 + 32, vb);
+        tmem_ld_wait();
+        uint8_t* row = wrow + j * 16384;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t w[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int c = q * 8 + 2 * jj;
+            const float a = fmaxf(__uint_as_float(q < 4 ? va[c & 31] : vb[c & 31]) + b11[c], 0.f);
+            const float bb = fmaxf(__uint_as_float(q < 4 ? va[(c + 1) & 31] : vb[(c + 1) & 31]) + b11[c + 1], 0.f);
+            w[jj] = valid ? pack2(a, bb) : 0u;
+          }
+          *reinterpret_cast<uint4*>(row + ((q ^ (px & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&win_full[b]);
+    };
+    // C: pooled conv1_2 epilogue of tile (t, it)
+    auto pooled = [&](int t, int it) {
+      int n, y0, x0;
+      tile_of(p, t, n, y0, x0);
+      const int b = it & 1;
+      const uint32_t bph = (it >> 1) & 1;
+      mbar_wait(&acc2_full[b], bph);
+      tc_fence_after();
+      const bool pvalid = px < kTileCols && x0 + px < p.W;
+      const uint32_t tb0 = tmem + lane_base + kAcc2Col + b * 128;
+      uint8_t* buf = stg + quad * 2048;
+      if (sub == 0 && lane == 0) bulk_wait_read<0>();
+      named_bar_sync(2 + quad, 64);  // the quad's previous store has read the staging box
+      {
+        const int hlf = sub;
+        uint32_t va[32], vb[32];
+        tmem_ld32(tb0 + 32 * hlf, va);
+        tmem_ld32(tb0 + 64 + 32 * hlf, vb);
+        tmem_ld_wait();
+        uint32_t w[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          float m0 = fmaxf(__uint_as_float(va[j]), __uint_as_float(vb[j]));
+          float m1 = fmaxf(__uint_as_float(va[j + 1]), __uint_as_float(vb[j + 1]));
+          m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+          m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+          const int c = 32 * hlf + j;
+          const float a = fmaxf(m0 + b12[c], 0.f), bb = fmaxf(m1 + b12[c + 1], 0.f);
+          w[j / 2] = pvalid ? pack2(a, bb) : 0u;
+        }
+        if ((lane & 1) == 0) {
+          const uint32_t row = lane >> 1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t qq = 4 * hlf + q;
+            *reinterpret_cast<uint4*>(buf + row * 128 + ((qq ^ (row & 7)) << 4)) =
+                make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc2_empty[b]);
+      fence_proxy_async_smem();
+      named_bar_sync(2 + quad, 64);
+      if (sub == 0 && lane == 0) {
+        // warp 3's 16th pooled column is the next tile's first: 15-column box
+        tma_store_4d(quad == 3 ? &maps.out_pool[1] : &maps.out_pool[0], buf, p.g[0].out_c_off,
+                     x0 / 2 + int(quad) * 16 + p.pool_P, y0 / 2 + p.pool_P, n);
+        bulk_commit();
+      }
+    };
+    const int g0 = blockIdx.x, gs = gridDim.x;
+    if (g0 < p.total_tiles) im2col(g0, 0);
+    int it = 0;
+    for (int t = g0; t < p.total_tiles; t += gs, ++it) {
+      mbar_wait(a1_full, it & 1);  // conv1_1(t) done: acc1 holds it, the im2col buffer is free
+      tc_fence_after();
+      if (t + gs < p.total_tiles) im2col(t + gs, it + 1);
+      act11(t, it);
+      if (it > 0) pooled(t - gs, it - 1);
+    }
+    if (it > 0) pooled(g0 + (it - 1) * gs, it - 1);
+    if (sub == 0 && lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+}  // namespace
+
+void conv12_configure() {
+  check_cuda(cudaFuncSetAttribute(conv12_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem12::total + 1024),
+             "conv12 smem attribute");
+}
+
+int conv12_tile_cols() { return kTileCols; }
+
+void launch_conv12(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
+  const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
+  conv12_kernel<<<grid, kThreads, Smem12::total + 1024, stream>>>(maps, p);
+  check_cuda(cudaGetLastError(), "conv12 launch");
+}
+
+}  // namespace avec

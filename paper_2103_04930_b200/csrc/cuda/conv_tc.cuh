@@ -155,6 +155,10 @@ void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cud
 // -> 3x3x3 taps built in smem -> tcgen05 -> 64-channel padded-flat NHWC output
 void conv_first_configure();
 void conv_head_configure();
+// conv1_1 + conv1_2 + pool1 (conv12.cu)
+void conv12_configure();
+int conv12_tile_cols();
+void launch_conv12(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
 void launch_conv_head(const HeadMaps& maps, const HeadParams& p, int sm_count, cudaStream_t stream);
 void launch_conv_first(const ConvMaps& maps, const ConvParams& p, const float* frames, int sm_count,
                        cudaStream_t stream);

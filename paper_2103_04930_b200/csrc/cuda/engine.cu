@@ -140,6 +140,20 @@ CUtensorMap make_map_4d_store(const void* base, uint64_t C, uint64_t Wp, uint64_
   return m;
 }
 
+// fp32 frames [N*3][H][W] (the wire layout), box {132 columns, 6 rows, 3 channels}
+CUtensorMap make_map_frames(const void* base, uint64_t W, uint64_t H, uint64_t planes) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {W, H, planes};
+  cuuint64_t strides[2] = {W * 4, H * W * 4};
+  cuuint32_t box[3] = {132, 6, 3};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled (frames) failed: " + std::to_string(int(r)));
+  return m;
+}
+
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 // ------------------------------------------------------------------ slots
@@ -406,6 +420,68 @@ struct PlanBuilder {
     in.c = 3;
     record_io(layer, in, out);  // parity hook shows the layer its real 3-channel input
     plan.ops.push_back(op);
+  }
+
+  // conv1_1 + conv1_2 + pool1 as one kernel (conv12.cu) writing the pooled
+  // level-1 buffer; false when the shapes do not allow it (AVEC_CONV12=0 disables)
+  bool conv12(int l1, int l2, int pooled) {
+    static const bool on = [] {
+      const char* e = std::getenv("AVEC_CONV12");
+      return !(e && e[0] == '0');
+    }();
+    const ConvLayerDev& A = net.layers[l1];
+    const ConvLayerDev& B = net.layers[l2];
+    const Geometry& g0 = plan.geo[0];
+    if (!on || A.def.cin != 3 || A.def.k != 3 || A.def.cout != 64 || A.def.act != kActRelu || B.exec_k != 3 ||
+        B.def.cin != 64 || B.def.cout != 64 || B.def.act != kActRelu || g0.H % 2 || g0.W % 4 ||
+        plan.buf_c[pooled] != 64)
+      return false;
+    PlanOp op;
+    op.kind = PlanOp::kConv12;
+    op.layers[0] = l2;
+    op.head_l6[0] = l1;
+    ConvParams& p = op.cp;
+    p.k = 3;
+    p.n_images = plan.n;
+    p.H = g0.H;
+    p.W = g0.W;
+    p.Hp = g0.Hp();
+    p.Wp = g0.Wp();
+    p.P = g0.P;
+    p.n_groups = 1;
+    p.pool = 1;
+    p.pool_P = plan.geo[1].P;
+    p.col_blocks = (p.W + conv12_tile_cols() - 1) / conv12_tile_cols();
+    p.tiles_per_image = p.H / 2 * p.col_blocks;
+    p.total_tiles = p.n_images * p.tiles_per_image;
+    ConvGroupParams& g2 = p.g[0];
+    g2.bias = B.bias;
+    g2.slope = B.slope;
+    g2.act = B.def.act;
+    g2.cout = 64;
+    g2.out = plan.bufs[pooled]->p;
+    g2.out_c_off = 0;
+    g2.out_c_stride = 64;
+    ConvGroupParams& g1 = p.g[1];
+    g1.bias = A.bias;
+    g1.slope = A.slope;
+    g1.act = A.def.act;
+    g1.cout = 64;
+    op.maps.act_big[0] = make_map_frames(plan.in.p, uint64_t(p.W), uint64_t(p.H), uint64_t(plan.n) * 3);
+    op.maps.wgt[0] = make_map_2d(B.w, 9 * 64, B.cout_pad, 64);
+    op.maps.wgt[1] = make_map_2d(A.w, 64, A.cout_pad, 64);
+    const Geometry& g1g = plan.geo[1];
+    op.maps.out_pool[0] = make_map_4d_store(plan.bufs[pooled]->p, 64, g1g.Wp(), g1g.Hp(), plan.n, 16);
+    op.maps.out_pool[1] = make_map_4d_store(plan.bufs[pooled]->p, 64, g1g.Wp(), g1g.Hp(), plan.n, 15);
+    TensorView in;
+    in.buf = -2;
+    in.c = 3;
+    record_io(l2, in, view(pooled, 0, 64));  // conv1_2's parity view: the frame in, pooled out
+    plan.layer_fusion[l1] = 2;
+    plan.layer_fusion[l2] = 3;
+    plan.layer_in_from[l2] = l1;
+    plan.ops.push_back(op);
+    return true;
   }
 
   // A 3x3 ReLU conv writing all of a 64/128-channel buffer that only a 2x2
@@ -706,10 +782,14 @@ struct PlanBuilder {
 int build_trunk(PlanBuilder& b, Plan& plan, int cat, int trunk_off) {
   int li = 0;
   // level 0
-  const int a0 = b.buffer(0, 64);
-  b.first(li++, b.view(a0, 0, 64));  // conv1_1 fused with the frame conversion
   const int p1 = b.buffer(1, 64), a1 = b.buffer(1, 128);
-  b.conv_pool(li++, b.view(a0, 0, 64), p1);  // conv1_2 + pool1
+  if (b.conv12(0, 1, p1)) {  // conv1_1 + conv1_2 + pool1 in one kernel
+    li = 2;
+  } else {
+    const int a0 = b.buffer(0, 64);
+    b.first(li++, b.view(a0, 0, 64));          // conv1_1 fused with the frame conversion
+    b.conv_pool(li++, b.view(a0, 0, 64), p1);  // conv1_2 + pool1
+  }
   b.conv({li++}, {b.view(p1, 0, 64)}, {b.view(a1, 0, 128)});   // conv2_1
   const int p2 = b.buffer(2, 128), a2 = b.buffer(2, 256), b2 = b.buffer(2, 256);
   b.conv_pool(li++, b.view(a1, 0, 128), p2);  // conv2_2 + pool2
@@ -824,6 +904,9 @@ void run_ops(avec_ctx* ctx, const Plan& plan, const PoseNet& net, size_t first, 
       case PlanOp::kHead:
         launch_conv_head(op.hm, op.hp, ctx->sms, st);
         break;
+      case PlanOp::kConv12:
+        launch_conv12(op.maps, op.cp, ctx->sms, st);
+        break;
       case PlanOp::kConv:
         if (op.cp.pixel_major)
           launch_conv_pm(op.maps, op.cp, ctx->sms, st);
@@ -932,6 +1015,7 @@ void ctx_init(avec_ctx* ctx, int device, int slots) {
   conv_pm_configure();
   conv_first_configure();
   conv_head_configure();
+  conv12_configure();
   if (slots <= 0) slots = 2;
   for (int i = 0; i < slots; ++i) {
     auto s = std::make_unique<Slot>();
@@ -1141,6 +1225,13 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
       const Geometry& g = plan->geo[op.level];
       p.kind = 2;
       p.bytes = double(n_img) * g.H * g.W * op.C * 2 * 1.25;  // read 4, write 1 bf16 per window
+      continue;
+    }
+    if (op.kind == PlanOp::kConv12) {  // conv1_1 + conv1_2 + pool1: frame in, pooled 64 channels out
+      p.kind = 5;
+      const double px = double(n_img) * h * w;
+      p.flops = 2.0 * px * (27.0 * 64 + 576.0 * 64);
+      p.bytes = px * (12.0 + 64 * 2 / 4.0);
       continue;
     }
     if (op.kind == PlanOp::kHead) {  // Mconv6 + Mconv7: both layers' FLOPs, input + head output bytes

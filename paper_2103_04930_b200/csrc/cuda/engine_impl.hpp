@@ -73,12 +73,12 @@ struct TensorView {
 };
 
 struct PlanOp {
-  enum Kind { kFirst, kConv, kPool, kHead } kind = kConv;
+  enum Kind { kFirst, kConv, kPool, kHead, kConv12 } kind = kConv;
   ConvParams cp{};
   ConvMaps maps{};
   HeadParams hp{};  // kHead: fused Mconv6 + Mconv7 (layers[] = the Mconv7 layers)
   HeadMaps hm{};
-  int head_l6[2] = {-1, -1};
+  int head_l6[2] = {-1, -1};  // kHead: the Mconv6 layers; kConv12: conv1_1 in [0]
   int layers[2] = {-1, -1};
   int src = -1, dst = -1, level = 0, C = 0;  // pool: src/dst buffers
 };
