@@ -36,7 +36,7 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 320;  // producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant)
+constexpr int kThreads = 352;  // weights, MMA, 8 epilogue warps (2 per TMEM lane quadrant), frame patches
 constexpr int kEpi = 256;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kTileCols = 126;  // output columns per tile (even: whole pooled columns)
@@ -134,26 +134,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_2d(w11, &maps.wgt[1], w11_full, 0, 0);
       int ws = 0;
       uint32_t wph = 0;
-      // the frame patch runs one tile ahead of the weights (the im2col of
-      // tile t+1 precedes conv1_2 of tile t)
-      auto load_patch = [&](int t, int it) {
-        int n, y0, x0;
-        tile_of(p, t, n, y0, x0);
-        const int pb = it & 1;
-        mbar_wait(&patch_empty[pb], ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&patch_full[pb], kPatchBytes);
-        tma_load_3d(patch + pb * (9728 / 4), &maps.act_big[0], &patch_full[pb], (x0 - 2) & ~3, y0 - 2, n * 3);
-      };
-      if (int(blockIdx.x) < p.total_tiles) load_patch(blockIdx.x, 0);
-      int it = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
-        if (t + int(gridDim.x) < p.total_tiles) load_patch(t + gridDim.x, it + 1);
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
         for (int tap = 0; tap < 9; ++tap) {
           mbar_wait(&w12_empty[ws], wph ^ 1);
           mbar_arrive_expect_tx(&w12_full[ws], 8192);
           tma_load_2d_hint(w12 + ws * 8192, &maps.wgt[0], &w12_full[ws], tap * 64, 0, keep);
           if (++ws == kW12Stages) { ws = 0; wph ^= 1; }
         }
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ frame patches
+    // its own warp, so a patch lands as soon as its buffer frees (the im2col
+    // of tile t+1 runs before conv1_2 of tile t and must not wait on HBM)
+    if (elect_one()) {
+      int it = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+        int n, y0, x0;
+        tile_of(p, t, n, y0, x0);
+        const int pb = it & 1;
+        mbar_wait(&patch_empty[pb], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&patch_full[pb], kPatchBytes);
+        tma_load_3d(patch + pb * (9728 / 4), &maps.act_big[0], &patch_full[pb], (x0 - 2) & ~3, y0 - 2, n * 3);
       }
     }
   } else if (warp == 1) {
