@@ -59,6 +59,13 @@ struct Smem12 {
   static_assert(total + 1024 <= 232448, "smem budget");
 };
 
+// bf16x2 {relu(a), relu(b)} (a in the low half) in one cvt: rn(relu(x)) == relu(rn(x))
+__device__ __forceinline__ uint32_t pack2_relu(float a, float b) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -299,9 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
             const int c = q * 8 + 2 * jj;
-            const float a = fmaxf(__uint_as_float(q < 4 ? va[c & 31] : vb[c & 31]) + b11[c], 0.f);
-            const float bb = fmaxf(__uint_as_float(q < 4 ? va[(c + 1) & 31] : vb[(c + 1) & 31]) + b11[c + 1], 0.f);
-            w[jj] = valid ? pack2(a, bb) : 0u;
+            const float2 bias = *reinterpret_cast<const float2*>(b11 + c);
+            w[jj] = valid ? pack2_relu(__uint_as_float(q < 4 ? va[c & 31] : vb[c & 31]) + bias.x,
+                                       __uint_as_float(q < 4 ? va[(c + 1) & 31] : vb[(c + 1) & 31]) + bias.y)
+                          : 0u;
           }
           *reinterpret_cast<uint4*>(row + ((q ^ (px & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
@@ -329,25 +337,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tb0 + 32 * hlf, va);
         tmem_ld32(tb0 + 64 + 32 * hlf, vb);
         tmem_ld_wait();
-        uint32_t w[16];
+        // vertical max in registers; the horizontal pair (lanes 2i, 2i+1)
+        // splits the 32 channels: the even lane finishes 0..15, the odd 16..31
+        const bool odd = lane & 1;
+        float m[16];
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          float m0 = fmaxf(__uint_as_float(va[j]), __uint_as_float(vb[j]));
-          float m1 = fmaxf(__uint_as_float(va[j + 1]), __uint_as_float(vb[j + 1]));
-          m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
-          m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
-          const int c = 32 * hlf + j;
-          const float a = fmaxf(m0 + b12[c], 0.f), bb = fmaxf(m1 + b12[c + 1], 0.f);
-          w[j / 2] = pvalid ? pack2(a, bb) : 0u;
+        for (int k = 0; k < 16; ++k) {
+          const float lo = fmaxf(__uint_as_float(va[k]), __uint_as_float(vb[k]));
+          const float hi = fmaxf(__uint_as_float(va[16 + k]), __uint_as_float(vb[16 + k]));
+          const float other = __shfl_xor_sync(0xffffffffu, odd ? lo : hi, 1);
+          m[k] = fmaxf(odd ? hi : lo, other);
         }
-        if ((lane & 1) == 0) {
-          const uint32_t row = lane >> 1;
+        const int c0 = 32 * hlf + (odd ? 16 : 0);
+        uint32_t w[8];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t qq = 4 * hlf + q;
-            *reinterpret_cast<uint4*>(buf + row * 128 + ((qq ^ (row & 7)) << 4)) =
-                make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-          }
+        for (int k = 0; k < 8; ++k) {
+          const float2 bias = *reinterpret_cast<const float2*>(b12 + c0 + 2 * k);
+          w[k] = pvalid ? pack2_relu(m[2 * k] + bias.x, m[2 * k + 1] + bias.y) : 0u;
+        }
+        const uint32_t row = lane >> 1;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t qq = 4 * hlf + (odd ? 2 : 0) + q;
+          *reinterpret_cast<uint4*>(buf + row * 128 + ((qq ^ (row & 7)) << 4)) =
+              make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
         }
       }
       tc_fence_before();

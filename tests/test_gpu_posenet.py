@@ -263,3 +263,45 @@ def test_plan_cache_eviction_keeps_results():
         f, ref = first[(hh, ww)]
         assert be.forward(h, f).data.tobytes() == ref.tobytes()
     be.close()
+
+
+_UNFUSED_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+import oracle_lib as O
+from paper_2103_04930_b200 import B200Backend, Dims, Frame, make_model, netspec
+be = B200Backend(0, slots=1)
+h = be.register_model(make_model("openpose", netspec.spec(), b"", netspec.COCO_DIVISOR))
+w, hgt, nb = int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+f = Frame(Dims(1, 3 * nb, hgt, w), O.batched_frame(w, hgt, nb, seed=5))
+assert be.layer_fusion(h, f.dims, 0)[0] == 0, "AVEC_CONV12=0 not honoured"
+np.savez(sys.argv[2], pooled=be.layer_io(h, f, 1)[1], out=be.forward(h, f).data)
+be.close()
+"""
+
+
+def test_conv12_bit_identical_to_unfused(net, tmp_path):
+    """The fused conv1_1 + conv1_2 + pool1 kernel uses the same bf16 operands,
+    K order and MMA shapes as conv_first + the pooled conv1_2, so pool1 and the
+    whole forward are bit-identical to the unfused path (run in a subprocess
+    with AVEC_CONV12=0). Width 400 gives four 126-column tiles whose frame
+    patches start at both 16-byte alignments ((x0 - 2) & 3 = 2 and 0)."""
+    import os
+    import pathlib
+    import subprocess
+    import sys
+    from paper_2103_04930_b200 import Dims, Frame
+    be, h = net["be"], net["h"]
+    w, hgt, nb = 400, 48, 2
+    frame = Frame(Dims(1, 3 * nb, hgt, w), O.batched_frame(w, hgt, nb, seed=5))
+    assert be.layer_fusion(h, frame.dims, 0)[0] == 2 and be.layer_fusion(h, frame.dims, 1)[0] == 3
+    pooled = be.layer_io(h, frame, 1)[1]
+    out = be.forward(h, frame).data
+    root = str(pathlib.Path(__file__).resolve().parent.parent)
+    dst = tmp_path / "unfused.npz"
+    env = dict(os.environ, AVEC_CONV12="0")
+    subprocess.run([sys.executable, "-c", _UNFUSED_SCRIPT, root, str(dst), str(w), str(hgt), str(nb)],
+                   env=env, check=True, timeout=600)
+    ref = np.load(dst)
+    assert pooled.tobytes() == ref["pooled"].tobytes()
+    assert out.tobytes() == ref["out"].tobytes()

@@ -1,4 +1,4 @@
-"""tcgen05 probes (tests/native/tc_probe.cu, tc2_probe.cu): the descriptor /
+"""tcgen05 / TMA probes (tests/native/tc_probe.cu, tc2_probe.cu, tma3d_probe.cu): the descriptor /
 instruction-descriptor encodings the conv kernels rely on produce exact
 GEMMs (single CTA and CTA pair), and the measured MMA rates the kernel
 choices in DESIGN.md §3 are built on still hold."""
@@ -41,3 +41,19 @@ def test_cta_pair_probe():
     rate = {x["N"]: x["cycles_per_mma"] for x in d["rate"]}
     assert rate[256] < 128 * 1.05 and rate[128] < 64 * 1.05
     assert rate[96] < 56  # the pair lifts N = 96 off the single-CTA 56-cycle operand bound
+
+
+@pytest.mark.parametrize("c0,c1", [(0, 0), (-4, -2), (124, 5), (-4, 62)])
+def test_tma_fp32_patch_probe(c0, c1):
+    """The conv12 frame-patch load (tests/native/tma3d_probe.cu): a 3D fp32
+    TMA box {132, 6, 3} with zero fill outside the frame is exact whenever the
+    inner coordinate is a multiple of 4 floats (16 bytes), negative included.
+    (An inner coordinate that is not — e.g. -2 — faults with an illegal
+    instruction, which is why conv12 starts its patch at (x0 - 2) & ~3.)"""
+    exe = ROOT / "build" / "tma3d_probe"
+    if not exe.exists():
+        subprocess.run(["make", "-C", str(ROOT), "build/tma3d_probe"], check=True, stdout=subprocess.DEVNULL)
+    r = subprocess.run([str(exe), "200", "64", "6", "132", "6", "3", str(c0), str(c1), "3", "0"],
+                       capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert json.loads(r.stdout.strip().splitlines()[-1])["ok"]
