@@ -14,10 +14,12 @@ bash tools/wire_sweep.sh > $O/wire_sweep.txt 2>&1
 # launch list of the bench command (serialised, cold caches: compare shares)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv \
     python bench.py --steps 2 --warmup 3 > $O/ncu_launches.log 2>&1
-# full captures: 7x7 swap-AB, the CTA-pair pixel-major conv, the fused head, conv1_1
+# full captures: 7x7 swap-AB, the CTA-pair pixel-major conv, the fused head,
+# the fused conv1_1+conv1_2+pool1 (and the unfused conv1_1 it replaces)
 python tools/profile_forward.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:conv_tc -s 2 -c 1 -o $O/conv7x7 python tools/profile_forward.py > $O/ncu1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:conv_pm -s 4 -c 1 -o $O/conv_pm_pair python tools/profile_forward.py > $O/ncu2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:conv_pm -s 3 -c 1 -o $O/conv_pm_pair python tools/profile_forward.py > $O/ncu2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:conv_head -s 1 -c 1 -o $O/conv_head python tools/profile_forward.py > $O/ncu3.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:conv_first -c 1 -o $O/conv_first python tools/profile_forward.py > $O/ncu4.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:conv12 -c 1 -o $O/conv12 python tools/profile_forward.py > $O/ncu4.log 2>&1
+AVEC_CONV12=0 ncu --set full --clock-control none --import-source on -k regex:conv_first -c 1 -o $O/conv_first python tools/profile_forward.py > $O/ncu5.log 2>&1
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/smi.txt
