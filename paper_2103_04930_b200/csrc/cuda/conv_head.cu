@@ -11,8 +11,9 @@
 //         and/or the fp32 NCHW network output.
 // On BODY_25 (c6 = 512 at 1312x736 x 32 frames) this removes a 495 MB write
 // and read per stage and one launch; on COCO (c6 = 128) mostly the launch.
-// Warp roles as in conv_pm.cu: warp 0 TMA producer, warp 1 TMEM owner + MMA
-// issuer, warps 2-5 both epilogues. Persistent over (branch, image, tile).
+// Warp roles: warp 0 X/W6 TMA producer, warp 1 TMEM owner + MMA issuer,
+// warps 2-9 both epilogues (two per TMEM lane quadrant, splitting the
+// columns), warp 10 W7 TMA producer. Persistent over (branch, image, tile).
 #include <cuda_bf16.h>
 
 #include <type_traits>
@@ -27,7 +28,8 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kHThreads = 192;
+constexpr int kHThreads = 352;  // X/W6 producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant), W7 producer
+constexpr int kHEpi = 256;
 constexpr uint32_t kHTmemCols = 512;
 constexpr int kAcc2Col = 256;  // acc2 lives at TMEM columns 256..319
 constexpr int kNB = 128;        // c6 block width (MMA1 N)
@@ -40,8 +42,8 @@ struct HeadSmem {
   static constexpr int w6 = x + kXStages * 16384;      // kW6Stages x [128 rows][64]
   static constexpr int y = w6 + kW6Stages * 16384;     // 2 x [128 px][128 ch] as 2 SW128 chunks each
   static constexpr int w7 = y + 2 * 32768;             // kW7Stages x [64 rows][64]
-  static constexpr int stg = w7 + kW7Stages * 8192;    // 4 warps x [32 px][<=64 ch]
-  static constexpr int bias = stg + 4 * 4096;          // b6/s6 per Y buffer (2 x 2 x 128) + b7 (64)
+  static constexpr int stg = w7 + kW7Stages * 8192;    // 8 warps x [32 px][<=32 ch]
+  static constexpr int bias = stg + 8 * 2048;          // b6/s6 per Y buffer (2 x 2 x 128) + b7 (64)
   static constexpr int bars = bias + (4 * kNB + 64) * 4;
   static constexpr int total = bars + 256;
   static_assert(total + 1024 <= 232448, "smem budget");
@@ -100,11 +102,11 @@ __global__ void __launch_bounds__(kHThreads, 1)
     for (int i = 0; i < kW7Stages; ++i) { mbar_init(&w7_full[i], 1); mbar_init(&w7_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&a1_full[i], 1);
-      mbar_init(&y_full[i], 128);
+      mbar_init(&y_full[i], kHEpi);
       mbar_init(&y_empty[i], 1);
     }
     mbar_init(a2_full, 1);
-    mbar_init(a2_empty, 128);
+    mbar_init(a2_empty, kHEpi);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kHTmemCols>(tmem_slot);
@@ -117,8 +119,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
       const uint64_t keep = policy_evict_last();
-      int xs = 0, w6s = 0, w7s = 0;
-      uint32_t xph = 0, w6ph = 0, w7ph = 0;
+      int xs = 0, w6s = 0;
+      uint32_t xph = 0, w6ph = 0;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
         int g, n, pt;
         head_decode(p, t, g, n, pt);
@@ -134,13 +136,27 @@ __global__ void __launch_bounds__(kHThreads, 1)
             tma_load_2d_hint(sw6 + w6s * 16384, &maps.w6[g], &w6_full[w6s], c * 64, j * NB, keep);
             if (++w6s == kW6Stages) { w6s = 0; w6ph ^= 1; }
           }
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ W7 producer
+    // its own warp: W7 stages free only when MMA2 of the previous block ran,
+    // which waits on the epilogue; the X/W6 stream must not stall behind it
+    if (elect_one()) {
+      const uint64_t keep = policy_evict_last();
+      int w7s = 0;
+      uint32_t w7ph = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        int g, n, pt;
+        head_decode(p, t, g, n, pt);
+        for (int j = 0; j < p.blocks; ++j)
           for (int kc = 0; kc < kc_per_block; ++kc) {
             mbar_wait(&w7_empty[w7s], w7ph ^ 1);
             mbar_arrive_expect_tx(&w7_full[w7s], 8192);
             tma_load_2d_hint(sw7 + w7s * 8192, &maps.w7[g], &w7_full[w7s], j * NB + kc * 64, 0, keep);
             if (++w7s == kW7Stages) { w7s = 0; w7ph ^= 1; }
           }
-        }
       }
     }
   } else if (warp == 1) {
@@ -150,14 +166,14 @@ __global__ void __launch_bounds__(kHThreads, 1)
       const uint32_t idesc2 = idesc_bf16_f32(128, 64);
       int xs = 0, w6s = 0, w7s = 0;
       uint32_t xph = 0, w6ph = 0, w7ph = 0, a2eph = 0;
-      uint32_t yfph[2] = {0, 0};
+      uint32_t yfph = 0;  // phase bit per Y buffer (bit b), kept in a register
       int bc = 0;  // running block counter: Y / acc1 buffer = bc & 1
       const uint32_t x_base = smem_u32(sx), w6_base = smem_u32(sw6), y_base = smem_u32(sy),
                      w7_base = smem_u32(sw7);
       // MMA2 of one block: acc2 (+)= Y[b] * W7[:, block]^T
       auto mma2 = [&](int jb, int b, bool first_of_tile) {
-        mbar_wait(&y_full[b], yfph[b]);  // Y[b] written (and acc1[b] drained)
-        yfph[b] ^= 1;
+        mbar_wait(&y_full[b], (yfph >> b) & 1);  // Y[b] written (and acc1[b] drained)
+        yfph ^= 1u << b;
         if (first_of_tile) {  // acc2 drained by the previous tile's epilogue
           mbar_wait(a2_empty, a2eph ^ 1);
           a2eph ^= 1;
@@ -206,15 +222,16 @@ __global__ void __launch_bounds__(kHThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogues
     const uint32_t quad = warp & 3;
+    const int sub = (int(warp) - 2) >> 2;  // which half of the columns this warp converts
     const uint32_t lane = lane_id();
-    const int ep = int(threadIdx.x) - 64;  // 0..127, loader index for the bias slices
-    // warp q may only touch TMEM lanes 32q..32q+31: this thread's pixel (and
-    // its TMEM lane, and its row of Y) is 32q + lane
+    const int ep = int(threadIdx.x) - 64;  // 0..255, loader index for the bias slices
+    // warp w may only touch TMEM lanes 32(w%4)..+31: this thread's pixel (and
+    // its TMEM lane, and its row of Y) is 32 quad + lane
     const int px = int(quad) * 32 + int(lane);
     const uint32_t lane_base = (quad * 32) << 16;
-    uint8_t* stg_w = stg + quad * 4096;
+    uint8_t* stg_w = stg + (int(warp) - 2) * 2048;
     uint8_t* yrow = sy + px * 128;  // this pixel's row in every 16 KB Y chunk
-    uint32_t a1ph[2] = {0, 0}, yeph[2] = {0, 0}, a2fph = 0;
+    uint32_t a1ph = 0, yeph = 0, a2fph = 0;  // phase bit per buffer (bit b)
     int bc = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       int gi, n, pt;
@@ -230,21 +247,23 @@ __global__ void __launch_bounds__(kHThreads, 1)
         float* ss = ss6 + b * NB;
         // this block's bias / slope: every epilogue warp is done with the
         // slices' previous block (and the previous tile's b7) before they change
-        named_bar_sync(1, 128);
-        {
-          const int co = j * NB + ep;  // NB == 128 == epilogue threads
+        named_bar_sync(1, kHEpi);
+        if (ep < NB) {
+          const int co = j * NB + ep;
           bs[ep] = g.bias6[co];
           ss[ep] = g.act6 == 1 ? 0.f : g.act6 == 2 ? g.slope6[co] : 1.f;
+        } else if (j == 0 && ep < NB + 64) {
+          sb7[ep - NB] = ep - NB < g.c7 ? g.bias7[ep - NB] : 0.f;
         }
-        if (j == 0 && ep < 64) sb7[ep] = ep < g.c7 ? g.bias7[ep] : 0.f;
-        named_bar_sync(1, 128);
-        mbar_wait(&y_empty[b], yeph[b] ^ 1);  // MMA2 of this buffer's previous block released Y[b]
-        yeph[b] ^= 1;
-        mbar_wait(&a1_full[b], a1ph[b]);
-        a1ph[b] ^= 1;
+        named_bar_sync(1, kHEpi);
+        mbar_wait(&y_empty[b], ((yeph >> b) & 1) ^ 1);  // MMA2 of this buffer's previous block released Y[b]
+        yeph ^= 1u << b;
+        mbar_wait(&a1_full[b], (a1ph >> b) & 1);
+        a1ph ^= 1u << b;
         tc_fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < NB; c0 += 32) {
+        for (int cc = 0; cc < NB / 2; cc += 32) {
+          const int c0 = sub * (NB / 2) + cc;
           uint32_t v[32];
           tmem_ld32(tmem + lane_base + b * NB + c0, v);
           tmem_ld_wait();
@@ -269,46 +288,47 @@ __global__ void __launch_bounds__(kHThreads, 1)
         tc_fence_before();
         mbar_arrive(&y_full[b]);
       }
-      // ---- epilogue 2: acc2 (+ b7) -> outputs
+      // ---- epilogue 2: acc2 (+ b7) -> outputs; this warp: channels 32 sub .. 32 sub + 31
       mbar_wait(a2_full, a2fph);
       a2fph ^= 1;
       tc_fence_after();
-      uint32_t v0[32], v1[32];
-      tmem_ld32(tmem + lane_base + kAcc2Col, v0);
-      tmem_ld32(tmem + lane_base + kAcc2Col + 32, v1);
+      uint32_t v[32];
+      tmem_ld32(tmem + lane_base + kAcc2Col + sub * 32, v);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(a2_empty);
-      float zf[64];
+      const int cb = sub * 32;  // first channel of this warp
+      float zf[32];
 #pragma unroll
-      for (int c = 0; c < 64; ++c) zf[c] = __uint_as_float(c < 32 ? v0[c] : v1[c - 32]) + sb7[c];
+      for (int c = 0; c < 32; ++c) zf[c] = __uint_as_float(v[c]) + sb7[cb + c];
       if (g.out2 != nullptr && valid) {  // fp32 NCHW copy for the wire
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (c < g.c7)
-            g.out2[((static_cast<size_t>(n) * g.out2_c_stride + g.out2_c_off + c) * p.H + hh) * p.W + ww] = zf[c];
+        for (int c = 0; c < 32; ++c)
+          if (cb + c < g.c7)
+            g.out2[((static_cast<size_t>(n) * g.out2_c_stride + g.out2_c_off + cb + c) * p.H + hh) * p.W + ww] =
+                zf[c];
       }
       if (g.out_mode == kOutNchwF32) {
         if (valid) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c)
-            if (c < g.c7)
-              static_cast<float*>(g.out)[((static_cast<size_t>(n) * g.out_c_stride + g.out_c_off + c) * p.H + hh) *
-                                             p.W + ww] = zf[c];
+          for (int c = 0; c < 32; ++c)
+            if (cb + c < g.c7)
+              static_cast<float*>(g.out)[((static_cast<size_t>(n) * g.out_c_stride + g.out_c_off + cb + c) * p.H +
+                                          hh) * p.W + ww] = zf[c];
         }
         continue;
       }
       // bf16 into the stage concat: round_up(c7, 8) channels as 32/16/8-channel
       // boxes of this warp's 32 pixels (channels past c7 carry zero weights and
       // bias, so they store zeros)
-      uint32_t packed[32];
+      uint32_t packed[16];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) packed[i] = valid ? pack2(zf[2 * i], zf[2 * i + 1]) : 0u;
+      for (int i = 0; i < 16; ++i) packed[i] = valid ? pack2(zf[2 * i], zf[2 * i + 1]) : 0u;
       const int row_w = p.P * p.Wp + p.P + pt * 128 + int(quad) * 32;
       const int c_end = (g.c7 + 7) & ~7;
       auto box = [&](auto width, auto first) {
         constexpr int W = decltype(width)::value;
-        constexpr int c0 = decltype(first)::value;
+        constexpr int c0 = decltype(first)::value;  // relative to this warp's first channel
         if (lane == 0) bulk_wait_read<0>();  // this warp's previous store has read the staging box
         __syncwarp();
 #pragma unroll
@@ -327,27 +347,23 @@ __global__ void __launch_bounds__(kHThreads, 1)
         __syncwarp();
         if (lane == 0) {
           const CUtensorMap* m = W == 32 ? &maps.out32[gi] : W == 16 ? &maps.out16[gi] : &maps.out8[gi];
-          tma_store_3d(m, stg_w, g.out_c_off + c0, row_w, n);
+          tma_store_3d(m, stg_w, g.out_c_off + cb + c0, row_w, n);
           bulk_commit();
         }
       };
-      // c_end in {8, 16, ..., 64}: 32-channel boxes, then 16 and 8 tails
+      // this warp's channels: [cb, min(c_end, cb + 32)), a 32-channel box or 16/8 tails
       using I0 = std::integral_constant<int, 0>;
       using I16 = std::integral_constant<int, 16>;
-      using I32 = std::integral_constant<int, 32>;
-      using I48 = std::integral_constant<int, 48>;
       using B8 = std::integral_constant<int, 8>;
       using B16 = std::integral_constant<int, 16>;
       using B32 = std::integral_constant<int, 32>;
-      switch (c_end) {
+      switch (c_end - cb) {
         case 8: box(B8{}, I0{}); break;
         case 16: box(B16{}, I0{}); break;
         case 24: box(B16{}, I0{}); box(B8{}, I16{}); break;
-        case 32: box(B32{}, I0{}); break;
-        case 40: box(B32{}, I0{}); box(B8{}, I32{}); break;
-        case 48: box(B32{}, I0{}); box(B16{}, I32{}); break;
-        case 56: box(B32{}, I0{}); box(B16{}, I32{}); box(B8{}, I48{}); break;
-        default: box(B32{}, I0{}); box(B32{}, I32{}); break;
+        default:
+          if (c_end - cb >= 32) box(B32{}, I0{});
+          break;
       }
     }
     if (lane_id() == 0) bulk_wait<0>();

@@ -2,7 +2,8 @@
 
     python tools/ncu_waits.py <report.ncu-rep>
 
-Each `@!P BRA <retry block>` whose target begins with a TRYWAIT is charged to
+Each `@!P BRA <retry block>` whose target begins with a TRYWAIT (after an
+optional YIELD) is charged to
 that TRYWAIT's barrier operand, together with the samples of the retry block
 itself; prints the barrier operands by samples, and the share of all samples.
 """
@@ -35,6 +36,8 @@ def main():
         if "BRA 0x" in src:
             tgt = "0x" + src.split("BRA 0x", 1)[1].split()[0].rstrip(";")
             j = idx.get(tgt)
+            if j is not None and "YIELD" in rows[j][1] and j + 1 < len(rows):
+                j += 1  # retry blocks may start with a YIELD
             if j is not None and bar_of(j):
                 acc[bar_of(j)] = acc.get(bar_of(j), 0) + samples[i]
     print(f"total samples {total}")
