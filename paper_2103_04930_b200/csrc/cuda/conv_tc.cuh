@@ -131,7 +131,8 @@ struct HeadParams {
   int n_images, H, W, Hp, Wp, P;
   int in_c_off, cin_chunks;
   int nb, blocks;       // c6 = nb * blocks, nb = 128
-  int tiles_per_image, total_tiles, n_groups;
+  int tiles_per_image, total_tiles, n_groups;  // ncta == 2: tiles = pairs of 128-pixel tiles
+  int ncta;                                     // 1, or 2 for the CTA-pair kernel (conv_head2)
   HeadGroup g[kConvMaxGroups];
 };
 
@@ -155,6 +156,7 @@ void launch_conv_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cud
 // -> 3x3x3 taps built in smem -> tcgen05 -> 64-channel padded-flat NHWC output
 void conv_first_configure();
 void conv_head_configure();
+int conv_head_pair_max_chunks();  // input chunks the pair head keeps resident
 // conv1_1 + conv1_2 + pool1 (conv12.cu)
 void conv12_configure();
 int conv12_tile_cols();

@@ -565,6 +565,14 @@ struct PlanBuilder {
     p.blocks = A0.def.cout / p.nb;
     p.tiles_per_image = (p.H * p.Wp + 127) / 128;
     p.n_groups = int(l6.size());
+    // CTA pairs (conv_head2) where several c6 blocks would re-read the input
+    // and the input tile fits in smem; AVEC_HEAD2=0 disables
+    static const bool pair_on = [] {
+      const char* e = std::getenv("AVEC_HEAD2");
+      return !(e && e[0] == '0');
+    }();
+    p.ncta = pair_on && p.blocks >= 2 && p.cin_chunks <= conv_head_pair_max_chunks() ? 2 : 1;
+    if (p.ncta == 2) p.tiles_per_image = (p.tiles_per_image + 1) / 2;  // pairs of 128-pixel tiles
     p.total_tiles = p.n_groups * p.n_images * p.tiles_per_image;
     const uint64_t rows = uint64_t(plan.n) * gi.Hp() * gi.Wp();
     for (size_t g = 0; g < l6.size(); ++g) {
@@ -588,8 +596,9 @@ struct PlanBuilder {
       hg.out2_c_stride = out2.empty() ? 0 : out2[g].c_stride;
       const int ib = in[g].buf;
       op.hm.x[g] = make_map_2d(plan.bufs[ib]->p, plan.buf_c[ib], rows, 128);
-      op.hm.w6[g] = make_map_2d(A.w, A.cin_pad, A.cout_pad, 128);
-      op.hm.w7[g] = make_map_2d(B.w, B.cin_pad, B.cout_pad, 64);
+      // the pair kernel loads half a block per CTA: 64 of W6's 128 rows, 32 of W7's 64
+      op.hm.w6[g] = make_map_2d(A.w, A.cin_pad, A.cout_pad, p.ncta == 2 ? 64 : 128);
+      op.hm.w7[g] = make_map_2d(B.w, B.cin_pad, B.cout_pad, p.ncta == 2 ? 32 : 64);
       if (o.buf != -1) {
         op.hm.out32[g] = make_map_3d_store(plan.bufs[o.buf]->p, plan.buf_c[o.buf], uint64_t(gi.Hp()) * gi.Wp(), plan.n, 32);
         op.hm.out16[g] = make_map_3d_store(plan.bufs[o.buf]->p, plan.buf_c[o.buf], uint64_t(gi.Hp()) * gi.Wp(), plan.n, 16);
