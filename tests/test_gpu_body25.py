@@ -86,3 +86,40 @@ def test_split_batch_equals_whole(b25):
     for i in range(NB):
         one = be.forward(h, Frame(Dims(1, 3, H, W), per[i])).data
         assert one.tobytes() == whole[i].tobytes()
+
+
+_SINGLE_CTA_HEADS = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+import oracle_lib as O
+from paper_2103_04930_b200 import B200Backend, Dims, Frame, make_model, netspec
+be = B200Backend(0, slots=1)
+h = be.register_model(make_model("body25", netspec.spec("openpose_body25"), b"", netspec.BODY25_DIVISOR))
+w, hgt, nb = int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+f = Frame(Dims(1, 3 * nb, hgt, w), O.batched_frame(w, hgt, nb, seed=9))
+np.save(sys.argv[2], be.forward(h, f).data)
+be.close()
+"""
+
+
+def test_pair_heads_bit_identical_to_single_cta(b25, tmp_path):
+    """BODY_25's stage heads run on CTA pairs (conv_head2: M = 256 MMAs, the
+    input tile resident across the c6 blocks). Each output element sees the
+    same bf16 operands in the same K order as the single-CTA kernel, so the
+    whole forward is bit-identical to AVEC_HEAD2=0 (run in a subprocess). A
+    200x80 frame gives an odd number (3) of 128-pixel tiles per image at the head
+    level, so the pair's second CTA also runs a tile wholly past the image."""
+    import os
+    import pathlib
+    import subprocess
+    import sys
+    from paper_2103_04930_b200 import Dims, Frame
+    be, h = b25["be"], b25["h"]
+    w, hgt, nb = 200, 80, 3
+    frame = Frame(Dims(1, 3 * nb, hgt, w), O.batched_frame(w, hgt, nb, seed=9))
+    out = be.forward(h, frame).data
+    root = str(pathlib.Path(__file__).resolve().parent.parent)
+    dst = tmp_path / "single.npy"
+    subprocess.run([sys.executable, "-c", _SINGLE_CTA_HEADS, root, str(dst), str(w), str(hgt), str(nb)],
+                   env=dict(os.environ, AVEC_HEAD2="0"), check=True, timeout=600)
+    assert out.tobytes() == np.load(dst).tobytes()
