@@ -23,3 +23,7 @@ ncu --set full --clock-control none --import-source on -k regex:conv_head -s 1 -
 ncu --set full --clock-control none --import-source on -k regex:conv12 -c 1 -o $O/conv12 python tools/profile_forward.py > $O/ncu4.log 2>&1
 AVEC_CONV12=0 ncu --set full --clock-control none --import-source on -k regex:conv_first -c 1 -o $O/conv_first python tools/profile_forward.py > $O/ncu5.log 2>&1
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/smi.txt
+# BODY_25 stage head on CTA pairs (C5 shape)
+python tools/profile_forward.py --family openpose_body25 --width 1312 --height 736 --batch 32 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:conv_head2 -s 2 -c 1 -o $O/conv_head2 \
+    python tools/profile_forward.py --family openpose_body25 --width 1312 --height 736 --batch 32 > $O/ncu6.log 2>&1
