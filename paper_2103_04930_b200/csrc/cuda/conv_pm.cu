@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (POOL) {
           // sub-tile 0 (row y0) reads W_r, sub-tile 1 (row y0+1) reads W_r+1
           for (int c = 0; c < p.cin_chunks; ++c) {
+            const int kn = c + 1 == p.cin_chunks ? p.k16_last : 4;
             mbar_wait(&win_full[ws], wph);
             tc_fence_after();
             for (int r = 0; r < k; ++r) {
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t bb = wgt_base + wst * C::kWgtBytes;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
+                  if (kk >= kn) break;
                   const uint64_t bd = desc_sw128(bb + kk * 32);
                   const uint32_t accum = (first && kk == 0) ? 0u : 1u;
                   mma(d0, desc_sw128(wb0 + s * 128 + kk * 32), bd, accum);
@@ -282,6 +284,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
         for (int c = 0; c < p.cin_chunks; ++c) {
+          // the last chunk's zero-weight channel tail (96-channel dense blocks,
+          // mapped stage inputs) is skipped in 16-channel K steps
+          const int kn = c + 1 == p.cin_chunks ? p.k16_last : 4;
           for (int r = 0; r < k; ++r) {
             mbar_wait(&win_full[ws], wph);
             tc_fence_after();
@@ -294,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int sub = 0; sub < SUBS_M; ++sub) {
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
+                  if (kk >= kn) break;
                   const uint64_t ad = desc_sw128(wb + (sub * 128 + s) * 128 + kk * 32);
                   const uint64_t bd = desc_sw128(bb + kk * 32);
                   mma(d0 + sub * N, ad, bd, (first && kk == 0) ? 0u : 1u);

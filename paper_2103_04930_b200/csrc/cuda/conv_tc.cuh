@@ -71,6 +71,7 @@ struct ConvGroupParams {
 struct ConvParams {
   int k;               // filter size (1, 3, 7), stride 1, pad k/2
   int cin_chunks;      // input channels / 64 (padded)
+  int k16_last;        // pixel-major: 16-channel K steps with nonzero weights in the last chunk (1..4)
   int in_c_off;        // first input channel inside the source buffer
   int n_images;
   int H, W;            // output = input spatial size

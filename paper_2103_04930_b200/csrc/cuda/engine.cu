@@ -628,6 +628,20 @@ struct PlanBuilder {
     const Geometry& gi = plan.geo[in[0].level];
     p.k = L0.exec_k;
     p.cin_chunks = L0.cin_pad / 64;
+    // live input channels (highest nonzero weight column + 1) over the group:
+    // the pixel-major kernel skips the zero tail of the last 64-channel chunk
+    // (AVEC_K16TAIL=0 turns this off)
+    static const bool k16_tail = [] {
+      const char* e = std::getenv("AVEC_K16TAIL");
+      return !(e && e[0] == '0');
+    }();
+    int live = k16_tail ? 0 : L0.cin_pad;
+    for (int l : layers) {
+      const ConvDef& d = net.layers[l].def;
+      if (net.layers[l].exec_k != d.k) live = L0.cin_pad;  // conv1_1's packed taps
+      else live = std::max(live, d.cin_map.empty() ? d.cin : *std::max_element(d.cin_map.begin(), d.cin_map.end()) + 1);
+    }
+    p.k16_last = std::min(4, std::max(1, (live - 64 * (p.cin_chunks - 1) + 15) / 16));
     p.in_c_off = in[0].c_off;
     p.n_images = plan.n;
     p.H = gi.H;
