@@ -177,12 +177,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto conv11 = [&](uint32_t ph) {
         mbar_wait(imc_full, ph);
         tc_fence_after();
+        const uint64_t bd11 = desc_sw128(w11_base);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t ad = desc_sw64(imc_base + j * 8192);
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk)  // K = 32 covers the 27 taps
-            mma_bf16_ss(tmem + j * 64, desc_sw64(imc_base + j * 8192 + kk * 32), desc_sw128(w11_base + kk * 32),
-                        idesc, kk ? 1u : 0u);
+          for (int kk = 0; kk < 2; ++kk)  // K = 32 covers the 27 taps; a 32-byte K step adds 2 to a descriptor
+            mma_bf16_ss(tmem + j * 64, ad + 2 * kk, bd11 + 2 * kk, idesc, kk ? 1u : 0u);
+        }
         mma_commit(a1_full);
       };
       int ws = 0;
@@ -203,13 +205,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int s = 0; s < 3; ++s) {
             mbar_wait(&w12_full[ws], wph);
             tc_fence_after();
-            const uint32_t bb = w12_base + ws * 8192;
+            // descriptors once per tap; a 32-byte K step adds 2 to each
+            const uint64_t bd = desc_sw128(w12_base + ws * 8192);
+            const uint64_t a0 = desc_sw128(wb + r * 16384 + s * 128), a1 = desc_sw128(wb + (r + 1) * 16384 + s * 128);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t bd = desc_sw128(bb + kk * 32);
               const uint32_t accum = (r == 0 && s == 0 && kk == 0) ? 0u : 1u;
-              mma_bf16_ss(d0, desc_sw128(wb + r * 16384 + s * 128 + kk * 32), bd, idesc, accum);
-              mma_bf16_ss(d0 + 64, desc_sw128(wb + (r + 1) * 16384 + s * 128 + kk * 32), bd, idesc, accum);
+              mma_bf16_ss(d0, a0 + 2 * kk, bd + 2 * kk, idesc, accum);
+              mma_bf16_ss(d0 + 64, a1 + 2 * kk, bd + 2 * kk, idesc, accum);
             }
             mma_commit(&w12_empty[ws]);
             if (++ws == kW12Stages) { ws = 0; wph ^= 1; }

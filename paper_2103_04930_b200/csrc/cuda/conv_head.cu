@@ -182,10 +182,10 @@ __global__ void __launch_bounds__(kHThreads, 1)
         for (int kc = 0; kc < kc_per_block; ++kc) {
           mbar_wait(&w7_full[w7s], w7ph);
           tc_fence_after();
-          const uint32_t ya = y_base + b * 32768 + kc * 16384, wb = w7_base + w7s * 8192;
+          const uint64_t ya = desc_sw128(y_base + b * 32768 + kc * 16384), wb = desc_sw128(w7_base + w7s * 8192);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_bf16_ss(tmem + kAcc2Col, desc_sw128(ya + kk * 32), desc_sw128(wb + kk * 32), idesc2,
+          for (int kk = 0; kk < 4; ++kk)  // a 32-byte K step adds 2 to a descriptor
+            mma_bf16_ss(tmem + kAcc2Col, ya + 2 * kk, wb + 2 * kk, idesc2,
                         (first_of_tile && kc == 0 && kk == 0) ? 0u : 1u);
           mma_commit(&w7_empty[w7s]);
           if (++w7s == kW7Stages) { w7s = 0; w7ph ^= 1; }
@@ -202,10 +202,10 @@ __global__ void __launch_bounds__(kHThreads, 1)
             mbar_wait(&x_full[xs], xph);
             mbar_wait(&w6_full[w6s], w6ph);
             tc_fence_after();
-            const uint32_t xa = x_base + xs * 16384, wb = w6_base + w6s * 16384;
+            const uint64_t xa = desc_sw128(x_base + xs * 16384), wb = desc_sw128(w6_base + w6s * 16384);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ss(tmem + b * NB, desc_sw128(xa + kk * 32), desc_sw128(wb + kk * 32), idesc1,
+              mma_bf16_ss(tmem + b * NB, xa + 2 * kk, wb + 2 * kk, idesc1,
                           (c == 0 && kk == 0) ? 0u : 1u);
             mma_commit(&x_empty[xs]);
             mma_commit(&w6_empty[w6s]);
@@ -535,10 +535,10 @@ __global__ void __launch_bounds__(kH2Threads, 1)
         for (int kc = 0; kc < NB / 64; ++kc) {
           mbar_wait(&w7_full[s7], ph7);
           tc_fence_after();
-          const uint32_t ya = y_base + b * 32768 + kc * 16384, wb = w7_base + s7 * 4096;
+          const uint64_t ya = desc_sw128(y_base + b * 32768 + kc * 16384), wb = desc_sw128(w7_base + s7 * 4096);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_bf16_ss_pair(tmem + kAcc2Col, desc_sw128(ya + kk * 32), desc_sw128(wb + kk * 32), idesc2,
+          for (int kk = 0; kk < 4; ++kk)  // a 32-byte K step adds 2 to a descriptor
+            mma_bf16_ss_pair(tmem + kAcc2Col, ya + 2 * kk, wb + 2 * kk, idesc2,
                              (first_of_tile && kc == 0 && kk == 0) ? 0u : 1u);
           mma_commit_pair(&w7_empty[s7]);
           if (++s7 == kH2W7Stages) { s7 = 0; ph7 ^= 1; }
@@ -552,10 +552,10 @@ __global__ void __launch_bounds__(kH2Threads, 1)
             if (j == 0) mbar_wait(&x_full[c], xph);
             mbar_wait(&w6_full[s6], ph6);
             tc_fence_after();
-            const uint32_t xa = x_base + c * 16384, wb = w6_base + s6 * 8192;
+            const uint64_t xa = desc_sw128(x_base + c * 16384), wb = desc_sw128(w6_base + s6 * 8192);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ss_pair(tmem + b * NB, desc_sw128(xa + kk * 32), desc_sw128(wb + kk * 32), idesc1,
+              mma_bf16_ss_pair(tmem + b * NB, xa + 2 * kk, wb + 2 * kk, idesc1,
                                (c == 0 && kk == 0) ? 0u : 1u);
             mma_commit_pair(&w6_empty[s6]);
             if (j == p.blocks - 1) mma_commit_pair(&x_empty[c]);  // the next tile may refill chunk c

@@ -52,7 +52,10 @@ struct PmCfg {
   static constexpr int kWinBytes = kWinRows * 128;
   // N = 64 serves the short-K high-resolution conv1_2 (and the thin heads):
   // one more window in flight keeps its HBM reads streaming
-  static constexpr int kWinStages = POOL ? 6 : N == 64 ? 4 : N == 256 ? 2 : 3;
+#ifndef AVEC_PM_WIN_EXTRA
+#define AVEC_PM_WIN_EXTRA 0
+#endif
+  static constexpr int kWinStages = POOL ? 6 : N == 64 ? 4 : N == 256 ? 2 : 3 + AVEC_PM_WIN_EXTRA;
   static constexpr int kWgtBytes = (N / NCTA) * 128;  // this CTA's N/NCTA rows x 64 bf16
   static constexpr int kAccCols = SUBS_M * N;
   static constexpr int kAccStages = 2;
@@ -262,14 +265,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int s = 0; s < k; ++s) {
                 mbar_wait(&w_full[wst], wtph);
                 tc_fence_after();
-                const uint32_t bb = wgt_base + wst * C::kWgtBytes;
+                const uint64_t bd = desc_sw128(wgt_base + wst * C::kWgtBytes);
+                const uint64_t a0 = desc_sw128(wb0 + s * 128), a1 = desc_sw128(wb1 + s * 128);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
+                for (int kk = 0; kk < 4; ++kk) {  // a 32-byte K step adds 2 to a descriptor
                   if (kk >= kn) break;
-                  const uint64_t bd = desc_sw128(bb + kk * 32);
                   const uint32_t accum = (first && kk == 0) ? 0u : 1u;
-                  mma(d0, desc_sw128(wb0 + s * 128 + kk * 32), bd, accum);
-                  mma(d0 + N, desc_sw128(wb1 + s * 128 + kk * 32), bd, accum);
+                  mma(d0, a0 + 2 * kk, bd + 2 * kk, accum);
+                  mma(d0 + N, a1 + 2 * kk, bd + 2 * kk, accum);
                 }
                 first = false;
                 commit(&w_empty[wst]);
@@ -295,14 +298,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_wait(&w_full[wst], wtph);
               tc_fence_after();
               const uint32_t bb = wgt_base + wst * C::kWgtBytes;
+              // descriptors built once per tap: a 32-byte K step adds 2 to the
+              // start-address field (addresses < 256 KB, so it cannot carry out)
+              const uint64_t bd0 = desc_sw128(bb);
 #pragma unroll
               for (int sub = 0; sub < SUBS_M; ++sub) {
+                const uint64_t ad0 = desc_sw128(wb + (sub * 128 + s) * 128);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                   if (kk >= kn) break;
-                  const uint64_t ad = desc_sw128(wb + (sub * 128 + s) * 128 + kk * 32);
-                  const uint64_t bd = desc_sw128(bb + kk * 32);
-                  mma(d0 + sub * N, ad, bd, (first && kk == 0) ? 0u : 1u);
+                  mma(d0 + sub * N, ad0 + 2 * kk, bd0 + 2 * kk, (first && kk == 0) ? 0u : 1u);
                 }
               }
               first = false;

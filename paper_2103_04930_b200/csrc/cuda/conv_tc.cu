@@ -237,16 +237,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int s = 0; s < k; ++s) {
               mbar_wait(&w_full[wst], wtph);
               tc_fence_after();
-              const uint32_t ab = wgt_base + wst * kWgtBytes;
+              // descriptors once per tap; a 32-byte K step adds 2 to each
+              const uint64_t ad = desc_sw128(wgt_base + wst * kWgtBytes);
 #pragma unroll
               for (int sub = 0; sub < SUBS; ++sub) {
                 if (sub < nsub) {
+                  const uint64_t bd = desc_sw128(wb + (sub * kSubN + s) * 128);
 #pragma unroll
-                  for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t ad = desc_sw128(ab + kk * 32);
-                    const uint64_t bd = desc_sw128(wb + (sub * kSubN + s) * 128 + kk * 32);
-                    mma_bf16_ss(d0 + sub * kSubN, ad, bd, idesc[sub], (first && kk == 0) ? 0u : 1u);
-                  }
+                  for (int kk = 0; kk < 4; ++kk)
+                    mma_bf16_ss(d0 + sub * kSubN, ad + 2 * kk, bd + 2 * kk, idesc[sub], (first && kk == 0) ? 0u : 1u);
                 }
               }
               first = false;
