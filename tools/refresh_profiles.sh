@@ -27,3 +27,7 @@ nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/smi.txt
 python tools/profile_forward.py --family openpose_body25 --width 1312 --height 736 --batch 32 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:conv_head2 -s 2 -c 1 -o $O/conv_head2 \
     python tools/profile_forward.py --family openpose_body25 --width 1312 --height 736 --batch 32 > $O/ncu6.log 2>&1
+# BODY_25 96-channel dense-block conv (C5, the 12th pixel-major launch): MMA issue-bound before the
+# per-tap descriptors
+ncu --set full --clock-control none --import-source on -k regex:conv_pm -s 11 -c 1 -o $O/conv_pm96 \
+    python tools/profile_forward.py --family openpose_body25 --width 1312 --height 736 --batch 32 > $O/ncu7.log 2>&1
