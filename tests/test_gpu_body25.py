@@ -123,3 +123,24 @@ def test_pair_heads_bit_identical_to_single_cta(b25, tmp_path):
     subprocess.run([sys.executable, "-c", _SINGLE_CTA_HEADS, root, str(dst), str(w), str(hgt), str(nb)],
                    env=dict(os.environ, AVEC_HEAD2="0"), check=True, timeout=600)
     assert out.tobytes() == np.load(dst).tobytes()
+
+
+def test_k16_tail_skip_bit_identical(b25, tmp_path):
+    """The pixel-major kernel skips the zero-weight K16 steps of a layer's last
+    64-channel chunk (96-channel dense-block inputs, 288-channel block concats,
+    the mapped stage input). Those steps only add exact zeros, so the forward
+    is bit-identical to issuing them (AVEC_K16TAIL=0, in a subprocess)."""
+    import os
+    import pathlib
+    import subprocess
+    import sys
+    from paper_2103_04930_b200 import Dims, Frame
+    be, h = b25["be"], b25["h"]
+    w, hgt, nb = 200, 80, 3
+    frame = Frame(Dims(1, 3 * nb, hgt, w), O.batched_frame(w, hgt, nb, seed=9))
+    out = be.forward(h, frame).data
+    root = str(pathlib.Path(__file__).resolve().parent.parent)
+    dst = tmp_path / "full_k.npy"
+    subprocess.run([sys.executable, "-c", _SINGLE_CTA_HEADS, root, str(dst), str(w), str(hgt), str(nb)],
+                   env=dict(os.environ, AVEC_K16TAIL="0"), check=True, timeout=600)
+    assert out.tobytes() == np.load(dst).tobytes()
