@@ -66,10 +66,20 @@ struct PmCfg {
   static constexpr int win = 0;
   static constexpr int stg = win + kWinStages * kWinBytes;
   static constexpr int wgt = stg + kStgBytes;
-  static constexpr int kWgtStages = (232448 - 1024 - 4352 - wgt) / kWgtBytes > 16
-                                        ? 16
-                                        : (232448 - 1024 - 4352 - wgt) / kWgtBytes;
-  static constexpr int bias = wgt + kWgtStages * kWgtBytes;  // N bias + N slope floats per acc stage
+  // N = 96: one weight stage holds the 3 taps of a filter row (one barrier
+  // wait and one commit per row instead of per tap; BODY_25's 96-channel
+  // dense-block convs -7..-13%, 5 row stages in flight). N = 128/256 have
+  // only 3 row stages: the VGG layers lost 3-4% there, so they keep per-tap
+  // stages, as do pooled tiles. -DAVEC_PM_ROWW=0 turns it off.
+#ifndef AVEC_PM_ROWW
+#define AVEC_PM_ROWW 1
+#endif
+  static constexpr int kWgtFree = 232448 - 1024 - 4352 - wgt;
+  static constexpr int kTaps =
+      (AVEC_PM_ROWW && !POOL && N == 96 && kWgtFree / (3 * kWgtBytes) >= 3) ? 3 : 1;
+  static constexpr int kWgtStageBytes = kTaps * kWgtBytes;
+  static constexpr int kWgtStages = kWgtFree / kWgtStageBytes > 16 ? 16 : kWgtFree / kWgtStageBytes;
+  static constexpr int bias = wgt + kWgtStages * kWgtStageBytes;  // N bias + N slope floats per acc stage
   static constexpr int bars = bias + 2 * kAccStages * N * 4;
   static constexpr int total = bars + 256;
   static_assert(kWinBytes % 1024 == 0 && wgt % 1024 == 0 && stg % 1024 == 0, "SW128 alignment");
@@ -188,17 +198,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++ws == C::kWinStages) { ws = 0; wph ^= 1; }
       };
       auto load_weights = [&](const PmTile& tc, int c, int r) {
+        // kTaps == 3: the row's k taps share one stage (tap s at slot s)
+        const int per_stage = C::kTaps == 1 ? 1 : k;
         for (int s = 0; s < k; ++s) {
-          mbar_wait(&w_empty[wst], wtph ^ 1);
-          if (leader) mbar_arrive_expect_tx(&w_full[wst], NCTA * C::kWgtBytes);
+          const int sl = C::kTaps == 1 ? 0 : s;
+          if (sl == 0) {
+            mbar_wait(&w_empty[wst], wtph ^ 1);
+            if (leader) mbar_arrive_expect_tx(&w_full[wst], NCTA * C::kWgtBytes * per_stage);
+          }
           const int kx = ((r * k + s) * p.cin_chunks + c) * 64;
           const int wrow = tc.nt * N + int(rank) * (N / NCTA);  // this CTA's half of B
+          uint8_t* dst = wgt + wst * C::kWgtStageBytes + sl * C::kWgtBytes;
           if constexpr (NCTA == 2)
-            tma_load_2d_pair_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], mapa_shared(&w_full[wst], 0), kx,
-                                  wrow, keep);
+            tma_load_2d_pair_hint(dst, &maps.wgt[tc.g], mapa_shared(&w_full[wst], 0), kx, wrow, keep);
           else
-            tma_load_2d_hint(wgt + wst * C::kWgtBytes, &maps.wgt[tc.g], &w_full[wst], kx, wrow, keep);
-          if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
+            tma_load_2d_hint(dst, &maps.wgt[tc.g], &w_full[wst], kx, wrow, keep);
+          if (sl + 1 == per_stage && ++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
         }
       };
       for (int t = int(blockIdx.x) / NCTA; t < p.total_tiles; t += int(gridDim.x) / NCTA) {
@@ -265,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int s = 0; s < k; ++s) {
                 mbar_wait(&w_full[wst], wtph);
                 tc_fence_after();
-                const uint64_t bd = desc_sw128(wgt_base + wst * C::kWgtBytes);
+                const uint64_t bd = desc_sw128(wgt_base + wst * C::kWgtStageBytes);
                 const uint64_t a0 = desc_sw128(wb0 + s * 128), a1 = desc_sw128(wb1 + s * 128);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {  // a 32-byte K step adds 2 to a descriptor
@@ -294,10 +309,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&win_full[ws], wph);
             tc_fence_after();
             const uint32_t wb = win_base + ws * C::kWinBytes;
-            for (int s = 0; s < k; ++s) {
+            if constexpr (C::kTaps == 3) {
               mbar_wait(&w_full[wst], wtph);
               tc_fence_after();
-              const uint32_t bb = wgt_base + wst * C::kWgtBytes;
+            }
+            for (int s = 0; s < k; ++s) {
+              if constexpr (C::kTaps == 1) {
+                mbar_wait(&w_full[wst], wtph);
+                tc_fence_after();
+              }
+              const uint32_t bb = wgt_base + wst * C::kWgtStageBytes + (C::kTaps == 1 ? 0 : s * C::kWgtBytes);
               // descriptors built once per tap: a 32-byte K step adds 2 to the
               // start-address field (addresses < 256 KB, so it cannot carry out)
               const uint64_t bd0 = desc_sw128(bb);
@@ -311,6 +332,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
               first = false;
+              if constexpr (C::kTaps == 1) {
+                commit(&w_empty[wst]);
+                if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
+              }
+            }
+            if constexpr (C::kTaps == 3) {
               commit(&w_empty[wst]);
               if (++wst == C::kWgtStages) { wst = 0; wtph ^= 1; }
             }
