@@ -55,7 +55,13 @@ struct PmCfg {
 #ifndef AVEC_PM_WIN_EXTRA
 #define AVEC_PM_WIN_EXTRA 0
 #endif
-  static constexpr int kWinStages = POOL ? 6 : N == 64 ? 4 : N == 256 ? 2 : 3 + AVEC_PM_WIN_EXTRA;
+#ifndef AVEC_PM_ROWW128
+#define AVEC_PM_ROWW128 0
+#endif
+  // AVEC_PM_ROWW128: N = 128 tiles trade their third window stage for row-wide
+  // weight stages (5 instead of 3)
+  static constexpr int kWinStages = POOL ? 6 : N == 64 ? 4 : N == 256 ? 2
+                                  : (N == 128 && AVEC_PM_ROWW128) ? 2 : 3 + AVEC_PM_WIN_EXTRA;
   static constexpr int kWgtBytes = (N / NCTA) * 128;  // this CTA's N/NCTA rows x 64 bf16
   static constexpr int kAccCols = SUBS_M * N;
   static constexpr int kAccStages = 2;
@@ -76,7 +82,7 @@ struct PmCfg {
 #endif
   static constexpr int kWgtFree = 232448 - 1024 - 4352 - wgt;
   static constexpr int kTaps =
-      (AVEC_PM_ROWW && !POOL && N == 96 && kWgtFree / (3 * kWgtBytes) >= 3) ? 3 : 1;
+      (AVEC_PM_ROWW && !POOL && (N == 96 || (N == 128 && AVEC_PM_ROWW128)) && kWgtFree / (3 * kWgtBytes) >= 3) ? 3 : 1;
   static constexpr int kWgtStageBytes = kTaps * kWgtBytes;
   static constexpr int kWgtStages = kWgtFree / kWgtStageBytes > 16 ? 16 : kWgtFree / kWgtStageBytes;
   static constexpr int bias = wgt + kWgtStages * kWgtStageBytes;  // N bias + N slope floats per acc stage
