@@ -75,8 +75,8 @@ struct PmCfg {
   // N = 96: one weight stage holds the 3 taps of a filter row (one barrier
   // wait and one commit per row instead of per tap; BODY_25's 96-channel
   // dense-block convs -7..-13%, 5 row stages in flight). N = 128/256 have
-  // only 3 row stages: the VGG layers lost 3-4% there, so they keep per-tap
-  // stages, as do pooled tiles. -DAVEC_PM_ROWW=0 turns it off.
+  // only 3 row stages and measured no better (within C5's clock noise), so
+  // they keep per-tap stages, as do pooled tiles. -DAVEC_PM_ROWW=0 turns it off.
 #ifndef AVEC_PM_ROWW
 #define AVEC_PM_ROWW 1
 #endif
