@@ -135,6 +135,17 @@ int avec_posenet_layer_fusion(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32
 int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                           uint32_t w, const float* in, int layer, float* layer_in,
                           uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);
+/* Full-size parity hook: the same run as avec_posenet_layer_io, but only the
+ * selected rows are copied out, so configurations of any size (C2, C5) can be
+ * checked row by row against the CPU oracle. in_rows / out_rows: n_in / n_out
+ * (image, y) pairs of the layer's input view (avec_posenet_layer_io's input,
+ * at the layer's level) and output view (at avec_posenet_layer_out_level).
+ * Rows with y outside [0, H) come back as zeros, which is the conv's zero
+ * padding, so a k-row input window can be requested as is. layer_in:
+ * [n_in][W_in][cin], layer_out: [n_out][W_out][cout], unpadded fp32. */
+int avec_posenet_layer_rows(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                            const float* in, int layer, int n_in, const int32_t* in_rows, float* layer_in,
+                            int n_out, const int32_t* out_rows, float* layer_out);
 /* Profiling hook (bench.py roofline): replays the plan of this shape op by op
  * with CUDA events on the slot stream, `reps` times, after one warm graph run.
  * Per op i < *n_ops: kind (0 = fused first layer, 1 = pixel-major tcgen05 conv,

@@ -45,6 +45,12 @@ float oracle_bf16_round(float x);
 void oracle_conv2d_nhwc(const float* in, int n, int h, int w, int cin,
                         const float* weight, const float* bias, int cout, int k,
                         int act, const float* slope, int out_round_bf16, float* out);
+/* Selected output rows: out[r][w][cout] from the k-row input window
+ * win[r][k][w][cin] of each row (rows outside the image zero-filled by the
+ * caller); identical arithmetic to oracle_conv2d_nhwc. */
+void oracle_conv2d_rows(const float* win, int n_rows, int k, int w, int cin, const float* weight,
+                        const float* bias, int cout, int act, const float* slope, int out_round_bf16,
+                        float* out);
 void oracle_maxpool2_nhwc(const float* in, int n, int h, int w, int c, float* out);
 
 /* ---- post-processing oracle ---- */

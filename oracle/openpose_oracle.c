@@ -106,6 +106,75 @@ void oracle_conv2d_nhwc(const float* in, int n, int h, int w, int cin,
   free(wt);
 }
 
+/* Selected output rows of one conv layer (full-size parity checks): each of
+ * the n_rows outputs row r comes from its own k-row input window
+ * win[r][0..k-1][w][cin] (rows outside the image already zero — the layer's
+ * zero padding), columns padded by k/2 zeros here. Same arithmetic as
+ * oracle_conv2d_nhwc, so a row computed here equals that row of the whole
+ * tensor. Work is split over (row, 16-column chunk). */
+typedef struct {
+  const float* win; const double* wt; const float* bias; float* out;
+  int n_rows, k, w, cin, cout, act, rnd;
+  const float* slope;
+  int next; /* guarded by atomic fetch-add */
+} rows_job;
+
+static void* rows_worker(void* arg) {
+  rows_job* j = (rows_job*)arg;
+  const int k = j->k, pad = k / 2, w = j->w, cin = j->cin, cout = j->cout;
+  const int chunks = (w + 15) / 16;
+  double* acc = (double*)malloc(sizeof(double) * (size_t)cout);
+  for (;;) {
+    int item = __atomic_fetch_add(&j->next, 1, __ATOMIC_RELAXED);
+    if (item >= j->n_rows * chunks) break;
+    const int row = item / chunks, x0 = (item % chunks) * 16;
+    const int x1 = x0 + 16 < w ? x0 + 16 : w;
+    const float* win = j->win + (size_t)row * k * w * cin;
+    for (int x = x0; x < x1; ++x) {
+      for (int co = 0; co < cout; ++co) acc[co] = 0.0;
+      for (int r = 0; r < k; ++r)
+        for (int s = 0; s < k; ++s) {
+          const int ix = x + s - pad;
+          if (ix < 0 || ix >= w) continue;
+          const float* px = win + ((size_t)r * w + ix) * cin;
+          const double* wrs = j->wt + ((size_t)r * k + s) * cin * cout;
+          for (int ci = 0; ci < cin; ++ci) {
+            const double v = (double)px[ci];
+            const double* wr = wrs + (size_t)ci * cout;
+            for (int co = 0; co < cout; ++co) acc[co] += v * wr[co];
+          }
+        }
+      float* o = j->out + ((size_t)row * w + x) * cout;
+      for (int co = 0; co < cout; ++co) {
+        float v = (float)(acc[co] + (double)j->bias[co]);
+        if (j->act == 1 && v < 0.f) v = 0.f;
+        if (j->act == 2 && v < 0.f) v = v * j->slope[co];
+        o[co] = j->rnd ? oracle_bf16_round(v) : v;
+      }
+    }
+  }
+  free(acc);
+  return NULL;
+}
+
+void oracle_conv2d_rows(const float* win, int n_rows, int k, int w, int cin, const float* weight,
+                        const float* bias, int cout, int act, const float* slope, int out_round_bf16,
+                        float* out) {
+  double* wt = (double*)malloc(sizeof(double) * (size_t)k * k * cin * cout);
+  for (int co = 0; co < cout; ++co)
+    for (int ci = 0; ci < cin; ++ci)
+      for (int r = 0; r < k; ++r)
+        for (int s = 0; s < k; ++s)
+          wt[(((size_t)r * k + s) * cin + ci) * cout + co] =
+              (double)weight[(((size_t)co * cin + ci) * k + r) * k + s];
+  rows_job j = {win, wt, bias, out, n_rows, k, w, cin, cout, act, out_round_bf16, slope, 0};
+  int nt = oracle_threads();
+  pthread_t th[64];
+  for (int t = 0; t < nt; ++t) pthread_create(&th[t], NULL, rows_worker, &j);
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+  free(wt);
+}
+
 /* Caffe Pooling MAX kernel 2 stride 2, NHWC; h and w even */
 void oracle_maxpool2_nhwc(const float* in, int n, int h, int w, int c, float* out) {
   const int ho = h / 2, wo = w / 2;

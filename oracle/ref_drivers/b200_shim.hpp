@@ -49,7 +49,10 @@ class B200Backend final : public Backend {
     if (rc == AVEC_OK) return;
     const std::string msg = avec_last_error();
     switch (rc) {
-      case AVEC_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+      // a shape the net rejects comes from the client's own FrameData/Resolution; the
+      // reference Server only catches accelfwd::Error (server.cpp:315, 334), so it must
+      // not leave as std::invalid_argument (that would terminate the server)
+      case AVEC_ERR_INVALID_ARGUMENT: raise(ErrorCode::invariant_violation, msg);
       case AVEC_ERR_UNKNOWN_MODEL: raise(ErrorCode::unknown_model, msg);
       case AVEC_ERR_INVALID_MODEL: raise(ErrorCode::invalid_model, msg);
       case AVEC_ERR_DEGENERATE_OUTPUT: raise(ErrorCode::degenerate_output, msg);

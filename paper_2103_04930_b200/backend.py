@@ -225,6 +225,26 @@ class B200Backend:
                                                  lin.size, lout.ctypes.data, lout.size))
         return lin, lout
 
+    def layer_rows(self, handle: ModelHandle, frame: Frame, layer: int, in_rows, out_rows):
+        """Selected rows of conv `layer`'s input and output views
+        (avec_posenet_layer_rows): `in_rows` / `out_rows` are (image, y) pairs;
+        rows outside the image come back as zeros. Returns fp32 arrays
+        [len(in_rows)][W_in][cin] and [len(out_rows)][W_out][cout]."""
+        info = self.layer_info(handle, layer)
+        d = frame.dims
+        ol = self.layer_out_level(handle, d, layer)
+        _, src = self.layer_fusion(handle, d, layer)
+        cin = self.layer_info(handle, src)["cin"]
+        ir = np.ascontiguousarray(np.asarray(in_rows, np.int32).reshape(-1, 2))
+        orr = np.ascontiguousarray(np.asarray(out_rows, np.int32).reshape(-1, 2))
+        lin = np.empty((len(ir), d.width >> info["level"], cin), np.float32)
+        lout = np.empty((len(orr), d.width >> ol, info["cout"]), np.float32)
+        data = np.ascontiguousarray(frame.data, np.float32).ravel()
+        _lib.check(self._L.avec_posenet_layer_rows(self._ctx, handle.id, d.batch, d.channels, d.height, d.width,
+                                                   data.ctypes.data, layer, len(ir), ir.ctypes.data,
+                                                   lin.ctypes.data, len(orr), orr.ctypes.data, lout.ctypes.data))
+        return lin, lout
+
     def profile(self, handle: ModelHandle, dims: Dims, d_in: int, reps: int = 3) -> list:
         """Per-launch device timings of the pose-net plan (see avec_posenet_profile)."""
         n = ctypes.c_int(0)

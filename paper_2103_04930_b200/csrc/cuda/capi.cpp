@@ -323,6 +323,17 @@ int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c
   });
 }
 
+int avec_posenet_layer_rows(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                            const float* in, int layer, int n_in, const int32_t* in_rows, float* layer_in,
+                            int n_out, const int32_t* out_rows, float* layer_out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(in, "in");
+    avec::posenet_layer_rows(ctx, handle, n, c, h, w, in, layer, n_in, in_rows, layer_in, n_out, out_rows,
+                             layer_out);
+  });
+}
+
 int avec_posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                          uint32_t w, const float* d_in, int reps, int max_ops, int* n_ops,
                          int* op_kind, double* op_flops, double* op_bytes, float* op_ms) {

@@ -591,6 +591,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int N, int SUBS_M, int NCTA, bool POOL = false>
 void launch_pm(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
+  // row-wide weight stages hold one filter row's taps (tap s in slot s): a
+  // wider filter would write past its stage into the next one
+  if (PmCfg<N, SUBS_M, NCTA, POOL>::kTaps > 1 && p.k > PmCfg<N, SUBS_M, NCTA, POOL>::kTaps)
+    fail(AVEC_ERR_UNSUPPORTED, "pixel-major conv: filter wider than the row-wide weight stage");
   const int pairs = sm_count / NCTA;
   const int grid = NCTA * (p.total_tiles < pairs ? p.total_tiles : pairs);
   cudaLaunchConfig_t cfg{};

@@ -319,7 +319,15 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
   }
   check_cuda(cudaSetDevice(device), "cudaSetDevice");
   net->mem.ensure(total, device);
-  check_cuda(cudaMemcpy(net->mem.p, host.data(), total, cudaMemcpyHostToDevice), "weights H2D");
+  // on a private stream, synchronised: a pageable cudaMemcpy may return before
+  // the DMA lands, and the slots' non-blocking streams do not order after the
+  // legacy stream
+  cudaStream_t up = nullptr;
+  check_cuda(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking), "upload stream");
+  cudaError_t e = cudaMemcpyAsync(net->mem.p, host.data(), total, cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(up);
+  cudaStreamDestroy(up);
+  check_cuda(e, "weights H2D");
   char* base = net->mem.as<char>();
   for (size_t i = 0; i < f.convs.size(); ++i) {
     net->layers[i].w = base + w_off[i];
@@ -349,6 +357,7 @@ struct PlanBuilder {
   Plan& plan;
   const PoseNet& net;
   int device;
+  cudaStream_t stream;  // the building slot's stream
 
   int sm_count() const {
     int n = 0;
@@ -361,7 +370,9 @@ struct PlanBuilder {
     auto m = std::make_unique<DevMem>();
     const size_t bytes = size_t(plan.n) * g.Hp() * g.Wp() * C * 2;
     m->ensure(bytes, device);
-    check_cuda(cudaMemset(m->p, 0, bytes), "zero activation buffer");  // zero border + pad channels
+    // zero border + pad channels, on the slot stream (get_plan synchronises it
+    // before the plan is used on any stream)
+    check_cuda(cudaMemsetAsync(m->p, 0, bytes, stream), "zero activation buffer");
     plan.bufs.push_back(std::move(m));
     plan.buf_level.push_back(level);
     plan.buf_c.push_back(C);
@@ -831,9 +842,9 @@ int build_trunk(PlanBuilder& b, Plan& plan, int cat, int trunk_off) {
 }
 
 // COCO program (pose_deploy_linevec.prototxt) on padded-flat buffers
-void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
+void build_coco_plan(Plan& plan, const PoseNet& net, int device, cudaStream_t stream) {
   const PoseFamily& f = net.fam;
-  PlanBuilder b{plan, net, device};
+  PlanBuilder b{plan, net, device, stream};
   const int nl = int(f.convs.size());
   plan.layer_in.assign(nl, TensorView{});
   plan.layer_out.assign(nl, TensorView{});
@@ -878,9 +889,9 @@ void build_coco_plan(Plan& plan, const PoseNet& net, int device) {
 // BODY_25 program: 4 PAF stages then 2 heatmap stages, each 5 dense blocks of
 // three 3x3 PReLU convs concatenated in place (ping-pong X/Y buffers) + Mconv6/7.
 // Stage concat buffer: [heat 0..25 | PAF 32..83 | trunk 88..215] (netspec.hpp).
-void build_body25_plan(Plan& plan, const PoseNet& net, int device) {
+void build_body25_plan(Plan& plan, const PoseNet& net, int device, cudaStream_t stream) {
   const PoseFamily& f = net.fam;
-  PlanBuilder b{plan, net, device};
+  PlanBuilder b{plan, net, device, stream};
   const int nl = int(f.convs.size());
   plan.layer_in.assign(nl, TensorView{});
   plan.layer_out.assign(nl, TensorView{});
@@ -980,9 +991,12 @@ Plan* get_plan(avec_ctx* ctx, Slot* slot, const Model& m, int n_img, int H, int 
   plan->in.ensure(plan->in_elems * 4, ctx->device);
   plan->out.ensure(plan->out_elems * 4, ctx->device);
   if (m.net->fam.body25())
-    build_body25_plan(*plan, *m.net, ctx->device);
+    build_body25_plan(*plan, *m.net, ctx->device, slot->stream);
   else
-    build_coco_plan(*plan, *m.net, ctx->device);
+    build_coco_plan(*plan, *m.net, ctx->device, slot->stream);
+  // the zeroed buffers must be in place before a forward on any stream (a
+  // caller's stream in forward_device) reads them
+  check_cuda(cudaStreamSynchronize(slot->stream), "plan zero-fill");
   // capture the whole op sequence once; replays cost one launch
   cudaGraph_t g = nullptr;
   check_cuda(cudaStreamBeginCapture(slot->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
@@ -1315,22 +1329,120 @@ int posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t
   return v.buf >= 0 ? v.level : f.convs[layer].level;
 }
 
+namespace {
+
+// Parity hooks: run the plan of this shape from the host frames `in` through
+// the op that produces `layer`, on the leased slot's stream (ordered after the
+// slot's previous asynchronous forward, which may still read plan->in).
+Plan* run_to_layer(avec_ctx* ctx, SlotLease& lease, const Model& m, uint32_t n, uint32_t c, uint32_t h,
+                   uint32_t w, const float* in, int layer, int& n_img) {
+  if (m.kind != AVEC_MODEL_POSENET) fail(AVEC_ERR_INVALID_ARGUMENT, "not a pose net");
+  posenet_shape(m, n, c, h, w, n_img);
+  const PoseFamily& f = m.net->fam;
+  if (layer < 0 || layer >= int(f.convs.size())) fail(AVEC_ERR_INVALID_ARGUMENT, "layer index");
+  Slot* s = lease.slot();
+  lease.after_pending(s->stream);
+  Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
+  if (plan->layer_fusion[layer] == 2)
+    fail(AVEC_ERR_UNSUPPORTED, f.convs[layer].name + " is fused into the next layer: its output never leaves the SM");
+  const uint64_t E = uint64_t(n) * c * h * w;
+  check_cuda(cudaMemcpyAsync(plan->in.p, in, E * 4, cudaMemcpyHostToDevice, s->stream), "H2D");
+  size_t last = 0;
+  for (size_t i = 0; i < plan->ops.size(); ++i)
+    if (plan->ops[i].layers[0] == layer || plan->ops[i].layers[1] == layer) last = i + 1;
+  run_ops(ctx, *plan, *m.net, 0, last, s->stream);
+  check_cuda(cudaStreamSynchronize(s->stream), "layer io sync");
+  return plan;
+}
+
+float bf16_to_float(uint16_t b) {
+  const uint32_t u = uint32_t(b) << 16;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+}  // namespace
+
+void posenet_layer_rows(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                        const float* in, int layer, int n_in, const int32_t* in_rows, float* layer_in, int n_out,
+                        const int32_t* out_rows, float* layer_out) {
+  const Model m = model_lookup(ctx, handle);
+  check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (n_in < 0 || n_out < 0 || (n_in && (!in_rows || !layer_in)) || (n_out && (!out_rows || !layer_out)))
+    fail(AVEC_ERR_INVALID_ARGUMENT, "row selections");
+  SlotLease lease(ctx);
+  Slot* s = lease.slot();
+  int n_img = 0;
+  Plan* plan = run_to_layer(ctx, lease, m, n, c, h, w, in, layer, n_img);
+  const PoseFamily& f = m.net->fam;
+  const ConvDef& d = f.convs[layer];
+  const ConvDef& din = f.convs[plan->layer_in_from[layer]];
+  std::vector<float> out_all;  // fp32 NCHW plan output, fetched once if a view needs it
+  // rows (image, y) of view `v` at level `lv` as unpadded fp32 [W][cdim];
+  // rows outside the image are zeros (the next layer's zero padding)
+  auto rows = [&](const TensorView& v, int lv, int cdim, const std::vector<int>& map, int count,
+                  const int32_t* sel, float* dst) {
+    const Geometry& g = plan->geo[lv];
+    const int Hl = int(h) >> lv, Wl = int(w) >> lv;
+    std::vector<uint16_t> raw;
+    for (int r = 0; r < count; ++r) {
+      const int b = sel[2 * r], y = sel[2 * r + 1];
+      float* o = dst + size_t(r) * Wl * cdim;
+      if (b < 0 || b >= n_img) fail(AVEC_ERR_INVALID_ARGUMENT, "row selection: image index");
+      if (y < 0 || y >= Hl) {
+        std::fill(o, o + size_t(Wl) * cdim, 0.f);
+        continue;
+      }
+      if (v.buf == -2) {  // the frames as the first layer sees them: bf16(x - 0.5)
+        for (int x = 0; x < Wl; ++x)
+          for (int ch = 0; ch < 3; ++ch)
+            o[x * 3 + ch] = bf16_value(in[((size_t(b) * 3 + ch) * Hl + y) * Wl + x] - 0.5f);
+      } else if (v.buf == -1) {
+        if (out_all.empty()) {
+          out_all.resize(plan->out_elems);
+          check_cuda(cudaMemcpy(out_all.data(), plan->out.p, out_all.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+        }
+        const int C = f.out_channels();
+        for (int ch = 0; ch < cdim; ++ch)
+          for (int x = 0; x < Wl; ++x)
+            o[size_t(x) * cdim + ch] = out_all[((size_t(b) * C + v.c_off + ch) * Hl + y) * Wl + x];
+      } else {
+        const int C = v.c_stride;
+        raw.resize(size_t(Wl) * C);
+        const size_t off = ((size_t(b) * g.Hp() + y + g.P) * g.Wp() + g.P) * C;
+        check_cuda(cudaMemcpy(raw.data(), plan->bufs[v.buf]->as<uint16_t>() + off, raw.size() * 2,
+                              cudaMemcpyDeviceToHost),
+                   "D2H row");
+        for (int x = 0; x < Wl; ++x)
+          for (int ch = 0; ch < cdim; ++ch)
+            o[size_t(x) * cdim + ch] = bf16_to_float(raw[size_t(x) * C + v.c_off + (map.empty() ? ch : map[ch])]);
+      }
+    }
+  };
+  const TensorView& vin = plan->layer_in[layer];
+  const TensorView& vout = plan->layer_out[layer];
+  const int in_level = vin.buf >= 0 ? vin.level : d.level;
+  const int out_level = vout.buf >= 0 ? vout.level : d.level;
+  // stage inputs: Caffe channel ci lives at window channel cin_map[ci] of the concat buffer
+  std::vector<int> map;
+  if (layer != 0 && !din.cin_map.empty() && vin.buf >= 0) map = din.cin_map;
+  rows(vin, in_level, din.cin, map, n_in, in_rows, layer_in);
+  rows(vout, out_level, d.cout, {}, n_out, out_rows, layer_out);
+  (void)s;
+}
+
 void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                       uint32_t w, const float* in, int layer, float* layer_in,
                       uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems) {
   const Model m = model_lookup(ctx, handle);
-  if (m.kind != AVEC_MODEL_POSENET) fail(AVEC_ERR_INVALID_ARGUMENT, "not a pose net");
-  int n_img = 0;
-  posenet_shape(m, n, c, h, w, n_img);
   const PoseFamily& f = m.net->fam;
-  if (layer < 0 || layer >= int(f.convs.size())) fail(AVEC_ERR_INVALID_ARGUMENT, "layer index");
-  const ConvDef& d = f.convs[layer];
   check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
   SlotLease lease(ctx);
   Slot* s = lease.slot();
-  Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
-  if (plan->layer_fusion[layer] == 2)
-    fail(AVEC_ERR_UNSUPPORTED, d.name + " is fused into the next layer: its output never leaves the SM");
+  int n_img = 0;
+  Plan* plan = run_to_layer(ctx, lease, m, n, c, h, w, in, layer, n_img);
+  const ConvDef& d = f.convs[layer];
   // a fused head's second layer sees the head's input (the first layer's input)
   const ConvDef& din = f.convs[plan->layer_in_from[layer]];
   // the output view is one level down when the layer's 2x2 pool is fused
@@ -1339,13 +1451,6 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
   const uint64_t need_out = uint64_t(n_img) * (int(h) >> out_level) * (int(w) >> out_level) * d.cout;
   if (layer_in_elems != need_in || layer_out_elems != need_out)
     fail(AVEC_ERR_INVALID_ARGUMENT, "layer buffers have the wrong size");
-  const uint64_t E = uint64_t(n) * c * h * w;
-  check_cuda(cudaMemcpy(plan->in.p, in, E * 4, cudaMemcpyHostToDevice), "H2D");
-  size_t last = 0;
-  for (size_t i = 0; i < plan->ops.size(); ++i)
-    if (plan->ops[i].layers[0] == layer || plan->ops[i].layers[1] == layer) last = i + 1;
-  run_ops(ctx, *plan, *m.net, 0, last, s->stream);
-  check_cuda(cudaStreamSynchronize(s->stream), "layer io sync");
   // `map`: Caffe channel -> channel inside the view's window (stage inputs)
   auto fetch = [&](const TensorView& v, int cdim, float* dst, const std::vector<int>& map) {
     const int lv = v.buf >= 0 ? v.level : d.level;

@@ -176,6 +176,10 @@ void posenet_layer_fusion(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c
                           int layer, int* kind, int* in_layer);
 int posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                             int layer);
+// selected rows (image, y) of a layer's input and output views, full-size parity
+void posenet_layer_rows(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                        const float* in, int layer, int n_in, const int32_t* in_rows, float* layer_in, int n_out,
+                        const int32_t* out_rows, float* layer_out);
 void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                       uint32_t w, const float* in, int layer, float* layer_in,
                       uint64_t layer_in_elems, float* layer_out, uint64_t layer_out_elems);

@@ -28,6 +28,18 @@ void check(int rc) {
 
 }  // namespace
 
+std::vector<FrameGroup> frame_groups(std::uint64_t frames, int groups) {
+  std::vector<FrameGroup> out;
+  if (groups < 1) return out;
+  std::uint64_t first = 0;
+  for (int g = 0; g < groups; ++g) {
+    const std::uint64_t n = frames / groups + (std::uint64_t(g) < frames % groups ? 1 : 0);
+    out.push_back({first, n});
+    first += n;
+  }
+  return out;
+}
+
 B200Backend::B200Backend(std::vector<int> devices, int slots_per_device, Policy policy)
     : slots_(slots_per_device < 1 ? 2 : slots_per_device), policy_(policy) {
   if (devices.empty()) {
@@ -126,13 +138,13 @@ double B200Backend::forward_into(ModelHandle model, const wire::Dims& d, const f
   // split: contiguous frame groups, one per GPU, concurrently
   const std::uint64_t per_frame_in = 3ull * d.height * d.width;
   const std::uint64_t per_frame_out = n_out / frames;
-  const int groups = int(std::min<std::uint64_t>(frames, G));
+  const auto part = frame_groups(frames, int(std::min<std::uint64_t>(frames, G)));
+  const int groups = int(part.size());
   std::vector<double> secs(groups, 0.0);
   std::vector<std::exception_ptr> errs(groups);
   std::vector<std::thread> th;
-  std::uint64_t f0 = 0;
   for (int g = 0; g < groups; ++g) {
-    const std::uint64_t nf = frames / groups + (std::uint64_t(g) < frames % groups ? 1 : 0);
+    const std::uint64_t f0 = part[g].first, nf = part[g].count;
     const wire::Dims sub{1, std::uint32_t(3 * nf), d.height, d.width};
     th.emplace_back([&, g, f0, nf, sub] {
       try {
@@ -142,7 +154,6 @@ double B200Backend::forward_into(ModelHandle model, const wire::Dims& d, const f
         errs[g] = std::current_exception();
       }
     });
-    f0 += nf;
   }
   for (auto& t : th) t.join();
   for (auto& ep : errs)
@@ -168,3 +179,13 @@ void* B200Backend::alloc_host(std::size_t bytes) {
 void B200Backend::free_host(void* p) { avec_host_free(p); }
 
 }  // namespace avec::backend
+
+extern "C" int avec_frame_groups(std::uint64_t frames, int groups, std::uint64_t* first, std::uint64_t* count) {
+  if (groups < 1 || !first || !count) return AVEC_ERR_INVALID_ARGUMENT;
+  const auto part = avec::backend::frame_groups(frames, groups);
+  for (int g = 0; g < groups; ++g) {
+    first[g] = part[g].first;
+    count[g] = part[g].count;
+  }
+  return AVEC_OK;
+}

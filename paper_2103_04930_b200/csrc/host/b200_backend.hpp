@@ -20,7 +20,19 @@
 
 struct avec_ctx;
 
+// exported by libavec_host.so for the Python mirror (sharding.py): the split
+// policy's partition of `frames` into `groups` (first[g], count[g])
+extern "C" int avec_frame_groups(std::uint64_t frames, int groups, std::uint64_t* first, std::uint64_t* count);
+
 namespace avec::backend {
+
+// Frame-group partition of the split policy (and of bench.py's ranks, through
+// avec_frame_groups): contiguous groups whose sizes differ by at most one,
+// earlier groups take the remainder.
+struct FrameGroup {
+  std::uint64_t first = 0, count = 0;
+};
+std::vector<FrameGroup> frame_groups(std::uint64_t frames, int groups);
 
 class B200Backend final : public Backend {
  public:

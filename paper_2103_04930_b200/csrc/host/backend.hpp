@@ -11,12 +11,10 @@
 //    dispatcher can keep every device busy while preserving FIFO dispatch.
 #pragma once
 
-#include <condition_variable>
 #include <cstdint>
 #include <map>
 #include <memory>
 #include <mutex>
-#include <set>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -49,30 +47,6 @@ struct ModelHandle {
   bool operator==(const ModelHandle&) const = default;
 };
 
-// FIFO admission for a single accelerator (reference backend.hpp:40-62)
-class FifoGate {
- public:
-  class Pass {
-   public:
-    explicit Pass(FifoGate* g) : g_(g) {}
-    Pass(Pass&& o) noexcept : g_(o.g_) { o.g_ = nullptr; }
-    Pass(const Pass&) = delete;
-    ~Pass() {
-      if (g_) g_->leave();
-    }
-
-   private:
-    FifoGate* g_;
-  };
-  Pass enter();
-
- private:
-  void leave();
-  std::mutex m_;
-  std::condition_variable cv_;
-  std::uint64_t next_ = 0, serving_ = 0;
-};
-
 class Backend {
  public:
   virtual ~Backend() = default;
@@ -97,17 +71,5 @@ class Backend {
   virtual void* alloc_host(std::size_t bytes);
   virtual void free_host(void* p);
 };
-
-// Emulation presets of the reference (backend.cpp:108-134) and the delay
-// wrapper (backend.cpp:138-174): each forward takes at least the preset's
-// per-frame time; the first registration per digest pays its load time.
-struct BackendProfile {
-  double per_frame_compute_s = 0;
-  double model_load_s = 0;
-  std::string label = "none";
-  bool is_zero() const { return per_frame_compute_s <= 0 && model_load_s <= 0; }
-};
-BackendProfile preset_profile(std::string_view name, std::string_view kind, double scale);
-std::shared_ptr<Backend> wrap_delay(std::shared_ptr<Backend> inner, BackendProfile profile);
 
 }  // namespace avec::backend

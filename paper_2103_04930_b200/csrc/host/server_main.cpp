@@ -89,12 +89,16 @@ int main(int argc, char** argv) {
     auto pol = policy == "split" ? backend::B200Backend::Policy::split
                                  : backend::B200Backend::Policy::affinity;
     if (policy != "split" && policy != "affinity") throw std::runtime_error("policy must be affinity or split");
-    auto profile = backend::preset_profile(preset, kind, scale);
-    if (gpu_s >= 0) profile.per_frame_compute_s = gpu_s * scale;
-    if (load_s >= 0) profile.model_load_s = load_s * scale;
+    // The reference's timing-emulation flags (server_main.cpp:25-43) are
+    // accepted so existing command lines parse, but this server runs the real
+    // network: an emulated device/edge/cloud delay has no meaning on it.
+    if (kind != "images" && kind != "video") throw std::runtime_error("unknown workload kind: " + kind);
+    if (!(scale > 0.0)) throw std::runtime_error("scale factor must be > 0");
+    if (preset != "none" || gpu_s > 0 || load_s > 0)
+      throw std::runtime_error("timing emulation (--preset/--gpu-s/--load-s) is not supported by the B200 "
+                               "server: it runs the network, use --preset none");
     std::shared_ptr<backend::Backend> be =
         std::make_shared<backend::B200Backend>(devs, int(slots), pol);
-    if (!profile.is_zero()) be = backend::wrap_delay(be, profile);
 
     server::ServerConfig cfg;
     cfg.limits.max_sessions = std::uint32_t(max_sessions);

@@ -1,10 +1,16 @@
 // TEST-ONLY: the product server (avec::server::Server) over a CPU stub backend,
 // so protocol/state-machine tests run on machines without a GPU. The stub
 // computes the reference's segment means (proj/src/backend.cpp:39-67) with a
-// plain loop; it is a test double (like the reference tests' MockPose /
-// wrap_delay), never linked into avec-server.
+// plain loop; it is a test double, never linked into avec-server.
+// --concurrency N makes it report N parallel workers (like GPUs x slots) and
+// --jitter-ms M sleeps a pseudo-random 0..M ms per forward so completions
+// interleave out of arrival order; --print-forward-log dumps
+// Server::forward_log() on shutdown for the FIFO check (harness.cpp:676-681).
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <csignal>
+#include <thread>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -17,6 +23,8 @@ namespace {
 
 class StubBackend final : public avec::backend::Backend {
  public:
+  StubBackend(int concurrency, int jitter_ms) : concurrency_(concurrency), jitter_ms_(jitter_ms) {}
+  int concurrency() const override { return concurrency_; }
   avec::backend::ModelHandle register_model(const avec::wire::ModelDescriptor& m) override {
     using avec::backend::Error;
     using avec::backend::ErrorCode;
@@ -41,7 +49,10 @@ class StubBackend final : public avec::backend::Backend {
       if (it == div_.end()) throw Error(ErrorCode::unknown_model, "handle was never issued by this backend");
       c = it->second;
     }
-    auto pass = gate_.enter();
+    if (jitter_ms_ > 0) {
+      const std::uint64_t r = (calls_.fetch_add(1) * 0x9E3779B97F4A7C15ull) >> 40;
+      std::this_thread::sleep_for(std::chrono::microseconds(r % (1000 * std::uint64_t(jitter_ms_))));
+    }
     const std::uint64_t e = f.data.size();
     const std::uint64_t k = std::uint64_t(std::llround(double(e) / c));
     if (k < 1 || k > e) throw Error(ErrorCode::degenerate_output, "degenerate output size");
@@ -61,8 +72,9 @@ class StubBackend final : public avec::backend::Backend {
   std::string_view label() const override { return "stub"; }
 
  private:
+  int concurrency_ = 1, jitter_ms_ = 0;
+  std::atomic<std::uint64_t> calls_{0};
   std::mutex m_;
-  avec::backend::FifoGate gate_;
   std::map<avec::wire::Digest, std::uint64_t> ids_;
   std::map<std::uint64_t, double> div_;
   std::uint64_t next_ = 1;
@@ -74,11 +86,23 @@ int main(int argc, char** argv) {
   std::string log;
   unsigned max_sessions = 16;
   unsigned long long max_model = 1ull << 30;
-  for (int i = 1; i + 1 < argc; i += 2) {
+  int concurrency = 1, jitter_ms = 0;
+  unsigned long long log_cap = 1ull << 20;
+  bool print_log = false;
+  for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
-    if (a == "--log") log = argv[i + 1];
+    if (a == "--print-forward-log") {
+      print_log = true;
+      continue;
+    }
+    if (i + 1 >= argc) break;
+    if (a == "--concurrency") concurrency = std::stoi(argv[i + 1]);
+    else if (a == "--jitter-ms") jitter_ms = std::stoi(argv[i + 1]);
+    else if (a == "--forward-log-cap") log_cap = std::stoull(argv[i + 1]);
+    else if (a == "--log") log = argv[i + 1];
     else if (a == "--max-sessions") max_sessions = std::stoul(argv[i + 1]);
     else if (a == "--max-model-bytes") max_model = std::stoull(argv[i + 1]);
+    ++i;
   }
   sigset_t set;
   sigemptyset(&set);
@@ -89,13 +113,25 @@ int main(int argc, char** argv) {
   cfg.log_path = log;
   cfg.limits.max_sessions = max_sessions;
   cfg.limits.max_model_bytes = max_model;
-  auto be = std::make_shared<StubBackend>();
+  cfg.forward_log_cap = log_cap;
+  auto be = std::make_shared<StubBackend>(concurrency, jitter_ms);
   avec::server::Server srv(be, cfg);
   const auto port = srv.listen("127.0.0.1", 0);
   std::printf("listening on 127.0.0.1:%u (backend %s)\n", port, std::string(be->label()).c_str());
   std::fflush(stdout);
   int sig = 0;
   sigwait(&set, &sig);
+  std::printf("shutting down (signal %d)\n", sig);
+  const std::size_t live_threads = srv.session_threads();  // before the drain joins them
   srv.shutdown();
+  if (print_log) {
+    std::printf("forward_log [");
+    const auto log_entries = srv.forward_log();
+    for (std::size_t i = 0; i < log_entries.size(); ++i)
+      std::printf("%s[%llu, %llu]", i ? ", " : "", (unsigned long long)log_entries[i].arrival_seq,
+                  (unsigned long long)log_entries[i].session_id);
+    std::printf("]\nsession_threads %zu\n", live_threads);
+  }
+  std::fflush(stdout);
   return 0;
 }

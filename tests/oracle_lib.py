@@ -38,6 +38,7 @@ def lib():
         L.oracle_bf16_round.argtypes = [ctypes.c_float]
         L.oracle_bf16_round.restype = ctypes.c_float
         L.oracle_conv2d_nhwc.argtypes = [f32p, i, i, i, i, f32p, f32p, i, i, i, f32p, i, f32p]
+        L.oracle_conv2d_rows.argtypes = [f32p, i, i, i, i, f32p, f32p, i, i, f32p, i, f32p]
         L.oracle_maxpool2_nhwc.argtypes = [f32p, i, i, i, i, f32p]
         L.oracle_upsample_plane.argtypes = [f32p, i, i, i, f32p]
         L.oracle_nms_plane.argtypes = [f32p, i, i, ctypes.c_float, i, i32p, f32p, f32p]
@@ -123,6 +124,24 @@ def conv2d_nhwc(x: np.ndarray, w: np.ndarray, b: np.ndarray, relu, round_bf16: b
     lib().oracle_conv2d_nhwc(np.ascontiguousarray(x, np.float32), n, h, wd, cin,
                              np.ascontiguousarray(w, np.float32), np.ascontiguousarray(b, np.float32),
                              cout, k, act, sl, int(round_bf16), out)
+    return out
+
+
+def conv2d_rows(win: np.ndarray, w: np.ndarray, b: np.ndarray, relu, round_bf16: bool,
+                slope: np.ndarray = None) -> np.ndarray:
+    """Selected output rows: win [rows][k][W][cin] (each row's k-row input
+    window, zeros outside the image) -> [rows][W][cout]; same arithmetic as
+    conv2d_nhwc (oracle_conv2d_rows)."""
+    r, k, wd, cin = win.shape
+    cout, cin2, k2, _ = w.shape
+    assert cin == cin2 and k == k2
+    act = int(relu)
+    sl = np.ascontiguousarray(slope if slope is not None else np.zeros(cout), np.float32)
+    out = np.empty((r, wd, cout), np.float32)
+    if r:
+        lib().oracle_conv2d_rows(np.ascontiguousarray(win, np.float32), r, k, wd, cin,
+                                 np.ascontiguousarray(w, np.float32), np.ascontiguousarray(b, np.float32),
+                                 cout, act, sl, int(round_bf16), out)
     return out
 
 

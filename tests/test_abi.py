@@ -61,3 +61,14 @@ def test_invalid_spec_is_invalid_model():
     with pytest.raises(AvecError) as e:
         synth_posenet_weights(b"avecnet 1\nfamily nope\n")
     assert e.value.name == "invalid_model"
+
+
+def test_host_library_exports_frame_groups():
+    """The split policy's partition is exported from the C++ host library
+    (b200_backend.hpp) and is what sharding.py binds."""
+    host = ROOT / "paper_2103_04930_b200" / "lib" / "libavec_host.so"
+    out = subprocess.run(["nm", "-D", "--defined-only", str(host)], capture_output=True, text=True,
+                         check=True).stdout
+    assert " T avec_frame_groups" in out
+    from paper_2103_04930_b200.sharding import frame_groups
+    assert frame_groups(32, 8) == [(4 * i, 4) for i in range(8)]

@@ -181,6 +181,36 @@ def test_reference_server_with_b200_plugin():
         srv.stop()
 
 
+def test_reference_server_b200_plugin_survives_bad_shape():
+    """A pose-net frame the engine rejects (367 rows: not divisible by 8) comes
+    from the client; through the shim it must surface as accelfwd::Error ->
+    ErrorMsg internal (server.cpp:313-318), not as an exception that escapes
+    the reference's session thread and terminates the server. A second
+    session afterwards still gets served."""
+    from paper_2103_04930_b200 import netspec
+    exe = ROOT / "oracle" / "_ref" / "ref_b200_server"
+    srv = W.ServerProc([str(exe)])
+    try:
+        s = netspec.spec()
+        for hgt, ok in ((367, False), (368, True)):
+            p = W.Peer(srv.port, timeout=120)
+            p.handshake()
+            p.send(W.model_upload(s, b"", netspec.COCO_DIVISOR, name=b"openpose"))
+            assert p.recv_msg()[0] == "model_ack"
+            data = np.zeros(3 * hgt * 64, np.float32)
+            p.send(W.frame_data(data) + W.resolution(64, hgt) + W.frame_size(data.size))
+            if ok:
+                tag, payload = p.recv_msg()
+                assert tag == "forward_result"
+                assert W.forward_result(payload)[1].size == 57 * (hgt // 8) * 8
+            else:
+                assert p.expect_error()[0] == W.WIRE_ERRORS["internal"]
+            p.close()
+        assert srv.p.poll() is None
+    finally:
+        srv.stop()
+
+
 def test_split_policy_server(tmp_path):
     srv = W.ServerProc([str(SERVER), "--policy", "split", "--slots", "1"])
     try:

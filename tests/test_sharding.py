@@ -1,7 +1,10 @@
 """N>1 path on CPU: world_size-2 gloo ranks shard a batched cycle into frame
-groups, each computes its slice, rank 0 assembles — the result must equal the
-unsharded computation bit for bit (the per-frame op here is the oracle's
-conv layer, standing in for the pose net whose frames are independent)."""
+groups with the PRODUCT partition (avec_frame_groups in libavec_host.so, the
+function B200Backend's split policy calls), each computes its slice, rank 0
+assembles; the result must equal the unsharded computation bit for bit (the
+per-frame op here is the oracle's conv layer, standing in for the pose net
+whose frames are independent; the GPU split itself is checked in
+tests/test_gpu_multi.py)."""
 import os
 import socket
 
@@ -10,7 +13,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2103_04930_b200.sharding import frame_groups, slices
+from paper_2103_04930_b200.sharding import frame_groups
 
 
 def test_frame_groups_cover_exactly():
@@ -80,6 +83,8 @@ def test_gloo_two_ranks_match_unsharded(n_frames):
     assert q.get(timeout=5) is True
 
 
-def test_slices_are_contiguous_output_ranges():
-    s = slices(8, 2, in_per_frame=3 * 368 * 656, out_per_frame=57 * 46 * 82)
-    assert s[0][1] == (0, 4 * 57 * 46 * 82) and s[1][1] == (4 * 57 * 46 * 82, 8 * 57 * 46 * 82)
+def test_frame_groups_are_batch_major_output_slices():
+    # C2 batch of 8 on 2 GPUs: each GPU's reply is one contiguous range of the output
+    per = 57 * 46 * 82
+    g = frame_groups(8, 2)
+    assert [(f * per, (f + n) * per) for f, n in g] == [(0, 4 * per), (4 * per, 8 * per)]
