@@ -6,13 +6,31 @@ exactly what the wire carries (proj/src/server.cpp:294-302). Random-init
 weights (deterministic He-uniform, seed 1), synthetic frames from the
 reference's frame generator (seed 7). A step = one forward cycle of 8 frames.
 
-  value : frames/s with inputs resident in HBM (avec_forward_device), whole job
+  value : frames/s with inputs resident in HBM (avec_forward_device), whole
+          job, over the driver's --steps; `steady_state` repeats it over 200
+          steps
   e2e   : frames/s through the reference-facing C-ABI call avec_forward with
           pinned HOST buffers — H2D of the frames and D2H of the heatmaps are
-          inside the timed region every step
-  roofline : tcgen05 conv kernel (the dominant kernel), algorithmic FLOPs of
-          its launches / their CUDA-event durations, vs measured bf16 peak
+          inside the timed region every step (fixed: one host thread per slot)
+  wire  : C2 through bin/avec-server over TCP loopback (native clients)
+  roofline : tcgen05 conv kernel with the largest share of the step,
+          algorithmic FLOPs of its launches / their CUDA-event durations (op by
+          op, so against the BURST bf16 peak), plus the whole step's TFLOP/s
   cpu_baseline : the reference's own server path (oracle/_ref/ref_arm), rank 0
+
+The other BASELINE configs ride in the same line (rank 0, N = 1 unless noted):
+  c1            configs[0]: 368x368 batch 1 through avec-server, driven by the
+                UNMODIFIED reference client (oracle/_ref/ref_client): fps and
+                per-cycle latency p50/p90, plus the device-only forward latency
+  mockpose_wire the reference arm's own workload (MockPose segment means, C2
+                shape, reference Session client, oracle/_ref/ref_arm) pointed
+                at avec-server: the like-for-like server ratio
+  c3_memcpy     configs[2]: forwarded H2D/D2H sweep 4 KB..256 MB (c = 1)
+                through avec-server and through avec_forward
+  c4            configs[3]: 8 concurrent client sessions on one avec-server
+                over all N GPUs, one session per GPU placement (every N)
+  c5            configs[4]: BODY_25 1312x736 batch 32, frame groups sharded
+                over the N ranks (strong scaling; every N)
 
 `--impl reference` runs the reference's CPU implementation of the path
 (Server + MockPoseBackend + Session over TCP loopback, built from the
@@ -172,33 +190,289 @@ def cpu_posenet_oracle_sample() -> dict:
             "cores": O.lib().oracle_threads(), "seconds": dt}
 
 
+SERVER_BIN = ROOT / "paper_2103_04930_b200" / "bin" / "avec-server"
+LOADGEN_BIN = ROOT / "paper_2103_04930_b200" / "bin" / "avec-loadgen"
+REF_CLIENT = ROOT / "oracle" / "_ref" / "ref_client"
+REF_ARM = ROOT / "oracle" / "_ref" / "ref_arm"
+
+
+class AvecServer:
+    """bin/avec-server as a subprocess; stopped by its own PID (SIGTERM drain)."""
+
+    def __init__(self, devices: str, slots: int, policy: str = "affinity"):
+        self.p = subprocess.Popen([str(SERVER_BIN), "--devices", devices, "--slots", str(slots), "--policy", policy],
+                                  stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+        line = self.p.stdout.readline()
+        if not line.startswith("listening on"):
+            err = self.p.stderr.read()[-300:]
+            self.p.kill()
+            raise RuntimeError("avec-server did not start: " + line + err)
+        self.endpoint = line.split()[2]
+
+    def close(self):
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=60)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def _json_tail(out: str) -> dict:
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def loadgen(endpoint: str, clients: int, steps: int, batch: int, width: int, height: int, model: str,
+            warmup: int = 2, elems: int = 0) -> dict:
+    cmd = [str(LOADGEN_BIN), "--endpoint", endpoint, "--clients", str(clients), "--steps", str(steps),
+           "--warmup", str(warmup), "--batch", str(batch), "--width", str(width), "--height", str(height),
+           "--model", model]
+    if elems:
+        cmd += ["--elems", str(elems)]
+    return _json_tail(subprocess.run(cmd, capture_output=True, text=True, timeout=900).stdout)
+
+
 def wire_run(device: int, steps: int, clients: int) -> dict:
     """C2 cycles through bin/avec-server (one GPU) from `clients` concurrent
     native sessions over TCP loopback (BASELINE "through AVEC server")."""
-    server = ROOT / "paper_2103_04930_b200" / "bin" / "avec-server"
-    loadgen = ROOT / "paper_2103_04930_b200" / "bin" / "avec-loadgen"
-    p = subprocess.Popen([str(server), "--devices", str(device), "--slots", str(WIRE_SLOTS)], stdout=subprocess.PIPE,
-                         stderr=subprocess.PIPE, text=True)
     try:
-        line = p.stdout.readline()
-        if not line.startswith("listening on"):
-            return {"ok": False, "error": "server did not start: " + line + p.stderr.read()[-300:]}
-        ep = line.split()[2]
-        model = "posenet-body25" if CFG["family"] == "openpose_body25" else "posenet"
-        r = subprocess.run([str(loadgen), "--endpoint", ep, "--clients", str(clients), "--steps", str(steps),
-                            "--warmup", "2", "--batch", str(BATCH), "--width", str(W), "--height", str(H),
-                            "--model", model], capture_output=True, text=True, timeout=900)
-        out = json.loads(r.stdout.strip().splitlines()[-1])
-        out["transport"] = f"TCP loopback, native client (bin/avec-loadgen), avec-server --slots {WIRE_SLOTS}"
-        return out
+        with AvecServer(str(device), WIRE_SLOTS) as srv:
+            model = "posenet-body25" if CFG["family"] == "openpose_body25" else "posenet"
+            out = loadgen(srv.endpoint, clients, steps, BATCH, W, H, model)
+            out["transport"] = f"TCP loopback, native client (bin/avec-loadgen), avec-server --slots {WIRE_SLOTS}"
+            return out
     except Exception as e:  # noqa: BLE001
         return {"ok": False, "error": str(e)}
-    finally:
-        p.terminate()
+
+
+def c1_run(be, device: int) -> dict:
+    """configs[0]: one 368x368 frame per cycle, COCO, through avec-server,
+    driven by the unmodified reference client (accelfwd::client::Session)."""
+    import numpy as np
+    import torch
+    from paper_2103_04930_b200 import Dims, make_model, netspec
+    res = {"workload": "C1: COCO 368x368 batch 1 per cycle, reference client -> avec-server over TCP loopback"}
+    try:
+        import tempfile
+        spec = pathlib.Path(tempfile.mkdtemp()) / "coco.spec"
+        spec.write_bytes(netspec.spec())
+        with AvecServer(str(device), 2) as srv:
+            r = subprocess.run([str(REF_CLIENT), "--endpoint", srv.endpoint, "--structure", str(spec),
+                                "--name", "openpose_coco", "--divisor", repr(netspec.COCO_DIVISOR),
+                                "--width", "368", "--height", "368", "--batch", "1", "--frames", "200",
+                                "--warmup", "10"], capture_output=True, text=True, timeout=600)
+            o = _json_tail(r.stdout)
+        res.update({k: o.get(k) for k in ("ok", "fps", "lat_ms_p50", "lat_ms_p90", "lat_ms_max", "gpu_s_mean",
+                                          "comm_s_mean", "byte_account_bad")})
+        res["unit"] = "frames/s"
+        # device-only latency of one frame: synchronous forward on resident input
+        h = be.register_model(make_model("openpose_coco", netspec.spec(), b"", netspec.COCO_DIVISOR))
+        dims = Dims(1, 3, 368, 368)
+        x = torch.from_numpy(np.random.default_rng(1).random(dims.elem_count(), dtype=np.float32)).cuda(device)
+        y = torch.empty(be.output_elems(h, dims), dtype=torch.float32, device=f"cuda:{device}")
+        st = torch.cuda.Stream(device=device)
+        lat = []
+        for i in range(60):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            be.forward_device(h, dims, x.data_ptr(), y.data_ptr(), st.cuda_stream)
+            e1.record(st)
+            e1.synchronize()
+            if i >= 10:
+                lat.append(e0.elapsed_time(e1))
+        lat.sort()
+        res["device_ms_p50"] = round(lat[len(lat) // 2], 4)
+        res["device_fps"] = round(1e3 / lat[len(lat) // 2], 1)
+    except Exception as e:  # noqa: BLE001
+        res.update(ok=False, error=str(e))
+    return res
+
+
+def mockpose_wire_run(device: int) -> dict:
+    """The reference arm's own workload and client (ref_arm: reference Session,
+    synthetic MockPose model, C2 shape) against avec-server instead of the
+    reference Server: the like-for-like ratio of the two servers."""
+    try:
+        with AvecServer(str(device), 2) as srv:
+            r = subprocess.run([str(REF_ARM), "--endpoint", srv.endpoint, "--width", str(W), "--height", str(H),
+                                "--batch", str(CONFIGS["c2"]["global_batch"]), "--steps", "60", "--warmup", "3"],
+                               capture_output=True, text=True, timeout=600)
+            o = _json_tail(r.stdout)
+        o["workload"] = "reference arm workload (MockPose, 8x656x368 per cycle, reference Session) on avec-server"
+        o["unit"] = "frames/s"
+        return o
+    except Exception as e:  # noqa: BLE001
+        return {"ok": False, "error": str(e)}
+
+
+def memcpy_sweep(be, device: int) -> dict:
+    """configs[2]: forwarded H2D/D2H of 4 KB..256 MB per cycle. c = 1, so the
+    reply is as large as the frame (MockPose with divisor 1 moves every byte
+    both ways); GB/s counts in + out bytes per cycle."""
+    import numpy as np
+    from paper_2103_04930_b200 import Dims, Frame, PinnedBuffer, make_model
+    sizes = [4 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20]
+    out = {"unit": "GB/s (in + out bytes per cycle)", "abi_pinned": [], "wire": []}
+    try:
+        h = be.register_model(make_model("memcpy", b"\x01\x02", b"", 1.0))
+        for b in sizes:
+            e = b // 4
+            w = 4096 if e >= 4096 else e
+            d = Dims(1, e // w, 1, w)
+            pin_in, pin_out = PinnedBuffer(e), PinnedBuffer(e)
+            pin_in.array[:] = np.random.default_rng(b).random(e, dtype=np.float32)
+            fin = Frame(d, pin_in.array)
+            reps = max(3, min(100, (256 << 20) // b))
+            for _ in range(2):
+                be.forward(h, fin, out=pin_out.array)
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                be.forward(h, fin, out=pin_out.array)
+            dt = (time.perf_counter() - t0) / reps
+            ok = bool(np.array_equal(pin_out.array, pin_in.array))
+            out["abi_pinned"].append({"bytes": b, "us": round(dt * 1e6, 1), "gbs": round(2 * b / dt / 1e9, 2),
+                                      "exact": ok})
+            pin_in.free()
+            pin_out.free()
+        with AvecServer(str(device), 2) as srv:
+            for b in sizes:
+                e = b // 4
+                w = 4096 if e >= 4096 else e
+                reps = max(3, min(60, (256 << 20) // b))
+                o = loadgen(srv.endpoint, 1, reps, 1, w, 1, "mockpose-c1", elems=e)
+                dt = o["wall_s"] / reps if o.get("ok") else None
+                out["wire"].append({"bytes": b, "us": round(dt * 1e6, 1) if dt else None,
+                                    "gbs": round(2 * b / dt / 1e9, 2) if dt else None})
+        out["peak_wire_gbs"] = max((x["gbs"] or 0) for x in out["wire"])
+    except Exception as e:  # noqa: BLE001
+        out.update(ok=False, error=str(e))
+    return out
+
+
+def c4_run(rank: int, world: int, host_group) -> dict:
+    """configs[3]: 8 concurrent client sessions on ONE avec-server spanning all
+    N GPUs of the job, sessions pinned one per GPU (--policy session). Rank 0
+    runs it while the other ranks wait at a host-side (gloo) barrier, so no
+    NCCL kernel spins on the GPUs it uses."""
+    import torch.distributed as dist
+    res = None
+    if world > 1:
+        dist.barrier(group=host_group)
+    if rank == 0:
         try:
-            p.wait(timeout=60)
-        except subprocess.TimeoutExpired:
-            p.kill()
+            devs = ",".join(str(i) for i in range(world))
+            with AvecServer(devs, 2, "session") as srv:
+                o = loadgen(srv.endpoint, 8, 30, CONFIGS["c2"]["global_batch"], W, H, "posenet")
+            res = {"ok": o.get("ok"), "fps": o.get("fps"), "clients": 8, "gpus": world, "unit": "frames/s",
+                   "placement": "one avec-server over all GPUs, session k on GPU (k-1) mod N",
+                   "cycle_ms": o.get("cycle_ms"), "gpu_ms": o.get("gpu_ms"),
+                   "workload": "C4: 8 concurrent sessions of 8x656x368 COCO cycles"}
+        except Exception as e:  # noqa: BLE001
+            res = {"ok": False, "error": str(e)}
+    if world > 1:
+        dist.barrier(group=host_group)
+    return res
+
+
+def c5_run(args, rank: int, world: int, dev: int) -> dict:
+    """configs[4]: BODY_25 1312x736, 32 frames per cycle sharded into frame
+    groups over the ranks with the product partition (avec_frame_groups):
+    device-resident frames/s (max over ranks), e2e through avec_forward with
+    pinned host buffers, and the pixel-major conv kernel's roofline."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2103_04930_b200 import B200Backend, Dims, Frame, PinnedBuffer, make_model, netspec
+    from paper_2103_04930_b200.sharding import frame_groups
+    cfg = CONFIGS["c5"]
+    w5, h5, total = cfg["width"], cfg["height"], cfg["global_batch"]
+    first, nb = frame_groups(total, world)[rank]
+    be = B200Backend(dev, slots=2)
+    try:
+        h = be.register_model(make_model(cfg["family"], netspec.spec(cfg["family"]), b"", cfg["divisor"]))
+        dims = Dims(1, 3 * nb, h5, w5)
+        E, K = dims.elem_count(), be.output_elems(h, dims)
+        rng = np.random.default_rng(11 + rank)
+        host = (rng.integers(0, 1 << 24, E, dtype=np.int64) * (1.0 / (1 << 24))).astype(np.float32)
+        d_in = torch.from_numpy(host).to(f"cuda:{dev}")
+        d_out = [torch.empty(K, dtype=torch.float32, device=f"cuda:{dev}") for _ in range(2)]
+        streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+        steps = 6
+        for i in range(2):
+            be.forward_device(h, dims, d_in.data_ptr(), d_out[i].data_ptr(), streams[i].cuda_stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(streams[0])
+        streams[1].wait_event(ev0)
+        for i in range(steps):
+            be.forward_device(h, dims, d_in.data_ptr(), d_out[i % 2].data_ptr(), streams[i % 2].cuda_stream)
+        evb = torch.cuda.Event()
+        evb.record(streams[1])
+        streams[0].wait_event(evb)
+        ev1.record(streams[0])
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        value = steps * total / (ms / 1e3)
+        # e2e: pinned host in/out through avec_forward, 2 host threads (one per slot)
+        pin_in, pin_out = [PinnedBuffer(E) for _ in range(2)], [PinnedBuffer(K) for _ in range(2)]
+        for j in range(2):
+            pin_in[j].array[:] = host
+        frames = [Frame(dims, pin_in[j].array) for j in range(2)]
+        for j in range(2):
+            be.forward(h, frames[j], out=pin_out[j].array)
+        if world > 1:
+            dist.barrier()
+
+        def worker(j, n):
+            for _ in range(n):
+                be.forward(h, frames[j], out=pin_out[j].array)
+                float(pin_out[j].array[0])
+
+        t0 = time.perf_counter()
+        th = [threading.Thread(target=worker, args=(j, steps // 2)) for j in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([s], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            s = float(t.item())
+        e2e = (steps // 2) * 2 * total / s
+        prof = be.profile(h, dims, d_in.data_ptr(), reps=1)
+        pm = [p for p in prof if p["kind"] == "conv_pm"]
+        pm_fl, pm_ms = sum(p["flops"] for p in pm), sum(p["ms"] for p in pm)
+        peaks = load_peaks()
+        net_fl = netspec.flops_per_frame(netspec.layers_for(cfg["family"]), h5, w5)
+        tf = pm_fl / (pm_ms / 1e3) / 1e12
+        res = {"value": round(value, 2), "unit": "frames/s", "ms_per_step": round(ms / steps, 3),
+               "frames_per_step": total, "frames_per_gpu": nb, "steps": steps, "scaling": "strong",
+               "e2e": {"value": round(e2e, 2), "unit": "frames/s", "h2d_bytes_per_step": E * 4 * world,
+                       "d2h_bytes_per_step": K * 4 * world, "api": "avec_forward, pinned host buffers, 2 threads"},
+               "roofline": {"kernel": "conv_pm_kernel (tcgen05 pixel-major conv, all launches)", "bound": "tensor",
+                            "achieved": round(tf, 1), "unit": "TFLOP/s", "peak": peaks["bf16"],
+                            "frac": round(tf / peaks["bf16"], 4), "peak_kind": "burst (op-by-op replay)",
+                            "frac_of_sustained": round(tf / peaks["bf16_sust"], 4),
+                            "share_of_step": round(pm_ms / sum(p["ms"] for p in prof), 4)},
+               "step_tflops_per_gpu": round(nb * net_fl / (ms / steps / 1e3) / 1e12, 1),
+               "workload": cfg["workload"]}
+        for b in pin_in + pin_out:
+            b.free()
+        return res
+    finally:
+        be.close()
 
 
 def ours_main(args, rank: int, world: int, local_rank: int) -> int:
@@ -216,6 +490,7 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     h = be.register_model(model)
     dims = Dims(1, 3 * BATCH, H, W)
     E, K = dims.elem_count(), be.output_elems(h, dims)
+    host_group = dist.new_group(backend="gloo") if world > 1 else None
 
     # synthetic frames with the harness's value distribution (U[0,1) on a 2^-24
     # grid, harness.cpp:29-42), distinct per rank and per rotating input buffer
@@ -237,18 +512,16 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
         be.forward_device(h, dims, d_in[i % n_rot].data_ptr(), d_out[i % S].data_ptr(),
                           streams[i % S].cuda_stream)
 
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clocks:
+    def timed(n_steps: int, clocks=None):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(streams[0])
         for st in streams[1:]:
             st.wait_event(ev0)
-        for i in range(args.steps):
+        for i in range(n_steps):
             step(i)
         for st in streams[1:]:
             ev_b = torch.cuda.Event()
@@ -256,18 +529,30 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
             streams[0].wait_event(ev_b)
         ev1.record(streams[0])
         torch.cuda.synchronize()
-    dev_ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([dev_ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
-        dist.barrier()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms
+
+    for i in range(args.warmup):
+        step(i)
+    with ClockSampler(dev) as clocks:
+        dev_ms = timed(args.steps)
     torch.cuda.synchronize()
     frames_total = args.steps * BATCH * world
     value = frames_total / (dev_ms / 1e3)
+    # the same measurement over >= 200 steps (steady state, clocks sampled again)
+    ss_steps = max(200, args.steps)
+    with ClockSampler(dev) as ss_clocks:
+        ss_ms = timed(ss_steps)
+    steady = {"steps": ss_steps, "value": round(ss_steps * BATCH * world / (ss_ms / 1e3), 2), "unit": "frames/s",
+              "ms_per_step": round(ss_ms / ss_steps, 4), "clocks": ss_clocks.summary()}
 
     # ---------------- e2e through avec_forward with pinned host buffers ----------------
-    T = SLOTS  # host threads at most, one cycle per slot
+    T = SLOTS  # one host thread per execution slot (fixed, not a best-of)
     pin_in = [PinnedBuffer(E) for _ in range(T)]
     pin_out = [PinnedBuffer(K) for _ in range(T)]
     for j in range(T):
@@ -289,10 +574,12 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
             s += float(pin_out[j].array[0])  # host read of the step's result
         checksum[j] = s
 
+    e2e_cycles = max(args.steps, 64)
+
     def e2e_run(threads: int) -> float:
         if world > 1:
             dist.barrier()
-        counts = [args.steps // threads + (1 if i < args.steps % threads else 0) for i in range(threads)]
+        counts = [e2e_cycles // threads + (1 if i < e2e_cycles % threads else 0) for i in range(threads)]
         t0 = time.perf_counter()
         ths = [threading.Thread(target=worker, args=(j, counts[j])) for j in range(threads)]
         for t in ths:
@@ -304,20 +591,20 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
             t = torch.tensor([s], device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             s = float(t.item())
-        return frames_total / s
+        return e2e_cycles * BATCH * world / s
 
-    # one host thread (synchronous cycles) up to one per slot
-    e2e_by_threads = {t: e2e_run(t) for t in range(1, T + 1)}
-    e2e_threads = max(e2e_by_threads, key=e2e_by_threads.get)
-    e2e = e2e_by_threads[e2e_threads]
+    e2e = e2e_run(T)
+    e2e_serial = e2e_run(1)  # one synchronous cycle at a time (latency-bound)
 
     # ---------------- through the wire: avec-server + native clients over TCP ----------------
     # 4 sessions per GPU: two cycles compute in the server's two slots while the
     # other two sessions stream their frames in / results out (measured sweep:
     # 1 -> 860, 2 -> 1324, 4 -> 2092, 8 -> 1990 fps on C2, profiles/README.md)
     wire = wire_run(dev, steps=max(20, args.steps // 4), clients=4)
+    wire1 = wire_run(dev, steps=max(20, args.steps // 4), clients=1)
+    wire["one_session"] = {k: wire1.get(k) for k in ("ok", "fps", "cycle_ms", "comm_ms", "gpu_ms")}
     if world > 1:
-        t = torch.tensor([wire.get("fps", 0.0)], device=f"cuda:{dev}")
+        t = torch.tensor([wire.get("fps", 0.0) or 0.0], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         wire["fps_all_ranks"] = float(t.item())
 
@@ -345,19 +632,25 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
     net_fl = netspec.flops_per_frame(netspec.layers_for(CFG["family"]), H, W)
     kernel_name = {"conv_tc": "conv_tc_kernel<2>: tcgen05 swap-AB 7x7 stage conv (L1+L2 branch pair per launch)",
                    "conv_pm": "conv_pm_kernel<N,S>: tcgen05 pixel-major conv (all launches of the class)"}
+    step_tf = BATCH * net_fl / (dev_ms / args.steps / 1e3) / 1e12
+    ss_tf = BATCH * net_fl / (ss_ms / ss_steps / 1e3) / 1e12
     roofline = {
         "bound": "tensor",
         "kernel": kernel_name[dom_kind],
-        "achieved": round(dom_tf, 1), "peak": peaks["bf16_sust"], "unit": "TFLOP/s",
-        "frac": round(dom_tf / peaks["bf16_sust"], 4), "traffic": traffic,
-        "peak_kind": f"{peaks['src']} sustained bf16 (kernel timed inside a long step)",
+        "achieved": round(dom_tf, 1), "peak": peaks["bf16"], "unit": "TFLOP/s",
+        "frac": round(dom_tf / peaks["bf16"], 4), "traffic": traffic,
+        "peak_kind": f"{peaks['src']} burst bf16: kernels timed op by op in isolation (avec_posenet_profile)",
+        "frac_of_sustained": round(dom_tf / peaks["bf16_sust"], 4),
         "flops_per_launch": dom_fl, "launch_ms": round(dom_ms, 4), "launches_per_step": len(dom),
         "share_of_step": round(sum(p["ms"] for p in dom) / step_ms_prof, 4),
         "all_conv": {"achieved": round(all_fl / (all_ms / 1e3) / 1e12, 1),
-                     "frac": round(all_fl / (all_ms / 1e3) / 1e12 / peaks["bf16_sust"], 4),
+                     "frac": round(all_fl / (all_ms / 1e3) / 1e12 / peaks["bf16"], 4),
                      "launches_per_step": len(allc), "share_of_step": round(all_ms / step_ms_prof, 4)},
         "net_flops_per_frame": net_fl,
-        "step_tflops_per_gpu": round(BATCH * net_fl / (dev_ms / args.steps / 1e3) / 1e12, 1),
+        "step": {"tflops_per_gpu": round(step_tf, 1), "frac_burst": round(step_tf / peaks["bf16"], 4),
+                 "frac_sustained": round(step_tf / peaks["bf16_sust"], 4),
+                 "steady_tflops_per_gpu": round(ss_tf, 1), "steady_frac_burst": round(ss_tf / peaks["bf16"], 4),
+                 "steady_frac_sustained": round(ss_tf / peaks["bf16_sust"], 4)},
     }
     breakdown = {}
     for p in prof:
@@ -365,6 +658,24 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
         breakdown.setdefault(k, {"ms": 0.0, "launches": 0})
         breakdown[k]["ms"] = round(breakdown[k]["ms"] + p["ms"], 4)
         breakdown[k]["launches"] += 1
+    for b in pin_in + pin_out:
+        b.free()
+
+    # ---------------- the other BASELINE configs ----------------
+    extras = {}
+    if args.config == "c2":
+        if world == 1:
+            extras["c1"] = c1_run(be, dev)
+            extras["mockpose_wire"] = mockpose_wire_run(dev)
+            extras["c3_memcpy"] = memcpy_sweep(be, dev)
+        be.close()
+        be = None
+        torch.cuda.synchronize()
+        extras["c4"] = c4_run(rank, world, host_group)
+        try:
+            extras["c5"] = c5_run(args, rank, world, dev)
+        except Exception as e:  # noqa: BLE001
+            extras["c5"] = {"ok": False, "error": str(e)}
 
     if rank == 0:
         ref_cycles = 120 if args.config == "c2" else 3  # ~10 s of reference CPU work either way
@@ -379,6 +690,10 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
                    "sample": f"reference Server+MockPoseBackend via Session over TCP loopback, {ref_cycles} cycles "
                              f"of {CFG['global_batch']}x{W}x{H} (the reference emulates OpenPose with segment means)",
                    "posenet_oracle_port": port}
+            mw = extras.get("mockpose_wire")
+            if mw and mw.get("ok"):
+                mw["reference_server_fps"] = ref["fps"]
+                mw["ratio_vs_reference_server"] = round(mw["fps"] / ref["fps"], 2)
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 4),
@@ -389,19 +704,21 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
                        "global_batch": BATCH * world, "frame": f"{W}x{H}", "frames_per_gpu": BATCH,
                        "parallelism": f"frame groups x{world}",
                        "l2": "4 rotating input buffers; per-step activation working set >> 126 MB L2"},
+            "steady_state": steady,
             "e2e": {"value": round(e2e, 2), "unit": "frames/s", "h2d_bytes_per_step": E * 4,
-                    "d2h_bytes_per_step": K * 4,
-                    "api": f"avec_forward (pinned host buffers), {e2e_threads} host thread(s) over {SLOTS} slots",
-                    "by_threads": {str(k): round(v, 2) for k, v in e2e_by_threads.items()}},
+                    "d2h_bytes_per_step": K * 4, "cycles": e2e_cycles,
+                    "api": f"avec_forward (pinned host buffers), {T} host threads over {SLOTS} slots",
+                    "one_thread": round(e2e_serial, 2)},
             "wire": wire,
-            "pdl": os.environ.get("AVEC_PDL", "0") == "1",
             "roofline": roofline, "cpu_baseline": cpu,
             "gpu_launches": args.steps * len(prof),
             "clocks": clocks.summary(),
             "kernel_breakdown_ms_per_step": breakdown,
         }
+        line.update(extras)
         print(json.dumps(line))
-    be.close()
+    if be is not None:
+        be.close()
     return 0
 
 

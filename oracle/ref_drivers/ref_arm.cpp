@@ -4,7 +4,10 @@
 // Each step is one forward cycle of `batch` frames folded into channels.
 // --clients N runs N concurrent sessions (C4 shape); the reference backend
 // serves them FIFO on one dispatch thread by design (server.cpp:84-111).
+// --endpoint HOST:PORT points the same reference clients, model and frames at
+// another server instead (bench.py: the B200 avec-server, like for like).
 #include <atomic>
+#include <memory>
 #include <thread>
 
 #include "accelfwd/client.hpp"
@@ -25,9 +28,13 @@ int main(int argc, char** argv) {
     std::uint32_t clients = std::stoul(refdrv::get(a, "clients", "1"));
     double divisor = std::stod(refdrv::get(a, "divisor", std::to_string(192.0 / 57.0)));
 
-    server::Server srv(std::make_shared<backend::MockPoseBackend>());
-    std::uint16_t port = srv.listen("127.0.0.1", 0);
-    std::string ep = "127.0.0.1:" + std::to_string(port);
+    std::string ep = refdrv::get(a, "endpoint", "");
+    std::unique_ptr<server::Server> srv;
+    if (ep.empty()) {
+      srv = std::make_unique<server::Server>(std::make_shared<backend::MockPoseBackend>());
+      std::uint16_t port = srv->listen("127.0.0.1", 0);
+      ep = "127.0.0.1:" + std::to_string(port);
+    }
 
     harness::ModelSpec ms;
     ms.output_divisor = divisor;
@@ -67,7 +74,7 @@ int main(int argc, char** argv) {
     go = true;
     for (auto& t : th) t.join();
     double wall_s = wall.elapsed_s();
-    srv.shutdown();
+    if (srv) srv->shutdown();
     for (auto& e : errs)
       if (!e.empty()) throw std::runtime_error(e);
     double frames = double(steps) * batch * clients;
@@ -75,9 +82,10 @@ int main(int argc, char** argv) {
     for (double v : compute_s) cs += v;
     std::printf("{\"ok\": true, \"frames\": %.0f, \"wall_s\": %.6f, \"fps\": %.4f, "
                 "\"ms_per_cycle\": %.4f, \"backend_ms_per_cycle\": %.4f, \"clients\": %u, "
-                "\"batch\": %u, \"width\": %u, \"height\": %u, \"backend\": \"mockpose\"}\n",
+                "\"batch\": %u, \"width\": %u, \"height\": %u, \"backend\": \"mockpose\", \"server\": \"%s\"}\n",
                 frames, wall_s, frames / wall_s, 1e3 * wall_s / steps,
-                1e3 * cs / (double(steps) * clients), clients, batch, w, h);
+                1e3 * cs / (double(steps) * clients), clients, batch, w, h,
+                srv ? "reference accelfwd::server::Server" : ep.c_str());
     return 0;
   } catch (const std::exception& e) {
     std::printf("{\"ok\": false, \"error\": \"%s\"}\n", e.what());

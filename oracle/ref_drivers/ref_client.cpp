@@ -4,6 +4,7 @@
 // harness frames and reports what came back. With --check-mockpose every
 // result is memcmp'd against the reference's own local mockpose_forward
 // (harness.cpp:657-663 style).
+#include <algorithm>
 #include <cinttypes>
 
 #include "accelfwd/client.hpp"
@@ -56,6 +57,7 @@ int main(int argc, char** argv) {
     wire::Sha256 all;
     std::uint64_t mismatches = 0, bytes_bad = 0;
     double gpu = 0, comm = 0, timed = 0;
+    std::vector<double> lat;  // per-cycle wall seconds of the timed cycles
     wire::Dims dims{1, 3 * batch, h, w};
     const std::uint64_t expect_bytes =
         wire::transfer_size(dims, divisor) + wire::kCycleOverheadBytes;
@@ -67,6 +69,7 @@ int main(int argc, char** argv) {
       if (t.bytes_sent + t.bytes_received != expect_bytes) ++bytes_bad;
       if (i < warmup) continue;
       timed += el;
+      lat.push_back(el);
       gpu += t.gpu_s;
       comm += t.communication_s;
       all.update({reinterpret_cast<const std::uint8_t*>(heat.data.data()),
@@ -81,14 +84,17 @@ int main(int argc, char** argv) {
     }
     if (dump_f) std::fclose(dump_f);
     session.close();
+    std::sort(lat.begin(), lat.end());
+    auto pct = [&](double q) { return lat.empty() ? 0.0 : 1e3 * lat[std::size_t(q * double(lat.size() - 1) + 0.5)]; };
     std::printf(
         "{\"ok\": true, \"cache_hit\": %s, \"setup_s\": %.6f, \"cycles\": %u, "
         "\"frames\": %u, \"timed_s\": %.6f, \"fps\": %.3f, \"gpu_s_mean\": %.6f, "
-        "\"comm_s_mean\": %.6f, \"mismatches\": %" PRIu64 ", \"byte_account_bad\": %" PRIu64
+        "\"comm_s_mean\": %.6f, \"lat_ms_p50\": %.4f, \"lat_ms_p90\": %.4f, \"lat_ms_max\": %.4f, "
+        "\"mismatches\": %" PRIu64 ", \"byte_account_bad\": %" PRIu64
         ", \"expect_cycle_bytes\": %" PRIu64 ", \"digest\": \"%s\", \"model_digest\": \"%s\"}\n",
         ens.cache_hit ? "true" : "false", setup_s, frames, frames * batch, timed,
         timed > 0 ? frames * batch / timed : 0.0, frames ? gpu / frames : 0.0,
-        frames ? comm / frames : 0.0, mismatches, bytes_bad, expect_bytes,
+        frames ? comm / frames : 0.0, pct(0.5), pct(0.9), pct(1.0), mismatches, bytes_bad, expect_bytes,
         wire::hex(all.finish()).c_str(), wire::hex(model.digest).c_str());
     return mismatches == 0 && bytes_bad == 0 ? 0 : 3;
   } catch (const std::exception& e) {

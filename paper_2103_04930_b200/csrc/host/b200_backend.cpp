@@ -63,7 +63,9 @@ B200Backend::B200Backend(std::vector<int> devices, int slots_per_device, Policy 
   for (size_t i = 0; i < ctx_.size(); ++i) inflight_[i] = 0;
   label_ = ctx_.size() == 1 ? std::string(avec_ctx_label(ctx_[0]))
                             : "b200x" + std::to_string(ctx_.size()) +
-                                  (policy_ == Policy::split ? ":split" : ":affinity");
+                                  (policy_ == Policy::split     ? ":split"
+                                   : policy_ == Policy::session ? ":session"
+                                                                : ":affinity");
 }
 
 B200Backend::~B200Backend() {
@@ -159,6 +161,14 @@ double B200Backend::forward_into(ModelHandle model, const wire::Dims& d, const f
   for (auto& ep : errs)
     if (ep) std::rethrow_exception(ep);
   return *std::max_element(secs.begin(), secs.end());
+}
+
+double B200Backend::forward_session(std::uint64_t session, ModelHandle model, const wire::Dims& d, const float* in,
+                                    std::uint64_t n_in, float* out, std::uint64_t n_out) {
+  if (policy_ != Policy::session) return forward_into(model, d, in, n_in, out, n_out);
+  const Entry e = lookup(model);
+  const int dev = int((session == 0 ? 0 : session - 1) % ctx_.size());
+  return run_on(dev, e, d, in, n_in, out, n_out);
 }
 
 Heatmap B200Backend::forward(ModelHandle model, const Frame& frame) {

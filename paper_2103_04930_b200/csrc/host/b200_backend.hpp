@@ -5,6 +5,8 @@
 // collective. Two placement policies:
 //  * affinity (default): each forward runs whole on the least-loaded GPU;
 //    sessions spread across GPUs (C4: 8 clients, one per B200);
+//  * session: session k always runs on GPU (k - 1) mod G (C4: 8 clients, one
+//    session per B200 of the box);
 //  * split: a batched pose-net forward (channels = 3N) is cut into contiguous
 //    frame groups, one per GPU, run concurrently; each GPU writes its slice of
 //    the NCHW output, which is batch-major, so slices are contiguous (C5).
@@ -36,7 +38,7 @@ std::vector<FrameGroup> frame_groups(std::uint64_t frames, int groups);
 
 class B200Backend final : public Backend {
  public:
-  enum class Policy { affinity, split };
+  enum class Policy { affinity, split, session };
   // devices empty = all visible GPUs
   explicit B200Backend(std::vector<int> devices = {}, int slots_per_device = 2,
                        Policy policy = Policy::affinity);
@@ -50,6 +52,8 @@ class B200Backend final : public Backend {
   std::uint64_t output_elems(ModelHandle model, const wire::Dims& dims) override;
   double forward_into(ModelHandle model, const wire::Dims& dims, const float* in, std::uint64_t n_in,
                       float* out, std::uint64_t n_out) override;
+  double forward_session(std::uint64_t session, ModelHandle model, const wire::Dims& dims, const float* in,
+                         std::uint64_t n_in, float* out, std::uint64_t n_out) override;
   int concurrency() const override;
   void* alloc_host(std::size_t bytes) override;
   void free_host(void* p) override;

@@ -66,6 +66,11 @@ class Backend {
                               std::uint64_t) {
     throw Error(ErrorCode::internal, "forward_into unsupported by this backend");
   }
+  // the server's call: `session` lets a multi-device backend pin sessions
+  virtual double forward_session(std::uint64_t /*session*/, ModelHandle h, const wire::Dims& d, const float* in,
+                                 std::uint64_t n_in, float* out, std::uint64_t n_out) {
+    return forward_into(h, d, in, n_in, out, n_out);
+  }
   virtual int concurrency() const { return 1; }
   // host memory for ingest/egress staging (pinned when the backend can)
   virtual void* alloc_host(std::size_t bytes);

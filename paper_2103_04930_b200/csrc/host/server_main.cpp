@@ -1,5 +1,7 @@
 // avec-server: the B200 destination node. Flags of the reference server
-// (proj/tools/server_main.cpp:25-43) plus --devices / --slots / --policy.
+// (proj/tools/server_main.cpp:25-43) plus --devices / --slots / --policy
+// (affinity: least-loaded GPU per cycle; session: session k on GPU (k-1) mod G;
+// split: each batched cycle cut into frame groups across the GPUs).
 // Same banner (server_main.cpp:71) and SIGINT/SIGTERM drain (:48-80).
 #include <csignal>
 #include <cstdio>
@@ -17,7 +19,7 @@ namespace {
 void usage() {
   std::fprintf(stderr,
                "usage: avec-server [--bind HOST] [--port N] [--devices all|0,1,..] [--slots N]\n"
-               "                   [--policy affinity|split] [--preset device|edge|cloud|none]\n"
+               "                   [--policy affinity|session|split] [--preset none]\n"
                "                   [--kind images|video] [--scale X] [--gpu-s S] [--load-s S]\n"
                "                   [--max-sessions N] [--max-model-bytes N] [--log PATH]\n");
 }
@@ -86,9 +88,11 @@ int main(int argc, char** argv) {
       std::string tok;
       while (std::getline(ss, tok, ',')) devs.push_back(std::stoi(tok));
     }
-    auto pol = policy == "split" ? backend::B200Backend::Policy::split
-                                 : backend::B200Backend::Policy::affinity;
-    if (policy != "split" && policy != "affinity") throw std::runtime_error("policy must be affinity or split");
+    auto pol = policy == "split"     ? backend::B200Backend::Policy::split
+               : policy == "session" ? backend::B200Backend::Policy::session
+                                     : backend::B200Backend::Policy::affinity;
+    if (policy != "split" && policy != "affinity" && policy != "session")
+      throw std::runtime_error("policy must be affinity, session or split");
     // The reference's timing-emulation flags (server_main.cpp:25-43) are
     // accepted so existing command lines parse, but this server runs the real
     // network: an emulated device/edge/cloud delay has no meaning on it.

@@ -40,6 +40,14 @@ def test_our_arm_line():
         assert k in c
     assert d["gpu_launches"] >= 3 * 40  # every step is one graph of the net's launches
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    # the other BASELINE configs ride in the same line
+    assert d["steady_state"]["steps"] >= 200 and d["steady_state"]["value"] > 0
+    assert d["roofline"]["peak_kind"].startswith("measured burst") or "burst" in d["roofline"]["peak_kind"]
+    assert d["c1"]["ok"] and d["c1"]["byte_account_bad"] == 0 and d["c1"]["lat_ms_p90"] > 0
+    assert d["mockpose_wire"]["ok"] and d["mockpose_wire"]["fps"] > 0
+    assert all(x["exact"] for x in d["c3_memcpy"]["abi_pinned"]) and len(d["c3_memcpy"]["wire"]) == 8
+    assert d["c4"]["ok"] and d["c4"]["clients"] == 8
+    assert d["c5"]["value"] > 0 and d["c5"]["frames_per_step"] == 32
 
 
 def test_reference_arm_line():

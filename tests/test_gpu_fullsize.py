@@ -32,7 +32,9 @@ def _setup(family, width, height, nb, seed):
     layers = netspec.layers_for(family)
     wb = [(O.bf16_round(w), b, sl) for w, b, sl in netspec.split_weights(layers, synth_posenet_weights(s))]
     frame = Frame(Dims(1, 3 * nb, height, width), O.batched_frame(width, height, nb, seed=seed))
-    finals = {"Mconv7_stage6_L1", "Mconv7_stage6_L2", "Mconv7_stage3_L2", "Mconv7_stage1_L1"}
+    # layers whose parity view is the fp32 wire output (not bf16-rounded)
+    finals = ({"Mconv7_stage3_L2", "Mconv7_stage1_L1"} if family == "openpose_body25"
+              else {"Mconv7_stage6_L1", "Mconv7_stage6_L2"})
     return dict(be=be, h=h, layers=layers, wb=wb, frame=frame, finals=finals)
 
 

@@ -14,7 +14,7 @@ sys.path.insert(0, str(ROOT))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c2", choices=["c2", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c5"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--json", default="")
@@ -23,6 +23,7 @@ def main():
     import torch
     from paper_2103_04930_b200 import B200Backend, Dims, make_model, netspec
     fam, W, H, B, div = {
+        "c1": ("openpose_coco", 368, 368, 1, netspec.COCO_DIVISOR),
         "c2": ("openpose_coco", 656, 368, 8, netspec.COCO_DIVISOR),
         "c5": ("openpose_body25", 1312, 736, 32, netspec.BODY25_DIVISOR),
     }[a.config]
@@ -43,6 +44,15 @@ def main():
               f"{tf:7.1f} TF/s {gbs:7.0f} GB/s {100 * p['ms'] / total:5.1f}%")
     conv_fl = sum(p["flops"] for p in prof)
     print(f"step {total:.3f} ms, {conv_fl / 1e12:.2f} TFLOP, {conv_fl / (total * 1e-3) / 1e12:.1f} TFLOP/s")
+    by = {}
+    for p in prof:
+        k = by.setdefault(p["kind"], [0, 0.0, 0.0])
+        k[0] += 1
+        k[1] += p["ms"]
+        k[2] += p["flops"]
+    for k, (n, ms, fl) in sorted(by.items(), key=lambda kv: -kv[1][1]):
+        print(f"  {k:12s} {n:3d} launches {ms:8.3f} ms {100 * ms / total:5.1f}% "
+              f"{fl / (ms * 1e-3) / 1e12 if ms else 0:7.1f} TF/s")
     if a.json:
         pathlib.Path(a.json).write_text(json.dumps(dict(config=a.config, batch=B, step_ms=total, rows=rows),
                                                    indent=1))
