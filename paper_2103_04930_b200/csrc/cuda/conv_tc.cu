@@ -60,9 +60,11 @@ __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t) {
   return c;
 }
 
-// One unit of work: output positions [o0, o0+len) of image n, branch g, channel tile mt.
+// One unit of work: output positions [o0, o0+len) of image n, branch g, channel
+// tile mt; with split-K, window iterations [w0, w1) of tile t's K loop only.
 struct Work {
   int g, n, mt, o0, len;
+  int t, ks;
 };
 
 // Iterates this CTA's work. Regular mode: fixed tiles strided by gridDim.x.
@@ -80,7 +82,7 @@ struct WorkIter {
       end = int(static_cast<long long>(blockIdx.x + 1) * p.balanced_units / gridDim.x);
     } else {
       cur = blockIdx.x;
-      end = p.total_tiles;
+      end = p.total_tiles * (p.splits > 1 ? p.splits : 1);
     }
   }
   template <int kMaxLen>
@@ -97,7 +99,12 @@ struct WorkIter {
       w.len = take * 32;
       cur += take;
     } else {
-      const TileCoord tc = decode_tile(p, cur);
+      // the splits of one tile are adjacent units: they run side by side and
+      // share the tile's activation windows in L2
+      const int S = p.splits > 1 ? p.splits : 1;
+      w.t = cur / S;
+      w.ks = cur - w.t * S;
+      const TileCoord tc = decode_tile(p, w.t);
       w.g = tc.g;
       w.n = tc.n;
       w.mt = tc.mt;
@@ -108,6 +115,18 @@ struct WorkIter {
     return true;
   }
 };
+
+// window iterations (channel chunk c, filter row r; index c * k + r) of a unit
+__device__ __forceinline__ void unit_windows(const ConvParams& p, const Work& w, int& w0, int& w1) {
+  const int nw = p.cin_chunks * p.k;
+  if (p.balanced_units > 0 || p.splits <= 1) {
+    w0 = 0;
+    w1 = nw;
+  } else {
+    w0 = w.ks * nw / p.splits;
+    w1 = (w.ks + 1) * nw / p.splits;
+  }
+}
 
 // Branch-free activation: max(x,0) + neg*min(x,0) with neg = 1 (none),
 // 0 (ReLU, +0 for negatives) or the channel's PReLU slope (lane = channel).
@@ -182,9 +201,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       Work tc;
       while (it.next<C::kTileN>(p, tc)) {
         const int row0 = tc.n * p.Hp * p.Wp + (p.P - pad) * (p.Wp + 1) + tc.o0;
-        for (int c = 0; c < p.cin_chunks; ++c) {
+        int w0, w1;
+        unit_windows(p, tc, w0, w1);
+        for (int wi = w0; wi < w1; ++wi) {
+          const int c = wi / k, r = wi - c * k;
           const int ch = p.in_c_off + c * 64;
-          for (int r = 0; r < k; ++r) {
+          {
             mbar_wait(&win_empty[ws], wph ^ 1);
             mbar_arrive_expect_tx(&win_full[ws], win_tx);
             uint8_t* wbuf = win + ws * C::kWinBytes;
@@ -229,8 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t d0 = tmem + acc * C::kTileN;
         bool first = true;
-        for (int c = 0; c < p.cin_chunks; ++c) {
-          for (int r = 0; r < k; ++r) {
+        int w0, w1;
+        unit_windows(p, tc, w0, w1);
+        for (int wi = w0; wi < w1; ++wi) {
+          {
             mbar_wait(&win_full[ws], wph);
             tc_fence_after();
             const uint32_t wb = win_base + ws * C::kWinBytes;
@@ -280,6 +304,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float neg = g.act == 1 ? 0.f : (live && g.act == 2) ? g.slope[co] : 1.f;
       mbar_wait(&acc_full[acc], aph);
       tc_fence_after();
+      if (p.splits > 1) {
+        // split-K partial: raw fp32 sums to the workspace, [px][128 channels]
+        // per unit, one 128-byte line per pixel and warp (conv_tc_reduce_kernel
+        // adds the splits in order and applies the epilogue)
+        float* dst = p.ws + (static_cast<size_t>(tc.t) * p.splits + tc.ks) * p.tile_px * kTileM + co_local;
+        for (int c0 = 0; c0 < tc.len; c0 += kChunk) {
+          uint32_t v[32];
+          tmem_ld32(tmem + ((quad * 32) << 16) + acc * C::kTileN + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j) dst[static_cast<size_t>(c0 + j) * kTileM] = __uint_as_float(v[j]);
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[acc]);
+        if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
+        continue;
+      }
       for (int sub = 0; sub < SUBS; ++sub) {
         for (int ch = 0; ch < kSubN / kChunk; ++ch) {
           if (sub * kSubN + ch * kChunk >= tc.len) break;  // uniform across the epilogue warps
@@ -355,6 +396,65 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Split-K fix-up: out = act(sum_{s in split order} partial_s + bias), zero
+// outside the image, bf16 into the padded-flat NHWC destination. Block =
+// 8 positions x 32 threads of 4 channels: a warp reads one 512-byte line per
+// split and writes 256 contiguous bytes; the split loop issues 4 loads ahead
+// of its (in-order) adds so the L2 latency is not paid per split.
+__global__ void __launch_bounds__(256) conv_tc_reduce_kernel(const __grid_constant__ ConvParams p) {
+  const int t = blockIdx.x;
+  const int px = blockIdx.y * 8 + int(threadIdx.x >> 5);
+  const int cq = int(threadIdx.x & 31) * 4;
+  if (px >= p.tile_px) return;
+  const TileCoord tc = decode_tile(p, t);
+  const ConvGroupParams& g = p.g[tc.g];
+  const int o = tc.pt * p.tile_px + px;
+  const int row = p.P * p.Wp + p.P + o;  // position inside the padded image
+  if (row >= p.Hp * p.Wp) return;        // past the image's buffer (clipped like the TMA store)
+  const int hh = o / p.Wp, ww = o - hh * p.Wp;
+  const bool valid = hh < p.H && ww < p.W;
+  const int cout_m = min(kTileM, g.cout - tc.mt * kTileM);
+  if (cq >= cout_m) return;
+  const size_t split_stride = static_cast<size_t>(p.tile_px) * kTileM;
+  const float* src = p.ws + (static_cast<size_t>(t) * p.splits * p.tile_px + px) * kTileM + cq;
+  float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+  int s = 1;
+  for (; s + 4 <= p.splits; s += 4) {
+    const float4 a = __ldcg(reinterpret_cast<const float4*>(src + s * split_stride));
+    const float4 b = __ldcg(reinterpret_cast<const float4*>(src + (s + 1) * split_stride));
+    const float4 c = __ldcg(reinterpret_cast<const float4*>(src + (s + 2) * split_stride));
+    const float4 d = __ldcg(reinterpret_cast<const float4*>(src + (s + 3) * split_stride));
+    acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+    acc.x += b.x; acc.y += b.y; acc.z += b.z; acc.w += b.w;
+    acc.x += c.x; acc.y += c.y; acc.z += c.z; acc.w += c.w;
+    acc.x += d.x; acc.y += d.y; acc.z += d.z; acc.w += d.w;
+  }
+  for (; s < p.splits; ++s) {
+    const float4 a = __ldcg(reinterpret_cast<const float4*>(src + s * split_stride));
+    acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+  }
+  const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+  __align__(8) __nv_bfloat16 out[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = cq + i;
+    float x = 0.f;
+    if (valid && c < cout_m) {
+      const int co = tc.mt * kTileM + c;
+      const float neg = g.act == 1 ? 0.f : g.act == 2 ? g.slope[co] : 1.f;
+      x = activate(__float_as_uint(v[i]), g.bias[co], neg);
+    }
+    out[i] = __float2bfloat16_rn(x);
+  }
+  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.out) +
+                       (static_cast<size_t>(tc.n) * p.Hp * p.Wp + row) * g.out_c_stride + g.out_c_off +
+                       tc.mt * kTileM + cq;
+  if (cq + 4 <= cout_m && ((g.out_c_stride | g.out_c_off) & 3) == 0)
+    *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(out);
+  else
+    for (int i = 0; i < 4 && cq + i < cout_m; ++i) dst[i] = out[i];
+}
+
 template <int SUBS>
 constexpr size_t smem_bytes() {
   return Cfg<SUBS>::total + 1024;
@@ -381,8 +481,25 @@ void conv_configure() {
              "conv smem attribute");
 }
 
+int conv_tc_splits(int tiles, int windows, int sm_count) {
+  static const bool on = [] {
+    const char* e = std::getenv("AVEC_SPLITK");
+    return !(e && e[0] == '0');
+  }();
+  static const int cap = [] {
+    const char* e = std::getenv("AVEC_SPLITK_MAX");
+    return e ? std::atoi(e) : 1 << 20;
+  }();
+  if (!on || tiles <= 0 || 2 * tiles > sm_count) return 1;
+  int s = sm_count / tiles;
+  if (s > windows) s = windows;
+  return s < cap ? s : (cap > 1 ? cap : 1);
+}
+
 void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
-  const int work = p.balanced_units > 0 ? p.balanced_units : p.total_tiles;
+  if (p.splits > 1 && (p.balanced_units > 0 || !p.ws || p.out_mode == kOutNchwF32))
+    fail(AVEC_ERR_UNSUPPORTED, "conv_tc split-K needs regular tiles, a workspace and a bf16 destination");
+  const int work = p.balanced_units > 0 ? p.balanced_units : p.total_tiles * (p.splits > 1 ? p.splits : 1);
   const int grid = work < sm_count ? work : sm_count;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -398,6 +515,10 @@ void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cud
     check_cuda(cudaLaunchKernelEx(&cfg, conv_tc_kernel<1>, maps, p), "conv_tc launch");
   else
     check_cuda(cudaLaunchKernelEx(&cfg, conv_tc_kernel<2>, maps, p), "conv_tc launch");
+  if (p.splits > 1) {
+    conv_tc_reduce_kernel<<<dim3(p.total_tiles, (p.tile_px + 7) / 8), 256, 0, stream>>>(p);
+    check_cuda(cudaGetLastError(), "conv_tc reduce launch");
+  }
 }
 
 }  // namespace avec

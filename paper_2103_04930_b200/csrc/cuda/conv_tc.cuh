@@ -96,6 +96,13 @@ struct ConvParams {
   // n_groups * n_images segments of units_per_seg units each
   int balanced_units;
   int units_per_seg;
+  // swap-AB split-K (small grids: C1, frame groups): each tile's window
+  // iterations (cin_chunks * k of them) are cut into `splits` contiguous ranges
+  // computed by different CTAs; they store raw fp32 partials to `ws`
+  // ([tile][split][tile_px][128]) and conv_tc_reduce_kernel sums them in split
+  // order (deterministic) and applies the epilogue. 1 = off.
+  int splits;
+  float* ws;
   ConvGroupParams g[kConvMaxGroups];
 };
 
@@ -148,6 +155,9 @@ struct HeadMaps {
 // per device, before the first launch (sets the dynamic smem limits)
 void conv_configure();
 void launch_conv_tc(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
+// split-K count for a swap-AB launch of `tiles` tiles with `windows` window
+// iterations each on `sm_count` SMs (1 = no split; AVEC_SPLITK=0 disables)
+int conv_tc_splits(int tiles, int windows, int sm_count);
 // pixel-major variant (conv_pm.cu)
 void conv_pm_configure();
 int conv_pm_subs(int n_tile);   // 128-pixel M sub-tiles per tile for a channel tile

@@ -714,6 +714,14 @@ struct PlanBuilder {
       const int per_img_units = int(layers.size()) * plan.n * p.m_tiles;  // tiles per pixel-tile index
       const int wide = per_img_units * ((p.H * p.Wp + 511) / 512);
       p.subs = (L0.exec_k == 7 || tc3 == 3 || (tc3 == 1 && wide >= 2 * 148)) ? 2 : 1;
+      // launches that will run split-K (wide tiles fill less than half the
+      // SMs) take 256-pixel tiles: twice the tiles, half the split count, half
+      // the fp32 partial traffic per tile. AVEC_SPLITK_NARROW=0 keeps 512.
+      static const bool narrow = [] {
+        const char* e = std::getenv("AVEC_SPLITK_NARROW");
+        return !(e && e[0] == '0');
+      }();
+      if (p.subs == 2 && narrow && conv_tc_splits(wide, p.cin_chunks * p.k, sm_count()) > 1) p.subs = 1;
       // Tile width: with 512-pixel tiles a C2 7x7 launch is 128 tiles on 148
       // SMs. Narrower tiles (the second MMA shrinks, N = T - 256) trade a
       // little per-tile weight streaming for filling the SMs: pick the width
@@ -759,6 +767,14 @@ struct PlanBuilder {
     p.balanced_units = (balanced_on && !p.pixel_major && p.subs == 2 && p.m_tiles == 1)
                            ? p.n_groups * p.n_images * p.units_per_seg
                            : 0;
+    // split-K for swap-AB launches too small to fill the SMs (C1's single
+    // frame: 10 tiles of 7x7 work for 148 SMs; frame groups of 1-4 frames)
+    p.splits = 1;
+    if (!p.pixel_major && p.balanced_units == 0 && p.out_mode != kOutNchwF32) {
+      p.splits = conv_tc_splits(p.total_tiles, p.cin_chunks * p.k, sm_count());
+      if (p.splits > 1)
+        plan.ws_bytes = std::max(plan.ws_bytes, size_t(p.total_tiles) * p.splits * p.tile_px * 128 * 4);
+    }
     for (size_t g = 0; g < layers.size(); ++g) {
       const ConvLayerDev& L = net.layers[layers[g]];
       if (L.exec_k != p.k || L.cin_pad != L0.cin_pad || L.cout_pad != L0.cout_pad ||
@@ -997,6 +1013,11 @@ Plan* get_plan(avec_ctx* ctx, Slot* slot, const Model& m, int n_img, int H, int 
   // the zeroed buffers must be in place before a forward on any stream (a
   // caller's stream in forward_device) reads them
   check_cuda(cudaStreamSynchronize(slot->stream), "plan zero-fill");
+  if (plan->ws_bytes) {  // split-K partials, shared by the plan's (stream-ordered) launches
+    plan->ws.ensure(plan->ws_bytes, ctx->device);
+    for (PlanOp& op : plan->ops)
+      if (op.kind == PlanOp::kConv && op.cp.splits > 1) op.cp.ws = plan->ws.as<float>();
+  }
   // capture the whole op sequence once; replays cost one launch
   cudaGraph_t g = nullptr;
   check_cuda(cudaStreamBeginCapture(slot->stream, cudaStreamCaptureModeThreadLocal), "begin capture");

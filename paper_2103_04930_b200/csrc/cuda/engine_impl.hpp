@@ -95,6 +95,8 @@ struct Plan {
   // fused head (its input view is the head's input, described by layer_in_from)
   std::vector<int> layer_fusion, layer_in_from;
   DevMem in, out;  // fp32 NCHW frames in, fp32 NCHW net output
+  DevMem ws;       // split-K partial sums (conv_tc), ws_bytes
+  size_t ws_bytes = 0;
   uint64_t in_elems = 0, out_elems = 0;
   cudaGraphExec_t graph = nullptr;
   uint64_t last_use = 0;  // slot-local LRU clock
