@@ -750,9 +750,10 @@ def main() -> int:
     if world > 1:
         import torch
         import torch.distributed as dist
-        # NCCL's version banner goes to stdout; keep rank 0's stdout one JSON line
-        if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-            os.environ["NCCL_DEBUG"] = "WARN"
+        # NCCL prints its version banner to stdout at NCCL_DEBUG=VERSION or WARN;
+        # keep rank 0's stdout one JSON line (unset = no banner)
+        if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "WARN"):
+            os.environ["NCCL_DEBUG"] = "NONE"
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
