@@ -9,6 +9,7 @@
 // HBM-bound: 4E bytes read + 4K bytes written per frame. Each CTA stages its
 // contiguous input span in shared memory with 16-byte loads, then every thread
 // walks four (short) segments in order.
+#include <cmath>
 #include <cstdint>
 
 #include "engine.hpp"
@@ -38,9 +39,11 @@ __device__ __forceinline__ float seg_mean(const float* x, uint64_t lo, uint64_t 
 // segments into shared memory (sized to the span: occupancy is bounded by
 // threads, not by a worst-case static buffer), then thread t walks segments
 // t, t + 256, ... so neighbouring lanes read neighbouring words.
+template <int MAXN>  // longest segment (0: any length, loop)
 __global__ void __launch_bounds__(kThreads) segmean_staged(const float* __restrict__ in,
                                                            float* __restrict__ out, uint64_t E,
                                                            uint64_t K, double width) {
+  __shared__ uint32_t bnd[kSegsPerCta + 1];  // segment boundaries, offsets into the stage
   extern __shared__ __align__(16) float stage[];
   const uint64_t j0 = static_cast<uint64_t>(blockIdx.x) * kSegsPerCta;
   const uint64_t j1 = j0 + kSegsPerCta < K ? j0 + kSegsPerCta : K;
@@ -48,19 +51,49 @@ __global__ void __launch_bounds__(kThreads) segmean_staged(const float* __restri
   const uint64_t span_hi = seg_bound(j1, K, E, width);
   // align the staged window down to 16 B so the bulk of it moves as float4
   const uint64_t base = span_lo & ~uint64_t(3);
-  const uint64_t n = span_hi - base;
-  const uint64_t n4 = n >> 2;
+  const uint32_t n = static_cast<uint32_t>(span_hi - base);
+  const uint32_t n4 = n >> 2;
   const float4* src4 = reinterpret_cast<const float4*>(in + base);
   float4* dst4 = reinterpret_cast<float4*>(stage);
-  for (uint64_t i = threadIdx.x; i < n4; i += kThreads) dst4[i] = __ldg(src4 + i);
-  for (uint64_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) stage[i] = __ldg(in + base + i);
+  for (uint32_t i = threadIdx.x; i < n4; i += kThreads) dst4[i] = __ldg(src4 + i);
+  for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) stage[i] = __ldg(in + base + i);
+  // every boundary once (segment j spans [bnd[j - j0], bnd[j - j0 + 1]) of the stage),
+  // 32-bit offsets from here on: a staged span is < 12K floats
+  const uint32_t nb = static_cast<uint32_t>(j1 - j0);
+  if (E <= 0xffffffffull) {
+    // 32-bit boundaries (every FrameData: E < 2^29): the same products
+    // double(j) * width truncated, j and the result exact in 32 bits
+    const uint32_t jb = static_cast<uint32_t>(j0), k32 = static_cast<uint32_t>(K);
+    const uint32_t e32 = static_cast<uint32_t>(E), b32 = static_cast<uint32_t>(base);
+    for (uint32_t b = threadIdx.x; b <= nb; b += kThreads) {
+      const uint32_t j = jb + b;
+      const uint32_t at = j == 0 ? 0u : j >= k32 ? e32 : __double2uint_rz(__dmul_rn(__uint2double_rn(j), width));
+      bnd[b] = at - b32;
+    }
+  } else {
+    for (uint32_t b = threadIdx.x; b <= nb; b += kThreads)
+      bnd[b] = static_cast<uint32_t>(seg_bound(j0 + b, K, E, width) - base);
+  }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kSegsPerThread; ++r) {
-    const uint64_t j = j0 + threadIdx.x + static_cast<uint64_t>(r) * kThreads;
-    if (j < K) {
-      const uint64_t lo = seg_bound(j, K, E, width), hi = seg_bound(j + 1, K, E, width);
-      out[j] = seg_mean(stage - base, lo, hi);
+    const uint32_t jl = threadIdx.x + static_cast<uint32_t>(r) * kThreads;
+    if (jl < nb) {
+      const uint32_t lo = bnd[jl], hi = bnd[jl + 1];
+      double sum = 0.0;
+      if constexpr (MAXN > 0) {
+        // straight-line: MAXN >= every segment's length; the missing terms
+        // add -0.0, the exact identity of IEEE addition (x + -0 == x for every
+        // x, -0 included), so the sum is the reference's left-to-right one
+#pragma unroll
+        for (uint32_t i = 0; i < MAXN; ++i) {
+          const float x = lo + i < hi ? stage[lo + i] : -0.0f;
+          sum = __dadd_rn(sum, static_cast<double>(x));
+        }
+      } else {
+        for (uint32_t i = lo; i < hi; ++i) sum = __dadd_rn(sum, static_cast<double>(stage[i]));
+      }
+      out[j0 + jl] = __double2float_rn(__ddiv_rn(sum, static_cast<double>(hi - lo)));
     }
   }
 }
@@ -82,10 +115,17 @@ void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t 
   const double width = static_cast<double>(E) / static_cast<double>(K);
   // a CTA spans at most ceil(kSegsPerCta * width) + 1 inputs (+3 for alignment)
   const double span = width * kSegsPerCta + 8;
-  if (span * 4 <= 48 * 1024) {
+  if (span * 4 <= 44 * 1024) {  // + 4 KB of static boundary table
     const uint64_t blocks = (K + kSegsPerCta - 1) / kSegsPerCta;
     const size_t smem = static_cast<size_t>(span) * 4 + 16;
-    segmean_staged<<<static_cast<unsigned>(blocks), kThreads, smem, stream>>>(d_in, d_out, E, K, width);
+    // segment lengths are floor((j+1)w) - floor(jw) <= ceil(w)
+    const int maxn = static_cast<int>(std::ceil(width));
+    const unsigned g = static_cast<unsigned>(blocks);
+    if (maxn <= 2) segmean_staged<2><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
+    else if (maxn <= 4) segmean_staged<4><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
+    else if (maxn <= 6) segmean_staged<6><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
+    else if (maxn <= 8) segmean_staged<8><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
+    else segmean_staged<0><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
   } else {
     const uint64_t blocks = (K + kThreads - 1) / kThreads;
     segmean_direct<<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(d_in, d_out, E, K, width);
