@@ -91,6 +91,29 @@ int avec_forward(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_
 int avec_forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h,
                         uint32_t w, const float* d_in, float* d_out, void* cuda_stream);
 
+/* Pipelined cycles: network receive, H2D, compute and D2H of ONE cycle
+ * overlap (north star: "a pinned, double-buffered H2D/D2H staging pipeline on
+ * side streams"). Replaces the reference's receive-everything-then-compute
+ * cycle (proj/src/server.cpp:272-320; channel.cpp:21-54). A stream lives on
+ * one GPU with its own copy/compute streams, staging and plans (one per
+ * session). avec_stream_begin starts a cycle for dims whose frames will land
+ * front to back in the PINNED host buffer `in`; avec_stream_feed reports how
+ * many leading bytes have landed (H2D of landed megabytes on a copy stream,
+ * compute of every frame group whose bytes are on the device, D2H of each
+ * finished group's output slice into the pinned `out` on a second stream);
+ * avec_stream_finish issues the rest, waits, and returns the device compute
+ * time of the cycle (groups + final D2H); avec_stream_abort drops the cycle
+ * (waits for work in flight). Results equal avec_forward of the same frames
+ * computed as the same frame groups. */
+typedef struct avec_stream avec_stream;
+int avec_stream_create(avec_ctx* ctx, avec_stream** out);
+void avec_stream_destroy(avec_stream* s);
+int avec_stream_begin(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                      const float* in, float* out, uint64_t out_elems);
+int avec_stream_feed(avec_stream* s, uint64_t landed_bytes);
+int avec_stream_finish(avec_stream* s, double* compute_s);
+int avec_stream_abort(avec_stream* s);
+
 /* Pose-net post-processing on device buffers (north-star kernel library):
  * bilinear x`scale` upsample of `planes` fp32 maps and 3x3 peak NMS.
  * peaks: [planes][max_peaks][5] = (x, y, refined_x, refined_y, score). */

@@ -33,6 +33,8 @@ EXPORTS = [
     "avec_nms_device", "avec_posenet_layer_io", "avec_posenet_layer_rows", "avec_posenet_layer_out_level", "avec_posenet_layer_fusion", "avec_posenet_layer_info",
     "avec_posenet_num_layers", "avec_posenet_profile", "avec_posenet_synth_weights", "avec_host_alloc", "avec_host_free",
     "avec_paf_candidates_device", "avec_assemble_people", "avec_coco_limbs",
+    "avec_stream_create", "avec_stream_destroy", "avec_stream_begin", "avec_stream_feed", "avec_stream_finish",
+    "avec_stream_abort",
 ]
 
 _lib = None
@@ -81,6 +83,12 @@ def load() -> ctypes.CDLL:
         "avec_posenet_profile": (i, [vp, u64, u32, u32, u32, u32, vp, i, i, c.POINTER(i), vp, vp, vp, vp]),
         "avec_posenet_synth_weights": (i, [u8p, c.c_size_t, fp, c.POINTER(u64)]),
         "avec_host_alloc": (vp, [u64]),
+        "avec_stream_create": (i, [vp, c.POINTER(vp)]),
+        "avec_stream_destroy": (None, [vp]),
+        "avec_stream_begin": (i, [vp, u64, u32, u32, u32, u32, vp, vp, u64]),
+        "avec_stream_feed": (i, [vp, u64]),
+        "avec_stream_finish": (i, [vp, c.POINTER(d)]),
+        "avec_stream_abort": (i, [vp]),
         "avec_host_free": (None, [vp]),
     }
     for name, (res, args) in sig.items():

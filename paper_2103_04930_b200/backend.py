@@ -283,6 +283,45 @@ class B200Backend:
                                            ctypes.c_void_p(stream) if stream else None))
 
 
+class PipelineStream:
+    """Pipelined cycle on one GPU (avec_stream_*): frames land front to back
+    in a pinned buffer, feed() reports landed bytes, finish() returns the
+    device compute seconds once the pinned output is complete."""
+
+    def __init__(self, backend: B200Backend):
+        self._L = backend._L
+        self._be = backend  # keeps the context alive
+        s = ctypes.c_void_p()
+        _lib.check(self._L.avec_stream_create(backend.ctx, ctypes.byref(s)))
+        self._s = s
+
+    def begin(self, handle: ModelHandle, dims: Dims, in_ptr: int, out_ptr: int, out_elems: int) -> None:
+        _lib.check(self._L.avec_stream_begin(self._s, handle.id, dims.batch, dims.channels, dims.height, dims.width,
+                                             in_ptr, out_ptr, out_elems))
+
+    def feed(self, landed_bytes: int) -> None:
+        _lib.check(self._L.avec_stream_feed(self._s, landed_bytes))
+
+    def finish(self) -> float:
+        secs = ctypes.c_double(0)
+        _lib.check(self._L.avec_stream_finish(self._s, ctypes.byref(secs)))
+        return secs.value
+
+    def abort(self) -> None:
+        _lib.check(self._L.avec_stream_abort(self._s))
+
+    def close(self) -> None:
+        if self._s:
+            self._L.avec_stream_destroy(self._s)
+            self._s = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def coco_limbs():
     """OpenPose COCO limb types: (limb_parts [19,2], limb_paf [19,2], new_row_limbs)."""
     L = _lib.load()

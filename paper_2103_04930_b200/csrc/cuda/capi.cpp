@@ -323,6 +323,53 @@ int avec_posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c
   });
 }
 
+int avec_stream_create(avec_ctx* ctx, avec_stream** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    *out = avec::stream_create(ctx);
+  });
+}
+
+void avec_stream_destroy(avec_stream* s) {
+  try {
+    avec::stream_destroy(s);
+  } catch (...) {
+  }
+}
+
+int avec_stream_begin(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
+                      const float* in, float* out, uint64_t out_elems) {
+  return guarded([&] {
+    need(s, "stream");
+    need(in, "in");
+    need(out, "out");
+    avec::stream_begin(s, handle, n, c, h, w, in, out, out_elems);
+  });
+}
+
+int avec_stream_feed(avec_stream* s, uint64_t landed_bytes) {
+  return guarded([&] {
+    need(s, "stream");
+    avec::stream_feed(s, landed_bytes);
+  });
+}
+
+int avec_stream_finish(avec_stream* s, double* compute_s) {
+  return guarded([&] {
+    need(s, "stream");
+    const double t = avec::stream_finish(s);
+    if (compute_s) *compute_s = t;
+  });
+}
+
+int avec_stream_abort(avec_stream* s) {
+  return guarded([&] {
+    need(s, "stream");
+    avec::stream_abort(s);
+  });
+}
+
 int avec_posenet_layer_rows(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                             const float* in, int layer, int n_in, const int32_t* in_rows, float* layer_in,
                             int n_out, const int32_t* out_rows, float* layer_out) {

@@ -973,6 +973,8 @@ void run_ops(avec_ctx* ctx, const Plan& plan, const PoseNet& net, size_t first, 
   }
 }
 
+}  // namespace
+
 Plan* get_plan(avec_ctx* ctx, Slot* slot, const Model& m, int n_img, int H, int W) {
   auto key = std::make_tuple(m.id, n_img, H, W);
   auto it = slot->plans.find(key);
@@ -1052,8 +1054,6 @@ void posenet_shape(const Model& m, uint32_t n, uint32_t c, uint32_t h, uint32_t 
                                         " gives " + std::to_string(law) + " outputs, the net yields " +
                                         std::to_string(K));
 }
-
-}  // namespace
 
 // ------------------------------------------------------------------ context
 void ctx_init(avec_ctx* ctx, int device, int slots) {

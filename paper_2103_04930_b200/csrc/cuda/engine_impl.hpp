@@ -156,6 +156,11 @@ uint64_t model_register(avec_ctx* ctx, const uint8_t* digest, const std::string&
                         uint64_t weights_len, double divisor);
 Model model_lookup(avec_ctx* ctx, uint64_t handle);
 uint64_t output_elems_for(const Model& m, uint32_t n, uint32_t c, uint32_t h, uint32_t w);
+// frames per pose-net forward of these dims (validates the shape and size law)
+void posenet_shape(const Model& m, uint32_t n, uint32_t c, uint32_t h, uint32_t w, int& n_img);
+// the slot's cached plan (activation buffers + CUDA graph) for this shape,
+// built and captured on the slot's stream on first use
+Plan* get_plan(avec_ctx* ctx, Slot* slot, const Model& m, int n_img, int H, int W);
 double forward_host(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                     const float* in, uint64_t in_elems, float* out, uint64_t out_elems);
 void forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
@@ -178,6 +183,14 @@ void posenet_layer_fusion(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c
                           int layer, int* kind, int* in_layer);
 int posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                             int layer);
+// pipelined cycles (pipeline.cu, avec_stream_* in include/avec_cuda.h)
+avec_stream* stream_create(avec_ctx* ctx);
+void stream_destroy(avec_stream* s);
+void stream_begin(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w, const float* in,
+                  float* out, uint64_t out_elems);
+void stream_feed(avec_stream* s, uint64_t landed_bytes);
+double stream_finish(avec_stream* s);
+void stream_abort(avec_stream* s);
 // selected rows (image, y) of a layer's input and output views, full-size parity
 void posenet_layer_rows(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                         const float* in, int layer, int n_in, const int32_t* in_rows, float* layer_in, int n_out,

@@ -2,6 +2,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <functional>
 #include <stdexcept>
 #include <thread>
 
@@ -60,7 +62,10 @@ B200Backend::B200Backend(std::vector<int> devices, int slots_per_device, Policy 
   }
   devices_ = devices;
   inflight_.reset(new std::atomic<int>[ctx_.size()]);
-  for (size_t i = 0; i < ctx_.size(); ++i) inflight_[i] = 0;
+  pipelines_.reset(new std::atomic<int>[ctx_.size()]);
+  streaming_.reset(new std::atomic<int>[ctx_.size()]);
+  for (size_t i = 0; i < ctx_.size(); ++i) inflight_[i] = pipelines_[i] = streaming_[i] = 0;
+  if (const char* e = std::getenv("AVEC_PIPELINE")) pipelining_ = e[0] != '0';
   label_ = ctx_.size() == 1 ? std::string(avec_ctx_label(ctx_[0]))
                             : "b200x" + std::to_string(ctx_.size()) +
                                   (policy_ == Policy::split     ? ":split"
@@ -169,6 +174,83 @@ double B200Backend::forward_session(std::uint64_t session, ModelHandle model, co
   const Entry e = lookup(model);
   const int dev = int((session == 0 ? 0 : session - 1) % ctx_.size());
   return run_on(dev, e, d, in, n_in, out, n_out);
+}
+
+namespace {
+
+// avec_stream on one GPU: the backend's model handle maps to that context's
+// A cycle is pipelined only while its GPU has nothing else to do: frame
+// groups trade some efficiency (smaller launches) for overlapping the
+// receive, which pays for one session but not when other sessions' whole
+// batches already keep the GPU busy (measured C2, 4 sessions: 2567 -> 2067
+// frames/s when every cycle was pipelined).
+class B200Pipeline final : public Pipeline {
+ public:
+  B200Pipeline(avec_ctx* ctx, std::function<std::uint64_t(ModelHandle)> handle_of, std::atomic<int>* open,
+               std::atomic<int>* active, std::atomic<int>* inflight)
+      : handle_of_(std::move(handle_of)), open_(open), active_(active), inflight_(inflight) {
+    check(avec_stream_create(ctx, &s_));
+    ++*open_;
+  }
+  ~B200Pipeline() override {
+    if (running_) --*active_;
+    avec_stream_destroy(s_);
+    --*open_;
+  }
+  bool begin(ModelHandle model, const wire::Dims& d, const float* in, float* out, std::uint64_t n_out) override {
+    if (inflight_->load() > 0) return false;
+    if (active_->fetch_add(1) > 0) {  // another session's cycle is pipelined on this GPU
+      --*active_;
+      return false;
+    }
+    running_ = true;
+    const int rc = avec_stream_begin(s_, handle_of_(model), d.batch, d.channels, d.height, d.width, in, out, n_out);
+    if (rc != AVEC_OK) {
+      release();
+      rethrow(rc);
+    }
+    return true;
+  }
+  void feed(std::uint64_t landed) override { check(avec_stream_feed(s_, landed)); }
+  double finish() override {
+    double secs = 0;
+    const int rc = avec_stream_finish(s_, &secs);
+    release();
+    check(rc);
+    return secs;
+  }
+  void abort() override {
+    const int rc = avec_stream_abort(s_);
+    release();
+    check(rc);
+  }
+
+ private:
+  void release() {
+    if (running_) --*active_;
+    running_ = false;
+  }
+  avec_stream* s_ = nullptr;
+  std::function<std::uint64_t(ModelHandle)> handle_of_;
+  std::atomic<int>*open_, *active_, *inflight_;
+  bool running_ = false;
+};
+
+}  // namespace
+
+std::unique_ptr<Pipeline> B200Backend::open_pipeline(std::uint64_t session) {
+  // split cycles span every GPU; a pipeline lives on one
+  if (!pipelining_ || (policy_ == Policy::split && ctx_.size() > 1)) return nullptr;
+  int dev = 0;
+  if (policy_ == Policy::session) {
+    dev = int((session == 0 ? 0 : session - 1) % ctx_.size());
+  } else {  // affinity: the GPU with the fewest open pipelines
+    for (size_t i = 1; i < ctx_.size(); ++i)
+      if (pipelines_[i].load() < pipelines_[dev].load()) dev = int(i);
+  }
+  return std::make_unique<B200Pipeline>(
+      ctx_[dev], [this, dev](ModelHandle h) { return lookup(h).per_device[dev]; }, &pipelines_[dev],
+      &streaming_[dev], &inflight_[dev]);
 }
 
 Heatmap B200Backend::forward(ModelHandle model, const Frame& frame) {

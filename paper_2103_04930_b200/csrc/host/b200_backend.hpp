@@ -55,6 +55,7 @@ class B200Backend final : public Backend {
   double forward_session(std::uint64_t session, ModelHandle model, const wire::Dims& dims, const float* in,
                          std::uint64_t n_in, float* out, std::uint64_t n_out) override;
   int concurrency() const override;
+  std::unique_ptr<Pipeline> open_pipeline(std::uint64_t session) override;
   void* alloc_host(std::size_t bytes) override;
   void free_host(void* p) override;
 
@@ -76,6 +77,9 @@ class B200Backend final : public Backend {
   Policy policy_;
   std::string label_;
   std::unique_ptr<std::atomic<int>[]> inflight_;
+  std::unique_ptr<std::atomic<int>[]> pipelines_;  // open pipelines per device (placement)
+  std::unique_ptr<std::atomic<int>[]> streaming_;  // pipelined cycles running per device
+  bool pipelining_ = true;                          // AVEC_PIPELINE=0 disables
   std::mutex m_;
   std::map<wire::Digest, std::uint64_t> id_by_digest_;
   std::map<std::uint64_t, Entry> models_;

@@ -47,6 +47,21 @@ struct ModelHandle {
   bool operator==(const ModelHandle&) const = default;
 };
 
+// A session's pipelined cycle (receive / H2D / compute / D2H overlap): begun
+// when a FrameData header arrives with the dims the session's previous cycle
+// had, fed as the payload lands in the pinned frame buffer, finished by the
+// dispatcher (or aborted when Resolution disagrees with the guess).
+class Pipeline {
+ public:
+  virtual ~Pipeline() = default;
+  // false: declined (e.g. the device is busy with other cycles, where whole
+  // batches use it better); the cycle then takes the dispatcher's normal path
+  virtual bool begin(ModelHandle model, const wire::Dims& dims, const float* in, float* out, std::uint64_t n_out) = 0;
+  virtual void feed(std::uint64_t landed_bytes) = 0;
+  virtual double finish() = 0;  // blocks; device compute seconds of the cycle
+  virtual void abort() = 0;
+};
+
 class Backend {
  public:
   virtual ~Backend() = default;
@@ -72,6 +87,8 @@ class Backend {
     return forward_into(h, d, in, n_in, out, n_out);
   }
   virtual int concurrency() const { return 1; }
+  // per-session pipelined cycles; nullptr: the backend has none
+  virtual std::unique_ptr<Pipeline> open_pipeline(std::uint64_t /*session*/) { return nullptr; }
   // host memory for ingest/egress staging (pinned when the backend can)
   virtual void* alloc_host(std::size_t bytes);
   virtual void free_host(void* p);

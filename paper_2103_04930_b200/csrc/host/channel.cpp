@@ -80,6 +80,7 @@ wire::Message Channel::recv(FrameSink* sink) {
         head_ += have;
         std::size_t done = have;
         auto* out = reinterpret_cast<std::uint8_t*>(dst);
+        if (done) sink->frame_progress(done);
         while (done < want) {
           const std::size_t got = stream_->read_some(out + done, want - done);
           if (got == 0) {
@@ -88,6 +89,7 @@ wire::Message Channel::recv(FrameSink* sink) {
           }
           done += got;
           received_ += got;
+          sink->frame_progress(done);
         }
         wire::FrameData fd;
         fd.elem_count = count;

@@ -33,6 +33,9 @@ class FrameSink {
   virtual float* frame_buffer(std::uint32_t elems) = 0;
   // same for an incoming ForwardResult (clients); default: buffer it
   virtual float* result_buffer(std::uint32_t /*elems*/) { return nullptr; }
+  // a streamed FrameData has `bytes` of its payload in the frame buffer
+  // (called after every socket read; lets the server start copies early)
+  virtual void frame_progress(std::size_t /*bytes*/) {}
 };
 
 class Channel {

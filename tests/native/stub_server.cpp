@@ -7,6 +7,8 @@
 // interleave out of arrival order; --print-forward-log dumps
 // Server::forward_log() on shutdown for the FIFO check (harness.cpp:676-681).
 #include <atomic>
+#include <memory>
+#include <stdexcept>
 #include <chrono>
 #include <cmath>
 #include <csignal>
@@ -21,10 +23,76 @@
 
 namespace {
 
+std::atomic<int> g_begins{0}, g_feeds{0}, g_finishes{0}, g_aborts{0};
+
+// segment means (proj/src/backend.cpp:39-67), shared by forward and the pipeline
+void segmeans(const float* x, std::uint64_t e, double c, float* out, std::uint64_t k) {
+  const double width = double(e) / double(k);
+  std::uint64_t lo = 0;
+  for (std::uint64_t j = 0; j < k; ++j) {
+    const std::uint64_t hi = (j + 1 == k) ? e : std::uint64_t(double(j + 1) * width);
+    double s = 0;
+    for (std::uint64_t i = lo; i < hi; ++i) s += double(x[i]);
+    out[j] = float(s / double(hi - lo));
+    lo = hi;
+  }
+  (void)c;
+}
+
+class StubBackend;
+
+// --pipeline: a CPU stand-in for the GPU pipeline, exercising the server's
+// cycle speculation (begin at the FrameData header with the previous cycle's
+// model and dims, feed while bytes land, finish by the dispatcher, abort when
+// Resolution disagrees). finish() computes with the GUESSED model, so a
+// guess the server failed to drop shows up as a wrong result.
+class StubPipeline final : public avec::backend::Pipeline {
+ public:
+  explicit StubPipeline(StubBackend* be) : be_(be) {}
+  bool begin(avec::backend::ModelHandle m, const avec::wire::Dims& d, const float* in, float* out,
+             std::uint64_t n_out) override;
+  void feed(std::uint64_t landed) override {
+    if (landed < landed_) throw std::runtime_error("feed went backwards");
+    landed_ = landed;
+    ++g_feeds;
+  }
+  double finish() override;
+  void abort() override { ++g_aborts; }
+
+ private:
+  StubBackend* be_;
+  avec::backend::ModelHandle model_;
+  avec::wire::Dims dims_;
+  const float* in_ = nullptr;
+  float* out_ = nullptr;
+  std::uint64_t n_out_ = 0, landed_ = 0;
+};
+
 class StubBackend final : public avec::backend::Backend {
  public:
-  StubBackend(int concurrency, int jitter_ms) : concurrency_(concurrency), jitter_ms_(jitter_ms) {}
+  StubBackend(int concurrency, int jitter_ms, bool pipeline)
+      : concurrency_(concurrency), jitter_ms_(jitter_ms), pipeline_(pipeline) {}
   int concurrency() const override { return concurrency_; }
+  bool zero_copy() const override { return pipeline_; }
+  std::uint64_t output_elems(avec::backend::ModelHandle h, const avec::wire::Dims& d) override {
+    return std::uint64_t(std::llround(double(d.elem_count()) / divisor(h)));
+  }
+  double forward_into(avec::backend::ModelHandle h, const avec::wire::Dims& d, const float* in, std::uint64_t n,
+                      float* out, std::uint64_t k) override {
+    (void)d;
+    segmeans(in, n, divisor(h), out, k);
+    return 0.0;
+  }
+  std::unique_ptr<avec::backend::Pipeline> open_pipeline(std::uint64_t) override {
+    if (!pipeline_) return nullptr;
+    return std::make_unique<StubPipeline>(this);
+  }
+  double divisor(avec::backend::ModelHandle h) {
+    std::lock_guard<std::mutex> lk(m_);
+    auto it = div_.find(h.id);
+    if (it == div_.end()) throw avec::backend::Error(avec::backend::ErrorCode::unknown_model, "unknown model");
+    return it->second;
+  }
   avec::backend::ModelHandle register_model(const avec::wire::ModelDescriptor& m) override {
     using avec::backend::Error;
     using avec::backend::ErrorCode;
@@ -73,12 +141,27 @@ class StubBackend final : public avec::backend::Backend {
 
  private:
   int concurrency_ = 1, jitter_ms_ = 0;
+  bool pipeline_ = false;
   std::atomic<std::uint64_t> calls_{0};
   std::mutex m_;
   std::map<avec::wire::Digest, std::uint64_t> ids_;
   std::map<std::uint64_t, double> div_;
   std::uint64_t next_ = 1;
 };
+
+bool StubPipeline::begin(avec::backend::ModelHandle m, const avec::wire::Dims& d, const float* in, float* out,
+                         std::uint64_t n_out) {
+  model_ = m, dims_ = d, in_ = in, out_ = out, n_out_ = n_out, landed_ = 0;
+  ++g_begins;
+  return true;
+}
+
+double StubPipeline::finish() {
+  if (landed_ != dims_.elem_count() * 4) throw std::runtime_error("finish before the frame landed");
+  segmeans(in_, dims_.elem_count(), be_->divisor(model_), out_, n_out_);
+  ++g_finishes;
+  return 0.0;
+}
 
 }  // namespace
 
@@ -88,11 +171,15 @@ int main(int argc, char** argv) {
   unsigned long long max_model = 1ull << 30;
   int concurrency = 1, jitter_ms = 0;
   unsigned long long log_cap = 1ull << 20;
-  bool print_log = false;
+  bool print_log = false, pipeline = false;
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
     if (a == "--print-forward-log") {
       print_log = true;
+      continue;
+    }
+    if (a == "--pipeline") {
+      pipeline = true;
       continue;
     }
     if (i + 1 >= argc) break;
@@ -114,7 +201,7 @@ int main(int argc, char** argv) {
   cfg.limits.max_sessions = max_sessions;
   cfg.limits.max_model_bytes = max_model;
   cfg.forward_log_cap = log_cap;
-  auto be = std::make_shared<StubBackend>(concurrency, jitter_ms);
+  auto be = std::make_shared<StubBackend>(concurrency, jitter_ms, pipeline);
   avec::server::Server srv(be, cfg);
   const auto port = srv.listen("127.0.0.1", 0);
   std::printf("listening on 127.0.0.1:%u (backend %s)\n", port, std::string(be->label()).c_str());
@@ -131,6 +218,8 @@ int main(int argc, char** argv) {
       std::printf("%s[%llu, %llu]", i ? ", " : "", (unsigned long long)log_entries[i].arrival_seq,
                   (unsigned long long)log_entries[i].session_id);
     std::printf("]\nsession_threads %zu\n", live_threads);
+    std::printf("pipeline begins %d feeds %d finishes %d aborts %d\n", g_begins.load(), g_feeds.load(),
+                g_finishes.load(), g_aborts.load());
   }
   std::fflush(stdout);
   return 0;

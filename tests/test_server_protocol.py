@@ -304,3 +304,44 @@ def test_forward_log_bounded_and_sessions_reaped():
     log, threads = _forward_log(out)
     assert [e[0] for e in log] == list(range(15, 20))
     assert threads <= 2, threads
+
+
+def test_pipelined_cycle_speculation():
+    """Receive/compute overlap (north star subsystem 2) on the server side: a
+    FrameData of the previous cycle's size starts the cycle on the backend
+    pipeline with the previous model and dims, before Resolution (which the
+    wire sends AFTER the frame, server.cpp:272-292) can confirm them. A
+    Resolution with other dims, or a new model, must drop the guess; every
+    reply must equal the reference's segment means for the cycle's own model.
+    The stub pipeline computes with the GUESSED model, so a guess the server
+    failed to drop would show up as a wrong result."""
+    _ensure_built()
+    srv = W.ServerProc([str(STUB), "--print-forward-log", "--pipeline"])
+    try:
+        p = _ready(srv, c=2.0)
+        rng = np.random.default_rng(5)
+
+        def cycle(w, h, c):
+            data = rng.random(w * h * 3, dtype=np.float32)
+            p.send(W.frame_data(data) + W.resolution(w, h) + W.frame_size(data.size))
+            tag, payload = p.recv_msg()
+            assert tag == "forward_result", tag
+            got = W.forward_result(payload)[1]
+            assert got.tobytes() == O.mockpose_forward(data, c).tobytes(), (w, h, c)
+
+        for _ in range(3):
+            cycle(64, 32, 2.0)      # cycles 2, 3 speculate and finish on the pipeline
+        cycle(32, 64, 2.0)          # same size, other dims: speculated, then dropped
+        cycle(32, 64, 2.0)          # speculates with the new dims
+        s2, w2 = b"\x05\x06", b"\x01" * 8
+        p.send(W.model_upload(s2, w2, 4.0))
+        assert p.recv_msg()[0] == "model_ack"
+        cycle(32, 64, 4.0)          # new model: no speculation
+        cycle(32, 64, 4.0)          # speculates with the new model
+        p.close()
+    finally:
+        out = srv.stop()
+    line = next(l for l in out.splitlines() if l.startswith("pipeline "))
+    counts = dict(zip(line.split()[1::2], map(int, line.split()[2::2])))
+    assert counts == {"begins": 5, "feeds": counts["feeds"], "finishes": 4, "aborts": 1}, counts
+    assert counts["feeds"] >= 5
