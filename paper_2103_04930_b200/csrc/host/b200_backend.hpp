@@ -60,6 +60,7 @@ class B200Backend final : public Backend {
   void free_host(void* p) override;
 
   int device_count() const { return int(ctx_.size()); }
+  int devices() const override { return int(ctx_.size()); }
 
  private:
   struct Entry {

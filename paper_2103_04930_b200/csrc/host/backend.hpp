@@ -87,6 +87,7 @@ class Backend {
     return forward_into(h, d, in, n_in, out, n_out);
   }
   virtual int concurrency() const { return 1; }
+  virtual int devices() const { return 1; }
   // per-session pipelined cycles; nullptr: the backend has none
   virtual std::unique_ptr<Pipeline> open_pipeline(std::uint64_t /*session*/) { return nullptr; }
   // host memory for ingest/egress staging (pinned when the backend can)
