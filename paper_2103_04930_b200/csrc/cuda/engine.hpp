@@ -30,8 +30,11 @@ inline void check_cuda(cudaError_t e, const char* what) {
 bool pdl_enabled();
 
 // ---- kernels (one .cu each) ----
-void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K,
-                          cudaStream_t stream);
+// segments [jbeg, jend) of the E -> K segment means (default: all)
+void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K, cudaStream_t stream,
+                          uint64_t jbeg = 0, uint64_t jend = ~uint64_t(0));
+// start of segment j in the input (the kernel's boundary, on the host)
+uint64_t segment_bound(uint64_t j, uint64_t E, uint64_t K);
 
 // PAF candidate scores [n_limbs][max_peaks][max_peaks][2] = (score, valid)
 // for the peaks of avec_nms_device (paf.cu), and the host person assembly

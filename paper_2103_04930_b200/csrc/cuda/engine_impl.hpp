@@ -111,6 +111,9 @@ struct Slot {
   bool pending = false;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   PinnedMem stage[2];
+  // side streams of the chunked segment-mean cycle (H2D, D2H) and its events
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
   DevMem d_in, d_out;  // segment-mean path
   // cached plans (activation buffers + CUDA graph) per (model, frames, H, W),
   // least recently used evicted beyond AVEC_PLANS_PER_SLOT (default 4): a

@@ -42,11 +42,12 @@ __device__ __forceinline__ float seg_mean(const float* x, uint64_t lo, uint64_t 
 template <int MAXN>  // longest segment (0: any length, loop)
 __global__ void __launch_bounds__(kThreads) segmean_staged(const float* __restrict__ in,
                                                            float* __restrict__ out, uint64_t E,
-                                                           uint64_t K, double width) {
+                                                           uint64_t K, double width, uint64_t jbeg,
+                                                           uint64_t jend) {
   __shared__ uint32_t bnd[kSegsPerCta + 1];  // segment boundaries, offsets into the stage
   extern __shared__ __align__(16) float stage[];
-  const uint64_t j0 = static_cast<uint64_t>(blockIdx.x) * kSegsPerCta;
-  const uint64_t j1 = j0 + kSegsPerCta < K ? j0 + kSegsPerCta : K;
+  const uint64_t j0 = jbeg + static_cast<uint64_t>(blockIdx.x) * kSegsPerCta;
+  const uint64_t j1 = j0 + kSegsPerCta < jend ? j0 + kSegsPerCta : jend;
   const uint64_t span_lo = seg_bound(j0, K, E, width);
   const uint64_t span_hi = seg_bound(j1, K, E, width);
   // align the staged window down to 16 B so the bulk of it moves as float4
@@ -101,34 +102,47 @@ __global__ void __launch_bounds__(kThreads) segmean_staged(const float* __restri
 // general: wide segments (large divisors) read straight from global/L1
 __global__ void __launch_bounds__(kThreads) segmean_direct(const float* __restrict__ in,
                                                            float* __restrict__ out, uint64_t E,
-                                                           uint64_t K, double width) {
-  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
-  if (j >= K) return;
+                                                           uint64_t K, double width, uint64_t jbeg,
+                                                           uint64_t jend) {
+  const uint64_t j = jbeg + static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  if (j >= jend) return;
   const uint64_t lo = seg_bound(j, K, E, width), hi = seg_bound(j + 1, K, E, width);
   out[j] = seg_mean(in, lo, hi);
 }
 
 }  // namespace
 
-void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K,
-                          cudaStream_t stream) {
+uint64_t segment_bound(uint64_t j, uint64_t E, uint64_t K) {
+  // the device's seg_bound on the host: same IEEE product, truncated
+  if (j == 0) return 0;
+  if (j >= K) return E;
   const double width = static_cast<double>(E) / static_cast<double>(K);
+  return static_cast<uint64_t>(static_cast<double>(j) * width);
+}
+
+void launch_segment_means(const float* d_in, float* d_out, uint64_t E, uint64_t K, cudaStream_t stream,
+                          uint64_t jbeg, uint64_t jend) {
+  if (jend > K) jend = K;
+  if (jbeg >= jend) return;
+  const double width = static_cast<double>(E) / static_cast<double>(K);
+  const uint64_t segs = jend - jbeg;
   // a CTA spans at most ceil(kSegsPerCta * width) + 1 inputs (+3 for alignment)
   const double span = width * kSegsPerCta + 8;
   if (span * 4 <= 44 * 1024) {  // + 4 KB of static boundary table
-    const uint64_t blocks = (K + kSegsPerCta - 1) / kSegsPerCta;
+    const uint64_t blocks = (segs + kSegsPerCta - 1) / kSegsPerCta;
     const size_t smem = static_cast<size_t>(span) * 4 + 16;
     // segment lengths are floor((j+1)w) - floor(jw) <= ceil(w)
     const int maxn = static_cast<int>(std::ceil(width));
     const unsigned g = static_cast<unsigned>(blocks);
-    if (maxn <= 2) segmean_staged<2><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
-    else if (maxn <= 4) segmean_staged<4><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
-    else if (maxn <= 6) segmean_staged<6><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
-    else if (maxn <= 8) segmean_staged<8><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
-    else segmean_staged<0><<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width);
+    auto go = [&](auto kernel) { kernel<<<g, kThreads, smem, stream>>>(d_in, d_out, E, K, width, jbeg, jend); };
+    if (maxn <= 2) go(segmean_staged<2>);
+    else if (maxn <= 4) go(segmean_staged<4>);
+    else if (maxn <= 6) go(segmean_staged<6>);
+    else if (maxn <= 8) go(segmean_staged<8>);
+    else go(segmean_staged<0>);
   } else {
-    const uint64_t blocks = (K + kThreads - 1) / kThreads;
-    segmean_direct<<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(d_in, d_out, E, K, width);
+    const uint64_t blocks = (segs + kThreads - 1) / kThreads;
+    segmean_direct<<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(d_in, d_out, E, K, width, jbeg, jend);
   }
   check_cuda(cudaGetLastError(), "segment means launch");
 }

@@ -179,3 +179,26 @@ def test_device_resident_path(be):
     torch.cuda.synchronize()
     be.forward_device(h, d, din.data_ptr(), dout.data_ptr())
     assert dout.cpu().numpy().tobytes() == O.mockpose_forward(f, 3.368421).tobytes()
+
+
+@pytest.mark.parametrize("elems,c", [(16 * 1024 * 1024 + 7, 1.0), (24_000_011, 3.368421), (5_000_000, 0.999)])
+def test_overlapped_chunks_bit_exact(elems, c):
+    """Pinned frames >= 16 MB take the chunked path (H2D / segment kernel /
+    D2H of ~8 MB chunks cut at segment boundaries, on three streams): still
+    bit-exact against the oracle, odd sizes and c < 1 (K > E rejected) included."""
+    from paper_2103_04930_b200 import B200Backend, Dims, Frame, PinnedBuffer, make_model
+    be = B200Backend(0, slots=1)
+    h = be.register_model(make_model("chunky", b"\x03\x04", b"", c))
+    data = np.random.default_rng(elems).random(elems, dtype=np.float32)
+    pin_in = PinnedBuffer(elems)
+    pin_in.array[:] = data
+    if c < 1.0:
+        with pytest.raises(Exception):
+            be.output_elems(h, Dims(1, 1, 1, elems))
+        be.close()
+        return
+    want = O.mockpose_forward(data, c)
+    pin_out = PinnedBuffer(want.size)
+    be.forward(h, Frame(Dims(1, 1, 1, elems), pin_in.array), out=pin_out.array)
+    assert pin_out.array.tobytes() == want.tobytes()
+    be.close()
