@@ -33,6 +33,7 @@
 #include "conv_tc.cuh"
 #include "engine.hpp"
 #include "ptx.cuh"
+#include "trace.cuh"
 
 namespace avec {
 
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::kAccStages);
 
   const uint32_t warp = warp_id();
+  if (threadIdx.x == 0) AVEC_STAMP(0);
   // CTA pair (NCTA == 2): rank 0 (leader) issues the M = 256 MMAs and owns the
   // full / acc_empty barriers; both CTAs load their own window and half of
   // every weight k-block, and run the epilogue of their own 128-row halves
@@ -176,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // see conv_tc.cu
+  if (threadIdx.x == 0) AVEC_STAMP(1);
 
   const int k = p.k;
   const int pad = k / 2;
@@ -247,9 +250,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             // window rows: kTileN (<= 256, one box when SUBS_M == 2) + 8-row halo
             load_window(tc, ch, row0 + r * p.Wp);
             load_weights(tc, c, r);
+            if (c == 0 && r == 0) AVEC_STAMP(2);
           }
         }
       }
+      AVEC_STAMP(3);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int r = 0; r < k; ++r) {
             mbar_wait(&win_full[ws], wph);
             tc_fence_after();
+            if (first) AVEC_STAMP(4);
             const uint32_t wb = win_base + ws * C::kWinBytes;
             if constexpr (C::kTaps == 3) {
               mbar_wait(&w_full[wst], wtph);
@@ -355,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         commit(&acc_full[acc]);
         if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
       }
+      AVEC_STAMP(5);
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else {
@@ -387,6 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 128);
       mbar_wait(&acc_full[acc], aph);
       tc_fence_after();
+      if (ep == 0) AVEC_STAMP(6);
       __nv_bfloat16* out = static_cast<__nv_bfloat16*>(g.out);
       const int c_left = g.cout - tc.nt * N;  // live channels of this tile
       if constexpr (POOL) {
@@ -577,7 +585,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
     }
+    if (ep == 0) AVEC_STAMP(7);
     if (lane == 0) bulk_wait<0>();
+    if (ep == 0) AVEC_STAMP(8);
   }
   tc_fence_before();
   if constexpr (NCTA == 2) cluster_sync_all();  // the leader's MMAs read peer smem until the end
@@ -587,6 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (NCTA == 2) tmem_dealloc_pair<kTmemCols>(tmem);
     else tmem_dealloc<kTmemCols>(tmem);
   }
+  if (threadIdx.x == 0) AVEC_STAMP(9);
 }
 
 template <int N, int SUBS_M, int NCTA, bool POOL = false>
@@ -630,6 +641,16 @@ void configure_pm() {
 }
 
 }  // namespace
+
+#ifdef AVEC_TRACE
+void conv_pm_trace(int on, cudaStream_t st) {
+  check_cuda(cudaMemcpyToSymbolAsync(g_trace_on, &on, sizeof on, 0, cudaMemcpyHostToDevice, st), "trace arm");
+  check_cuda(cudaStreamSynchronize(st), "trace arm");
+}
+int conv_pm_trace_dump(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 5;
+}
+#endif
 
 int conv_pm_subs(int n_tile) { return n_tile == 256 ? 1 : 2; }  // 2 acc stages fit TMEM
 

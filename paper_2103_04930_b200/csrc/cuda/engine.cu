@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "engine_impl.hpp"
+#include "trace.cuh"
 
 namespace avec {
 
@@ -1307,10 +1308,19 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
   std::vector<cudaEvent_t> ev(nops + 1);
   for (auto& e : ev) check_cuda(cudaEventCreate(&e), "event");
   std::vector<OpProfile> prof(nops);
+#ifdef AVEC_TRACE
+  const int trace_op = std::getenv("AVEC_TRACE_OP") ? std::atoi(std::getenv("AVEC_TRACE_OP")) : -1;
+#endif
   for (int r = 0; r < reps; ++r) {
     for (size_t i = 0; i < nops; ++i) {
       check_cuda(cudaEventRecord(ev[i], s->stream), "event");
+#ifdef AVEC_TRACE
+      if (r == reps - 1 && int(i) == trace_op) conv_pm_trace(1, s->stream);
       run_ops(ctx, *plan, *m.net, i, i + 1, s->stream);
+      if (r == reps - 1 && int(i) == trace_op) conv_pm_trace(0, s->stream);
+#else
+      run_ops(ctx, *plan, *m.net, i, i + 1, s->stream);
+#endif
     }
     check_cuda(cudaEventRecord(ev[nops], s->stream), "event");
     check_cuda(cudaEventSynchronize(ev[nops]), "event sync");
@@ -1568,3 +1578,8 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
 }
 
 }  // namespace avec
+
+#ifdef AVEC_TRACE
+// trace builds only: the stamps of the launch traced by avec_posenet_profile
+extern "C" int avec_trace_dump(unsigned long long* host, int n) { return avec::conv_pm_trace_dump(host, n); }
+#endif
