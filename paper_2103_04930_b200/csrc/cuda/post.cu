@@ -4,7 +4,10 @@
 #include <algorithm>
 #include <cstdint>
 
+#include <cstdlib>
+
 #include "engine.hpp"
+#include "ptx.cuh"
 
 namespace avec {
 
@@ -185,7 +188,8 @@ __device__ __forceinline__ bool lane_peak(const float* __restrict__ pl, int H, i
 // plane in shared memory with coalesced float4 loads (many in flight), then
 // each thread tests four columns per row from the tile. Rows and columns
 // outside the plane read as -inf, so "strictly greater" ignores them.
-constexpr int kNmsRows = 8;
+constexpr int kNmsRows = 8;      // two-pass kernels
+constexpr int kNmsRows1 = 8;     // one-pass tiles (16 measured slower: 119 vs 100 us; masks hold <= 16 rows)
 
 __device__ __forceinline__ void nms_stage_tile(float* tile, const float* __restrict__ p, int H, int W, int y0,
                                                int rows) {
@@ -306,6 +310,140 @@ __global__ void nms4_write_kernel(const float* __restrict__ in, int H, int W, fl
       }
       ++idx;
     }
+    __syncthreads();  // warp_cnt is rewritten for the next row
+  }
+}
+
+// Single pass (W % 4 == 0): every block takes the next 8-row tile in launch
+// order (atomic ticket, so every earlier tile has started), counts its peaks,
+// publishes the count, and finds the number of peaks before it in raster
+// order by looking back over the earlier tiles of its plane (decoupled
+// look-back: a tile whose inclusive prefix is already published ends the
+// walk). It then writes its peaks at those offsets from its staged rows, so
+// the heatmaps are read once instead of twice. Peak test and refinement are
+// the same code as the two-pass kernels (bit-exact against the oracle).
+constexpr unsigned long long kNmsAgg = 1ull << 62, kNmsPrefix = 1ull << 63;
+
+__global__ void nms4_onepass_kernel(const float* __restrict__ in, int H, int W, float threshold, int max_peaks,
+                                    int tiles_per_plane, unsigned long long* __restrict__ status,
+                                    int* __restrict__ ticket, int* __restrict__ counts, float* __restrict__ peaks) {
+  extern __shared__ __align__(16) float tile[];
+  __shared__ int s_id, s_prefix, warp_cnt[32], row_tot[kNmsRows1];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) {
+    s_id = atomicAdd(ticket, 1);
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_barrier_init();
+  }
+  if (threadIdx.x < kNmsRows1) row_tot[threadIdx.x] = 0;
+  __syncthreads();
+  const int id = s_id;
+  const int pl = id / tiles_per_plane, tt = id - pl * tiles_per_plane;
+  const int y0 = tt * kNmsRows1;
+  const int rows = y0 + kNmsRows1 < H ? kNmsRows1 : H - y0;
+  const float* p = in + static_cast<size_t>(pl) * H * W;
+  // stage rows y0-1 .. y0+rows: the in-plane ones are contiguous in memory,
+  // one bulk async copy (the whole tile in flight at once); the out-of-plane
+  // halo rows read as -inf
+  const int ya = y0 > 0 ? y0 - 1 : 0, yb = y0 + rows < H ? y0 + rows + 1 : H;  // [ya, yb) in the plane
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = static_cast<uint32_t>(yb - ya) * W * 4;
+    ptx::mbar_arrive_expect_tx(&bar, bytes);
+    ptx::bulk_load(tile + (ya - (y0 - 1)) * W, p + static_cast<size_t>(ya) * W, bytes, &bar);
+  }
+  {
+    const float NEG = -__int_as_float(0x7f800000);
+    if (y0 == 0)
+      for (int i = threadIdx.x; i < W; i += blockDim.x) tile[i] = NEG;
+    if (y0 + rows == H)
+      for (int i = threadIdx.x; i < W; i += blockDim.x) tile[(rows + 1) * W + i] = NEG;
+  }
+  ptx::mbar_wait(&bar, 0);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int x4 = threadIdx.x;  // blockDim covers W / 4 columns
+  uint64_t masks = 0;          // 4 columns x kNmsRows1 rows of peak bits
+  for (int r = 0; r < rows; ++r) {
+    float mid[4];
+    const unsigned m = nms_tile_peaks(tile, W, r, x4, threshold, mid);
+    masks |= static_cast<uint64_t>(m) << (4 * r);
+    int cnt = __popc(m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0 && cnt) atomicAdd(&row_tot[r], cnt);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    // warp 0: publish this tile's count, then look back 32 tiles at a time
+    int total = 0;
+    for (int r = 0; r < rows; ++r) total += row_tot[r];
+    unsigned long long* st = status + static_cast<size_t>(pl) * tiles_per_plane;
+    if (lane == 0) atomicExch(&st[tt], (tt == 0 ? kNmsPrefix : kNmsAgg) | static_cast<unsigned>(total));
+    int prefix = 0;
+    for (int j = tt - 1; j >= 0; j -= 32) {
+      const int idx = j - lane;  // lane k looks at tile j - k; before the plane: a prefix of 0
+      unsigned long long v = idx >= 0 ? 0ull : kNmsPrefix;
+      while (!__all_sync(0xffffffffu, (v & (kNmsAgg | kNmsPrefix)) != 0))
+        if (!(v & (kNmsAgg | kNmsPrefix))) v = atomicAdd(&st[idx], 0ull);
+      const unsigned pm = __ballot_sync(0xffffffffu, (v & kNmsPrefix) != 0);
+      const int first = pm ? __ffs(pm) - 1 : 32;  // nearest tile whose inclusive prefix is known
+      int c = lane <= first ? static_cast<int>(v & 0xffffffffu) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      prefix += c;
+      if (pm) break;
+    }
+    if (lane == 0) {
+      if (tt > 0) {
+        __threadfence();
+        atomicExch(&st[tt], kNmsPrefix | static_cast<unsigned>(prefix + total));
+      }
+      if (tt + 1 == tiles_per_plane) counts[pl] = prefix + total < max_peaks ? prefix + total : max_peaks;
+      s_prefix = prefix;
+    }
+  }
+  __syncthreads();
+  int base = s_prefix;
+  for (int r = 0; r < rows; ++r) {
+    if (base >= max_peaks) return;  // uniform across the block
+    const int y = y0 + r;
+    const unsigned m = static_cast<unsigned>(masks >> (4 * r)) & 15u;
+    const int mine = __popc(m);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_cnt[wid] = incl;
+    __syncthreads();
+    int before = 0;
+    for (int i = 0; i < wid; ++i) before += warp_cnt[i];
+    int idx = base + before + incl - mine;
+    for (int i = 0; i < 4; ++i) {
+      if (!((m >> i) & 1u)) continue;
+      if (idx < max_peaks) {
+        const int x = 4 * x4 + i;
+        float sw = 0.0f, sx = 0.0f, sy = 0.0f;
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int yy = y + dy, xx = x + dx;
+            if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+            const float sv = tile[(r + 1 + dy) * W + xx];
+            sw = __fadd_rn(sw, sv);
+            sx = __fadd_rn(sx, __fmul_rn(static_cast<float>(xx), sv));
+            sy = __fadd_rn(sy, __fmul_rn(static_cast<float>(yy), sv));
+          }
+        float* o = peaks + (static_cast<size_t>(pl) * max_peaks + idx) * 5;
+        o[0] = static_cast<float>(x);
+        o[1] = static_cast<float>(y);
+        o[2] = __fdiv_rn(sx, sw);
+        o[3] = __fdiv_rn(sy, sw);
+        o[4] = tile[(r + 1) * W + x];
+      }
+      ++idx;
+    }
+    base += row_tot[r];
     __syncthreads();  // warp_cnt is rewritten for the next row
   }
 }
@@ -446,7 +584,27 @@ void launch_nms(const float* d_in, int planes, int H, int W, float threshold, in
       check_cuda(cudaFuncSetAttribute(nms4_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(tile_bytes)), "nms smem");
     }
-    dim3 grid4((H + kNmsRows - 1) / kNmsRows, planes);
+    const int tiles = (H + kNmsRows - 1) / kNmsRows;
+    const int tiles1 = (H + kNmsRows1 - 1) / kNmsRows1;
+    const size_t tile1_bytes = static_cast<size_t>(kNmsRows1 + 2) * W * sizeof(float);
+    static const bool two_pass = [] {
+      const char* e = std::getenv("AVEC_NMS_TWOPASS");
+      return e && e[0] == '1';
+    }();
+    if (!two_pass && (reinterpret_cast<uintptr_t>(d_in) & 15) == 0) {
+      if (tile1_bytes > 48 * 1024)
+        check_cuda(cudaFuncSetAttribute(nms4_onepass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(tile1_bytes)), "nms smem");
+      // look-back status words + the tile ticket, zeroed for this launch
+      auto* status = reinterpret_cast<unsigned long long*>(d_scratch);
+      int* ticket = reinterpret_cast<int*>(status + static_cast<size_t>(planes) * tiles1);
+      check_cuda(cudaMemsetAsync(d_scratch, 0, static_cast<size_t>(planes) * tiles1 * 8 + 4, stream), "nms status");
+      nms4_onepass_kernel<<<tiles1 * planes, threads, tile1_bytes, stream>>>(d_in, H, W, threshold, max_peaks, tiles1,
+                                                                              status, ticket, d_counts, d_peaks);
+      check_cuda(cudaGetLastError(), "nms launch");
+      return;
+    }
+    dim3 grid4(tiles, planes);
     nms4_count_kernel<<<grid4, threads, tile_bytes, stream>>>(d_in, H, W, threshold, row_counts);
     nms_scan_kernel<<<planes, 32, 0, stream>>>(row_counts, H, max_peaks, row_offsets, d_counts);
     nms4_write_kernel<<<grid4, threads, tile_bytes, stream>>>(d_in, H, W, threshold, max_peaks, row_offsets,
