@@ -14,6 +14,7 @@
 #include <cerrno>
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -32,10 +33,17 @@ class TcpStream final : public Stream {
   explicit TcpStream(int fd) : fd_(fd) {
     int one = 1;
     setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &one, sizeof one);
-    // large socket buffers: frames are tens of MB
-    int buf = 8 << 20;
-    setsockopt(fd, SOL_SOCKET, SO_RCVBUF, &buf, sizeof buf);
-    setsockopt(fd, SOL_SOCKET, SO_SNDBUF, &buf, sizeof buf);
+    // frames are tens of MB. An explicit SO_RCVBUF/SO_SNDBUF turns off the
+    // kernel's buffer autotuning and is capped at net.core.[rw]mem_max, so it
+    // is only set when asked for (AVEC_SOCKBUF=<bytes>)
+    static const int buf = [] {
+      const char* e = std::getenv("AVEC_SOCKBUF");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (buf > 0) {
+      setsockopt(fd, SOL_SOCKET, SO_RCVBUF, &buf, sizeof buf);
+      setsockopt(fd, SOL_SOCKET, SO_SNDBUF, &buf, sizeof buf);
+    }
   }
   ~TcpStream() override { close(); }
 
