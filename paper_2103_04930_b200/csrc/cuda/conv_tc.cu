@@ -6,6 +6,7 @@
 #include "conv_tc.cuh"
 #include "engine.hpp"
 #include "ptx.cuh"
+#include "trace.cuh"
 
 namespace avec {
 
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::kAccStages);
 
   const uint32_t warp = warp_id();
+  if (threadIdx.x == 0) AVEC_STAMP(0);
   if (warp == 0 && elect_one()) {
     for (int g = 0; g < p.n_groups; ++g) {
       tma_prefetch(&maps.act_big[g]);
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // only once this CTA has issued its last MMA (see below), so its CTAs do
   // not park on SMs another stream could use.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) AVEC_STAMP(1);
 
   const int k = p.k;
   const int pad = k / 2;
@@ -257,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           {
             mbar_wait(&win_full[ws], wph);
             tc_fence_after();
+            if (wi == w0) AVEC_STAMP(4);
             const uint32_t wb = win_base + ws * C::kWinBytes;
             for (int s = 0; s < k; ++s) {
               mbar_wait(&w_full[wst], wtph);
@@ -283,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&acc_full[acc]);
         if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
       }
+      AVEC_STAMP(5);
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else {
@@ -304,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float neg = g.act == 1 ? 0.f : (live && g.act == 2) ? g.slope[co] : 1.f;
       mbar_wait(&acc_full[acc], aph);
       tc_fence_after();
+      if (threadIdx.x == 64) AVEC_STAMP(6);
       if (p.splits > 1) {
         // split-K partial: raw fp32 sums to the workspace, [px][128 channels]
         // per unit, one 128-byte line per pixel and warp (conv_tc_reduce_kernel
@@ -341,12 +347,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               else bulk_wait_read<0>();
             }
             named_bar_sync(kEpiBar, kEpiThreads);
-            if (live) {
+            {
+              // channels past cout (zero weights and bias) store zeros: a
+              // 96-channel layer's second box ends 32 channels into the
+              // destination's next slice, which a later layer overwrites
               uint8_t* half = buf + (co_local >> 6) * (kChunk * 128);
               const uint32_t cb = (co_local & 63) * 2;
 #pragma unroll
               for (int j = 0; j < kChunk; ++j) {
-                const float x = (mask >> j) & 1u ? activate(v[j], bias, neg) : 0.f;
+                const float x = live && ((mask >> j) & 1u) ? activate(v[j], bias, neg) : 0.f;
                 *reinterpret_cast<__nv_bfloat16*>(half + j * 128 + ((((cb >> 4) ^ (j & 7)) << 4) | (cb & 15))) =
                     __float2bfloat16_rn(x);
               }
@@ -386,7 +395,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&acc_empty[acc]);
       if (++acc == C::kAccStages) { acc = 0; aph ^= 1; }
     }
+    if (leader) AVEC_STAMP(7);
     if (leader) bulk_wait<0>();
+    if (leader) AVEC_STAMP(8);
   }
   tc_fence_before();
   __syncthreads();
@@ -394,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+  if (threadIdx.x == 0) AVEC_STAMP(9);
 }
 
 // Split-K fix-up: out = act(sum_{s in split order} partial_s + bias), zero
@@ -461,6 +473,16 @@ constexpr size_t smem_bytes() {
 }
 
 }  // namespace
+
+#ifdef AVEC_TRACE
+void conv_tc_trace(int on, cudaStream_t st) {
+  check_cuda(cudaMemcpyToSymbolAsync(g_trace_on, &on, sizeof on, 0, cudaMemcpyHostToDevice, st), "trace arm");
+  check_cuda(cudaStreamSynchronize(st), "trace arm");
+}
+int conv_tc_trace_dump(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 5;
+}
+#endif
 
 bool pdl_enabled() {
   static const bool on = [] {

@@ -629,8 +629,12 @@ struct PlanBuilder {
 
   // one launch covering 1 or 2 conv layers (sibling branches) of equal shape;
   // `pool`: the single output view is the 2x2-pooled result (level + 1)
+  // `spill`: the destination channels from the view's end up to the next
+  // multiple of 128 may be overwritten (a dense block's next slice, written by
+  // a later layer, or padding), which lets a 96-channel layer take the
+  // swap-AB kernel's 128-channel tiles
   void conv(std::initializer_list<int> layers_il, std::initializer_list<TensorView> ins,
-            std::initializer_list<TensorView> outs, bool pool = false) {
+            std::initializer_list<TensorView> outs, bool pool = false, bool spill = false) {
     std::vector<int> layers(layers_il);
     std::vector<TensorView> in(ins), out(outs);
     PlanOp op;
@@ -673,7 +677,20 @@ struct PlanBuilder {
       const char* e = std::getenv("AVEC_TC3");
       return e ? std::atoi(e) : 0;
     }();
-    const bool want_tc = L0.exec_k == 7 || (tc3 && L0.exec_k == 3 && L0.def.cout == 128 && L0.cin_pad >= 128);
+    // BODY_25's level-3 dense-block convs (3x3, 96/128 channels) on the
+    // swap-AB kernel (128 x 256 MMAs instead of the pixel-major N = 96/128
+    // ones). Measured at C5 and rejected, opt-in AVEC_TC_DENSE=1: 96-channel
+    // layers 96-107 -> 124-133 us (a quarter of every tile is padding), 128-
+    // channel layers 120 -> 125 us, the block's first convs 207/313 ->
+    // 271/323 us; all 90 launches 14.8 -> 16.0 ms (2 subs: 20.5 ms)
+    static const bool tc_dense = [] {
+      const char* e = std::getenv("AVEC_TC_DENSE");
+      return e && e[0] == '1';
+    }();
+    const bool dense_tc = tc_dense && spill && L0.exec_k == 3 && (L0.def.cout == 96 || L0.def.cout == 128) &&
+                          layers.size() == 1 && !pool && out[0].c_off + 128 <= out[0].c_stride;
+    const bool want_tc = L0.exec_k == 7 || dense_tc ||
+                         (tc3 && L0.exec_k == 3 && L0.def.cout == 128 && L0.cin_pad >= 128);
     bool tc_ok = want_tc && !to_output && !pool;
     for (size_t g = 0; g < layers.size(); ++g)
       tc_ok = tc_ok && out[g].c_off % 8 == 0 && out[g].level == in[g].level;
@@ -686,8 +703,9 @@ struct PlanBuilder {
     bool slab = !to_output;
     for (size_t g = 0; g < layers.size(); ++g) {
       const int cout = net.layers[layers[g]].def.cout;
-      slab = slab && (p.pixel_major || cout % 64 == 0) && out[g].c_off % 8 == 0 &&
-             out[g].c_off + round_up(cout, 8) <= out[g].c_stride && out[g].level == in[g].level + (pool ? 1 : 0);
+      const int span = !p.pixel_major && dense_tc ? 128 : round_up(cout, 8);
+      slab = slab && (p.pixel_major || cout % 64 == 0 || dense_tc) && out[g].c_off % 8 == 0 &&
+             out[g].c_off + span <= out[g].c_stride && out[g].level == in[g].level + (pool ? 1 : 0);
     }
     if (pool && (!slab || layers.size() != 1 || !p.pixel_major))
       fail(AVEC_ERR_UNSUPPORTED, "fused pooling needs one pixel-major slab output");
@@ -714,7 +732,12 @@ struct PlanBuilder {
       // 256-pixel tiles (double-buffered TMEM) when that leaves SMs idle
       const int per_img_units = int(layers.size()) * plan.n * p.m_tiles;  // tiles per pixel-tile index
       const int wide = per_img_units * ((p.H * p.Wp + 511) / 512);
+      static const int dense_subs = [] {
+        const char* e = std::getenv("AVEC_TC_DENSE_SUBS");
+        return e ? std::atoi(e) : 1;
+      }();
       p.subs = (L0.exec_k == 7 || tc3 == 3 || (tc3 == 1 && wide >= 2 * 148)) ? 2 : 1;
+      if (dense_tc) p.subs = dense_subs == 2 ? 2 : 1;
       // launches that will run split-K (wide tiles fill less than half the
       // SMs) take 256-pixel tiles: twice the tiles, half the split count, half
       // the fp32 partial traffic per tile. AVEC_SPLITK_NARROW=0 keeps 512.
@@ -922,9 +945,11 @@ void build_body25_plan(Plan& plan, const PoseNet& net, int device, cudaStream_t 
   auto stage = [&](TensorView in, int w, int c6, std::vector<TensorView> heads) {
     int X = X0, Y = Y0;
     for (int blk = 1; blk <= 5; ++blk) {
-      b.conv({li++}, {blk == 1 ? in : b.view(X, 0, 3 * w)}, {b.view(Y, 0, w)});
-      b.conv({li++}, {b.view(Y, 0, w)}, {b.view(Y, w, w)});
-      b.conv({li++}, {b.view(Y, w, w)}, {b.view(Y, 2 * w, w)});
+      // each layer may spill zeros past its slice: the next layer of the block
+      // overwrites them, the last one's land in the 3w..round_up(3w + 32) pad
+      b.conv({li++}, {blk == 1 ? in : b.view(X, 0, 3 * w)}, {b.view(Y, 0, w)}, false, true);
+      b.conv({li++}, {b.view(Y, 0, w)}, {b.view(Y, w, w)}, false, true);
+      b.conv({li++}, {b.view(Y, w, w)}, {b.view(Y, 2 * w, w)}, false, true);
       std::swap(X, Y);
     }
     const int l6 = li++, l7 = li++;  // Mconv6 (1x1, PReLU) + Mconv7 (1x1), fused
@@ -1315,9 +1340,9 @@ std::vector<OpProfile> posenet_profile(avec_ctx* ctx, uint64_t handle, uint32_t 
     for (size_t i = 0; i < nops; ++i) {
       check_cuda(cudaEventRecord(ev[i], s->stream), "event");
 #ifdef AVEC_TRACE
-      if (r == reps - 1 && int(i) == trace_op) conv_pm_trace(1, s->stream);
+      if (r == reps - 1 && int(i) == trace_op) conv_pm_trace(1, s->stream), conv_tc_trace(1, s->stream);
       run_ops(ctx, *plan, *m.net, i, i + 1, s->stream);
-      if (r == reps - 1 && int(i) == trace_op) conv_pm_trace(0, s->stream);
+      if (r == reps - 1 && int(i) == trace_op) conv_pm_trace(0, s->stream), conv_tc_trace(0, s->stream);
 #else
       run_ops(ctx, *plan, *m.net, i, i + 1, s->stream);
 #endif
@@ -1582,4 +1607,5 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
 #ifdef AVEC_TRACE
 // trace builds only: the stamps of the launch traced by avec_posenet_profile
 extern "C" int avec_trace_dump(unsigned long long* host, int n) { return avec::conv_pm_trace_dump(host, n); }
+extern "C" int avec_trace_dump_tc(unsigned long long* host, int n) { return avec::conv_tc_trace_dump(host, n); }
 #endif

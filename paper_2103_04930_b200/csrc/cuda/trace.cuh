@@ -17,9 +17,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// host side (conv_pm.cu): arm the next launches / read the stamps back
+// host side (conv_pm.cu, conv_tc.cu): arm the next launches / read the stamps back
 void conv_pm_trace(int on, cudaStream_t st);
 int conv_pm_trace_dump(unsigned long long* host, int n);
+void conv_tc_trace(int on, cudaStream_t st);
+int conv_tc_trace_dump(unsigned long long* host, int n);
 }  // namespace avec
 #define AVEC_STAMP(slot)                                                                  \
   do {                                                                                    \

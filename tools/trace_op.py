@@ -36,14 +36,15 @@ def main():
     prof = be.profile(h, dims, x.data_ptr(), reps=3)
     L = _lib.load()
     buf = (ctypes.c_ulonglong * (296 * 16))()
-    assert L.avec_trace_dump(buf, 296 * 16) == 0
+    dump = L.avec_trace_dump_tc if prof[a.op]["kind"] == "conv_tc" else L.avec_trace_dump
+    assert dump(buf, 296 * 16) == 0
     t = np.frombuffer(buf, dtype=np.uint64).reshape(296, 16).astype(np.float64)
     used = t[:, 0] > 0
     t = t[used]
     t0 = t[:, 0].min()
     print(f"op {a.op} ({prof[a.op]['kind']}, {prof[a.op]['ms'] * 1e3:.1f} us in the profile), {used.sum()} CTAs")
     names = ["entry", "prologue", "1st load issued", "producer done", "1st window landed", "mma done",
-             "acc ready (epi)", "stores issued", "stores done", "exit"]
+             "acc ready (epi)", "stores issued", "stores done", "exit"]  # conv_tc: no 2, 3
     for k, n in enumerate(names):
         v = t[:, k]
         v = v[v > 0] - t0
