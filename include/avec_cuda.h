@@ -108,6 +108,9 @@ int avec_forward_device(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, 
 typedef struct avec_stream avec_stream;
 int avec_stream_create(avec_ctx* ctx, avec_stream** out);
 void avec_stream_destroy(avec_stream* s);
+/* Build the stream's frame-group plans and staging for these dims ahead of
+ * time (avec_stream_begin would otherwise do it on the cycle's critical path). */
+int avec_stream_prepare(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w);
 int avec_stream_begin(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                       const float* in, float* out, uint64_t out_elems);
 int avec_stream_feed(avec_stream* s, uint64_t landed_bytes);

@@ -33,7 +33,7 @@ EXPORTS = [
     "avec_nms_device", "avec_posenet_layer_io", "avec_posenet_layer_rows", "avec_posenet_layer_out_level", "avec_posenet_layer_fusion", "avec_posenet_layer_info",
     "avec_posenet_num_layers", "avec_posenet_profile", "avec_posenet_synth_weights", "avec_host_alloc", "avec_host_free",
     "avec_paf_candidates_device", "avec_assemble_people", "avec_coco_limbs",
-    "avec_stream_create", "avec_stream_destroy", "avec_stream_begin", "avec_stream_feed", "avec_stream_finish",
+    "avec_stream_create", "avec_stream_destroy", "avec_stream_prepare", "avec_stream_begin", "avec_stream_feed", "avec_stream_finish",
     "avec_stream_abort",
 ]
 
@@ -85,6 +85,7 @@ def load() -> ctypes.CDLL:
         "avec_host_alloc": (vp, [u64]),
         "avec_stream_create": (i, [vp, c.POINTER(vp)]),
         "avec_stream_destroy": (None, [vp]),
+        "avec_stream_prepare": (i, [vp, u64, u32, u32, u32, u32]),
         "avec_stream_begin": (i, [vp, u64, u32, u32, u32, u32, vp, vp, u64]),
         "avec_stream_feed": (i, [vp, u64]),
         "avec_stream_finish": (i, [vp, c.POINTER(d)]),

@@ -338,6 +338,13 @@ void avec_stream_destroy(avec_stream* s) {
   }
 }
 
+int avec_stream_prepare(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w) {
+  return guarded([&] {
+    need(s, "stream");
+    avec::stream_prepare(s, handle, n, c, h, w);
+  });
+}
+
 int avec_stream_begin(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
                       const float* in, float* out, uint64_t out_elems) {
   return guarded([&] {

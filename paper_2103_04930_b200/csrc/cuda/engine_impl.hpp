@@ -189,6 +189,7 @@ int posenet_layer_out_level(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t
 // pipelined cycles (pipeline.cu, avec_stream_* in include/avec_cuda.h)
 avec_stream* stream_create(avec_ctx* ctx);
 void stream_destroy(avec_stream* s);
+void stream_prepare(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w);
 void stream_begin(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w, const float* in,
                   float* out, uint64_t out_elems);
 void stream_feed(avec_stream* s, uint64_t landed_bytes);

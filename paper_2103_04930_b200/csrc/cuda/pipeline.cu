@@ -171,6 +171,23 @@ void stream_destroy(avec_stream* s) {
   delete s;
 }
 
+void stream_prepare(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w) {
+  if (s->active) fail(AVEC_ERR_INVALID_ARGUMENT, "a pipelined cycle is active on this stream");
+  const Model m = model_lookup(s->ctx, handle);
+  const uint64_t E = uint64_t(n) * c * h * w;
+  const uint64_t K = output_elems_for(m, n, c, h, w);
+  check_cuda(cudaSetDevice(s->ctx->device), "cudaSetDevice");
+  if (m.kind == AVEC_MODEL_POSENET) {
+    int n_img = 0;
+    posenet_shape(m, n, c, h, w, n_img);
+    const int g = group_frames(n_img);
+    get_plan(s->ctx, &s->slot, m, g, int(h), int(w));
+    if (n_img % g) get_plan(s->ctx, &s->slot, m, n_img % g, int(h), int(w));
+  }
+  s->slot.d_in.ensure(E * 4, s->ctx->device);
+  s->slot.d_out.ensure(K * 4, s->ctx->device);
+}
+
 void stream_begin(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w, const float* in,
                   float* out, uint64_t out_elems) {
   if (s->active) fail(AVEC_ERR_INVALID_ARGUMENT, "a pipelined cycle is already active on this stream");

@@ -4,6 +4,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <functional>
+#include <set>
+#include <tuple>
 #include <stdexcept>
 #include <thread>
 
@@ -29,6 +31,52 @@ void check(int rc) {
 }
 
 }  // namespace
+
+// Pipelined cycles on one GPU run on a small pool of avec_streams shared by
+// all of the device's sessions (AVEC_PIPE_BUSY, default 1): group plans and
+// staging are built once per device and shape, not per session (a plan
+// build allocates hundreds of MB, and the driver serialises allocations
+// against every other session's work).
+//
+// A cycle is pipelined only while its GPU has nothing else to do: frame
+// groups trade some efficiency (smaller launches) for overlapping the
+// receive, which pays for one session but not when other sessions' whole
+// batches already keep the GPU busy (measured C2, 4 sessions: 2567 -> 2067
+// frames/s when every cycle was pipelined).
+struct B200Backend::PipePool {
+  using Key = std::tuple<std::uint64_t, std::uint32_t, std::uint32_t, std::uint32_t, std::uint32_t>;
+  avec_ctx* ctx = nullptr;
+  int cap = 1;
+  std::mutex m;
+  std::vector<avec_stream*> streams;
+  std::vector<char> held;            // a cycle or a preparation owns the stream
+  std::vector<std::set<Key>> ready;  // shapes each stream is prepared for
+  ~PipePool() {
+    for (auto* s : streams) avec_stream_destroy(s);
+  }
+  // a free stream (creating one below the cap); -1 if none. With `key`, only
+  // a stream already prepared for it.
+  int acquire(const Key* key) {
+    std::lock_guard<std::mutex> lk(m);
+    for (size_t i = 0; i < streams.size(); ++i)
+      if (!held[i] && (!key || ready[i].count(*key))) {
+        held[i] = 1;
+        return int(i);
+      }
+    if (key || int(streams.size()) >= cap) return -1;
+    avec_stream* s = nullptr;
+    if (avec_stream_create(ctx, &s) != AVEC_OK) return -1;
+    streams.push_back(s);
+    held.push_back(1);
+    ready.emplace_back();
+    return int(streams.size()) - 1;
+  }
+  void release(int i) {
+    std::lock_guard<std::mutex> lk(m);
+    held[i] = 0;
+  }
+};
+
 
 std::vector<FrameGroup> frame_groups(std::uint64_t frames, int groups) {
   std::vector<FrameGroup> out;
@@ -65,6 +113,15 @@ B200Backend::B200Backend(std::vector<int> devices, int slots_per_device, Policy 
   pipelines_.reset(new std::atomic<int>[ctx_.size()]);
   streaming_.reset(new std::atomic<int>[ctx_.size()]);
   for (size_t i = 0; i < ctx_.size(); ++i) inflight_[i] = pipelines_[i] = streaming_[i] = 0;
+  static const int cap = [] {
+    const char* e = std::getenv("AVEC_PIPE_BUSY");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  for (auto* c : ctx_) {
+    pools_.push_back(std::make_unique<PipePool>());
+    pools_.back()->ctx = c;
+    pools_.back()->cap = cap;
+  }
   if (const char* e = std::getenv("AVEC_PIPELINE")) pipelining_ = e[0] != '0';
   label_ = ctx_.size() == 1 ? std::string(avec_ctx_label(ctx_[0]))
                             : "b200x" + std::to_string(ctx_.size()) +
@@ -74,6 +131,7 @@ B200Backend::B200Backend(std::vector<int> devices, int slots_per_device, Policy 
 }
 
 B200Backend::~B200Backend() {
+  pools_.clear();  // streams before their contexts
   for (auto* c : ctx_) avec_ctx_destroy(c);
 }
 
@@ -178,62 +236,88 @@ double B200Backend::forward_session(std::uint64_t session, ModelHandle model, co
 
 namespace {
 
-// avec_stream on one GPU: the backend's model handle maps to that context's
-// A cycle is pipelined only while its GPU has nothing else to do: frame
-// groups trade some efficiency (smaller launches) for overlapping the
-// receive, which pays for one session but not when other sessions' whole
-// batches already keep the GPU busy (measured C2, 4 sessions: 2567 -> 2067
-// frames/s when every cycle was pipelined).
 class B200Pipeline final : public Pipeline {
  public:
-  B200Pipeline(avec_ctx* ctx, std::function<std::uint64_t(ModelHandle)> handle_of, std::atomic<int>* open,
-               std::atomic<int>* active, std::atomic<int>* inflight)
-      : handle_of_(std::move(handle_of)), open_(open), active_(active), inflight_(inflight) {
-    check(avec_stream_create(ctx, &s_));
+  B200Pipeline(B200Backend::PipePool* pool, std::function<std::uint64_t(ModelHandle)> handle_of,
+               std::atomic<int>* open, std::atomic<int>* active, std::atomic<int>* inflight)
+      : pool_(pool), handle_of_(std::move(handle_of)), open_(open), active_(active), inflight_(inflight) {
     ++*open_;
   }
   ~B200Pipeline() override {
-    if (running_) --*active_;
-    avec_stream_destroy(s_);
+    if (held_ >= 0) {
+      avec_stream_abort(pool_->streams[held_]);
+      release();
+    }
     --*open_;
   }
   bool begin(ModelHandle model, const wire::Dims& d, const float* in, float* out, std::uint64_t n_out) override {
-    if (inflight_->load() > 0) return false;
-    if (active_->fetch_add(1) > 0) {  // another session's cycle is pipelined on this GPU
+    // at most `cap` cycles (dispatched or pipelined) on this GPU
+    if (inflight_->load() >= pool_->cap) return false;
+    if (active_->fetch_add(1) + inflight_->load() >= pool_->cap) {
       --*active_;
       return false;
     }
-    running_ = true;
-    const int rc = avec_stream_begin(s_, handle_of_(model), d.batch, d.channels, d.height, d.width, in, out, n_out);
+    const auto key = key_of(model, d);
+    held_ = pool_->acquire(&key);
+    if (held_ < 0) {
+      --*active_;
+      return false;
+    }
+    const int rc =
+        avec_stream_begin(pool_->streams[held_], handle_of_(model), d.batch, d.channels, d.height, d.width, in, out, n_out);
     if (rc != AVEC_OK) {
       release();
       rethrow(rc);
     }
     return true;
   }
-  void feed(std::uint64_t landed) override { check(avec_stream_feed(s_, landed)); }
+  void prepare(ModelHandle model, const wire::Dims& d) override {
+    const auto key = key_of(model, d);
+    for (int tries = 0; tries < pool_->cap; ++tries) {
+      const int i = pool_->acquire(nullptr);
+      if (i < 0) return;  // all streams busy: prepared next time
+      const bool have = pool_->ready[i].count(key) > 0;
+      int rc = AVEC_OK;
+      if (!have)
+        rc = avec_stream_prepare(pool_->streams[i], handle_of_(model), d.batch, d.channels, d.height, d.width);
+      if (rc == AVEC_OK && !have) {
+        std::lock_guard<std::mutex> lk(pool_->m);
+        pool_->ready[i].insert(key);
+      }
+      pool_->release(i);
+      check(rc);
+      if (have) return;
+    }
+  }
+  void feed(std::uint64_t landed) override { check(avec_stream_feed(pool_->streams[held_], landed)); }
   double finish() override {
     double secs = 0;
-    const int rc = avec_stream_finish(s_, &secs);
+    const int rc = avec_stream_finish(pool_->streams[held_], &secs);
     release();
     check(rc);
     return secs;
   }
   void abort() override {
-    const int rc = avec_stream_abort(s_);
+    const int rc = held_ >= 0 ? avec_stream_abort(pool_->streams[held_]) : AVEC_OK;
     release();
     check(rc);
   }
 
  private:
-  void release() {
-    if (running_) --*active_;
-    running_ = false;
+  B200Backend::PipePool::Key key_of(ModelHandle m, const wire::Dims& d) const {
+    return {handle_of_(m), d.batch, d.channels, d.height, d.width};
   }
-  avec_stream* s_ = nullptr;
+  void release() {
+    if (held_ >= 0) {
+      pool_->release(held_);
+      --*active_;
+    }
+    held_ = -1;
+  }
+  B200Backend::PipePool* pool_;
   std::function<std::uint64_t(ModelHandle)> handle_of_;
   std::atomic<int>*open_, *active_, *inflight_;
-  bool running_ = false;
+  int held_ = -1;
 };
 
 }  // namespace
@@ -249,7 +333,7 @@ std::unique_ptr<Pipeline> B200Backend::open_pipeline(std::uint64_t session) {
       if (pipelines_[i].load() < pipelines_[dev].load()) dev = int(i);
   }
   return std::make_unique<B200Pipeline>(
-      ctx_[dev], [this, dev](ModelHandle h) { return lookup(h).per_device[dev]; }, &pipelines_[dev],
+      pools_[dev].get(), [this, dev](ModelHandle h) { return lookup(h).per_device[dev]; }, &pipelines_[dev],
       &streaming_[dev], &inflight_[dev]);
 }
 

@@ -60,6 +60,7 @@ class B200Backend final : public Backend {
   void free_host(void* p) override;
 
   int device_count() const { return int(ctx_.size()); }
+  struct PipePool;  // per-GPU avec_streams of pipelined cycles (b200_backend.cpp)
   int devices() const override { return int(ctx_.size()); }
 
  private:
@@ -80,6 +81,7 @@ class B200Backend final : public Backend {
   std::unique_ptr<std::atomic<int>[]> inflight_;
   std::unique_ptr<std::atomic<int>[]> pipelines_;  // open pipelines per device (placement)
   std::unique_ptr<std::atomic<int>[]> streaming_;  // pipelined cycles running per device
+  std::vector<std::unique_ptr<PipePool>> pools_;
   bool pipelining_ = true;                          // AVEC_PIPELINE=0 disables
   std::mutex m_;
   std::map<wire::Digest, std::uint64_t> id_by_digest_;

@@ -57,6 +57,9 @@ class Pipeline {
   // false: declined (e.g. the device is busy with other cycles, where whole
   // batches use it better); the cycle then takes the dispatcher's normal path
   virtual bool begin(ModelHandle model, const wire::Dims& dims, const float* in, float* out, std::uint64_t n_out) = 0;
+  // build what a cycle of these dims needs (plans, staging) off the critical
+  // path; the server calls it from a helper thread before speculating
+  virtual void prepare(ModelHandle /*model*/, const wire::Dims& /*dims*/) {}
   virtual void feed(std::uint64_t landed_bytes) = 0;
   virtual double finish() = 0;  // blocks; device compute seconds of the cycle
   virtual void abort() = 0;

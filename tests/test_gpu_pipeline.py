@@ -101,7 +101,8 @@ def test_server_pipelines_repeat_cycles(tmp_path):
     size are pipelined while their frames arrive, as two 4-frame groups (the
     server logs `cycle_pipelined`). Each reply equals the C-ABI forward of
     those frame groups bit for bit, and here also the whole-batch forward:
-    the 4-frame plan keeps every conv on the same kernels and K order."""
+    the 4-frame plan keeps every conv on the same kernels and K order, so
+    every cycle is checked against both whatever path it took."""
     import pathlib
     import subprocess
     import json
@@ -110,7 +111,7 @@ def test_server_pipelines_repeat_cycles(tmp_path):
     root = pathlib.Path(__file__).resolve().parent.parent
     spec = tmp_path / "coco.spec"
     spec.write_bytes(netspec.spec())
-    w, h, nb, cycles = 656, 368, 8, 3
+    w, h, nb, cycles = 656, 368, 8, 4
     log = tmp_path / "events.jsonl"
     srv = W.ServerProc([str(root / "paper_2103_04930_b200" / "bin" / "avec-server"), "--slots", "1", "--log",
                         str(log)])
@@ -130,13 +131,12 @@ def test_server_pipelines_repeat_cycles(tmp_path):
     for c in range(cycles):
         frames = O.batched_frame(w, h, nb, seed=7, first=c * nb).reshape(nb, -1)
         whole = be.forward(hd, Frame(Dims(1, 3 * nb, h, w), frames.ravel())).data
-        if c == 0:
-            assert got[c].tobytes() == whole.tobytes()
-            continue
+        assert got[c].tobytes() == whole.tobytes(), c
         for f0 in (0, 4):
             grp = be.forward(hd, Frame(Dims(1, 12, h, w), frames[f0:f0 + 4].ravel())).data
             assert got[c, f0 * per:(f0 + 4) * per].tobytes() == grp.tobytes(), (c, f0)
-        assert got[c].tobytes() == whole.tobytes()
     be.close()
+    # speculation starts once a helper thread has prepared the pipeline after
+    # the first cycle, so the second cycle may still run whole
     events = [json.loads(l)["event"] for l in log.read_text().splitlines() if l.strip()]
-    assert events.count("cycle_pipelined") == cycles - 1
+    assert cycles - 2 <= events.count("cycle_pipelined") <= cycles - 1

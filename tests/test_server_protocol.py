@@ -343,5 +343,10 @@ def test_pipelined_cycle_speculation():
         out = srv.stop()
     line = next(l for l in out.splitlines() if l.startswith("pipeline "))
     counts = dict(zip(line.split()[1::2], map(int, line.split()[2::2])))
-    assert counts == {"begins": 5, "feeds": counts["feeds"], "finishes": 4, "aborts": 1}, counts
-    assert counts["feeds"] >= 5
+    # speculation starts once the helper thread has prepared the pipeline for
+    # the session's last cycle; with the stub that is immediate, so normally
+    # cycles 2, 3, 4 (dropped), 5 and 7 speculate -- allow a slow helper thread
+    # to skip one, never a guess that is not dropped or finished
+    assert counts["begins"] == counts["finishes"] + counts["aborts"], counts
+    assert counts["aborts"] == 1 and 3 <= counts["finishes"] <= 4, counts
+    assert counts["feeds"] >= counts["begins"]
