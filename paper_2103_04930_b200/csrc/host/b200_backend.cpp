@@ -33,15 +33,16 @@ void check(int rc) {
 }  // namespace
 
 // Pipelined cycles on one GPU run on a small pool of avec_streams shared by
-// all of the device's sessions (AVEC_PIPE_BUSY, default 1): group plans and
+// all of the device's sessions (AVEC_PIPE_BUSY, default 2): group plans and
 // staging are built once per device and shape, not per session (a plan
 // build allocates hundreds of MB, and the driver serialises allocations
 // against every other session's work).
 //
-// A cycle is pipelined only while its GPU has nothing else to do: frame
-// groups trade some efficiency (smaller launches) for overlapping the
-// receive, which pays for one session but not when other sessions' whole
-// batches already keep the GPU busy (measured C2, 4 sessions: 2567 -> 2067
+// A cycle is pipelined only while its GPU has at most one other cycle to do
+// (and the server at most 2 sessions per GPU): frame groups trade some
+// efficiency (smaller launches) for overlapping the receive, which pays while
+// the GPU would otherwise wait for the network, not when other sessions'
+// whole batches keep it busy (measured C2, 4 sessions on 1 GPU: 2567 -> 2067
 // frames/s when every cycle was pipelined).
 struct B200Backend::PipePool {
   using Key = std::tuple<std::uint64_t, std::uint32_t, std::uint32_t, std::uint32_t, std::uint32_t>;
@@ -115,7 +116,7 @@ B200Backend::B200Backend(std::vector<int> devices, int slots_per_device, Policy 
   for (size_t i = 0; i < ctx_.size(); ++i) inflight_[i] = pipelines_[i] = streaming_[i] = 0;
   static const int cap = [] {
     const char* e = std::getenv("AVEC_PIPE_BUSY");
-    return e ? std::max(1, std::atoi(e)) : 1;
+    return e ? std::max(1, std::atoi(e)) : 2;
   }();
   for (auto* c : ctx_) {
     pools_.push_back(std::make_unique<PipePool>());
