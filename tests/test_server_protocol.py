@@ -350,3 +350,36 @@ def test_pipelined_cycle_speculation():
     assert counts["begins"] == counts["finishes"] + counts["aborts"], counts
     assert counts["aborts"] == 1 and 3 <= counts["finishes"] <= 4, counts
     assert counts["feeds"] >= counts["begins"]
+
+
+def test_pipelined_session_disconnect_mid_frame():
+    """A session whose speculative cycle is streaming when the client vanishes
+    (half a FrameData sent, then close) must not take the server down or leak
+    into the next session; the next session's cycles stay exact."""
+    _ensure_built()
+    srv = W.ServerProc([str(STUB), "--print-forward-log", "--pipeline"])
+    try:
+        p = _ready(srv, c=2.0)
+        data = np.random.default_rng(1).random(64 * 32 * 3, dtype=np.float32)
+        p.send(W.frame_data(data) + W.resolution(64, 32) + W.frame_size(data.size))
+        assert p.recv_msg()[0] == "forward_result"
+        import time
+        time.sleep(0.2)  # the helper thread prepares the pipeline
+        frame = W.frame_data(data)
+        p.send(frame[: len(frame) // 2])  # speculation starts, then the peer goes away
+        time.sleep(0.1)
+        p.close()
+        q = _ready(srv, c=2.0)
+        for k in range(3):
+            d = np.random.default_rng(10 + k).random(64 * 32 * 3, dtype=np.float32)
+            q.send(W.frame_data(d) + W.resolution(64, 32) + W.frame_size(d.size))
+            tag, payload = q.recv_msg()
+            assert tag == "forward_result"
+            assert W.forward_result(payload)[1].tobytes() == O.mockpose_forward(d, 2.0).tobytes()
+        q.close()
+        assert srv.p.poll() is None
+    finally:
+        out = srv.stop()
+    line = next(l for l in out.splitlines() if l.startswith("pipeline "))
+    counts = dict(zip(line.split()[1::2], map(int, line.split()[2::2])))
+    assert counts["begins"] >= 2  # the abandoned speculation and the second session's
