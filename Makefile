@@ -21,7 +21,7 @@ HOST_SRCS := $(filter-out $(HOST_DIR)/%_main.cpp,$(wildcard $(HOST_DIR)/*.cpp))
 HOST_HDRS := $(wildcard $(HOST_DIR)/*.hpp) include/avec_cuda.h
 HOST_OBJS := $(patsubst $(HOST_DIR)/%.cpp,build/obj/host/%.o,$(HOST_SRCS))
 
-.PHONY: all product oracle probe clean
+.PHONY: all product oracle probe clean tsan
 all: product oracle probe
 
 product: $(LIB)/libavec_cuda.so $(LIB)/libavec_host.so $(BIN)/avec-server $(BIN)/avec-loadgen
@@ -63,6 +63,16 @@ build/avec_stub_server: tests/native/stub_server.cpp $(LIB)/libavec_host.so
 oracle: $(LIB)/libavec_cuda.so
 	$(MAKE) -C oracle oracle
 	@if [ -d /root/reference/proj ]; then $(MAKE) -C oracle ref; else echo "no /root/reference: using prebuilt oracle/_ref"; fi
+
+# ThreadSanitizer build of the host server (libavec_host sources + the CPU
+# stub backend) for the protocol tests: AVEC_STUB_BIN=build/tsan/avec_stub_server
+TSAN_CXX ?= /usr/bin/g++
+TSAN_FLAGS := -std=c++20 -O1 -g -fsanitize=thread -fPIC -I/usr/local/cuda/include -Iinclude
+build/tsan/avec_stub_server: tests/native/stub_server.cpp $(HOST_SRCS) $(HOST_HDRS) $(LIB)/libavec_cuda.so
+	@mkdir -p build/tsan
+	$(TSAN_CXX) $(TSAN_FLAGS) -I$(HOST_DIR) -o $@ tests/native/stub_server.cpp $(HOST_SRCS) -L$(LIB) -lavec_cuda \
+	  -Wl,-rpath,'$$ORIGIN/../../$(LIB)' -l:libcrypto.a -lpthread
+tsan: build/tsan/avec_stub_server
 
 probe: build/tc_probe build/tc2_probe build/tma3d_probe
 build/tc_probe: tests/native/tc_probe.cu $(CUDA_DIR)/ptx.cuh

@@ -245,23 +245,30 @@ TcpListener::TcpListener(const std::string& host, std::uint16_t port) {
   port_ = ntohs(b.sin_port);
 }
 
-TcpListener::~TcpListener() { close(); }
+TcpListener::~TcpListener() {
+  close();
+  if (fd_ >= 0) ::close(fd_);
+  fd_ = -1;
+}
 
 std::unique_ptr<Stream> TcpListener::accept() {
   for (;;) {
+    if (closed_.load()) return nullptr;
     const int c = ::accept(fd_, nullptr, nullptr);
-    if (c >= 0) return std::make_unique<TcpStream>(c);
+    if (c >= 0) {
+      if (closed_.load()) {
+        ::close(c);
+        return nullptr;
+      }
+      return std::make_unique<TcpStream>(c);
+    }
     if (errno == EINTR) continue;
     return nullptr;
   }
 }
 
 void TcpListener::close() {
-  if (fd_ >= 0) {
-    ::shutdown(fd_, SHUT_RDWR);
-    ::close(fd_);
-    fd_ = -1;
-  }
+  if (!closed_.exchange(true) && fd_ >= 0) ::shutdown(fd_, SHUT_RDWR);  // wakes accept()
 }
 
 StreamPair make_pipe() {

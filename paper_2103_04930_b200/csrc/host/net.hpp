@@ -9,6 +9,7 @@
 
 #include <sys/uio.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -48,10 +49,14 @@ class TcpListener {
   TcpListener& operator=(const TcpListener&) = delete;
   std::uint16_t port() const { return port_; }
   std::unique_ptr<Stream> accept();  // nullptr once closed
+  // wakes a blocked accept (from any thread); the descriptor itself is
+  // released by the destructor, after the accepting thread is gone, so it
+  // can never be reused under a concurrent accept
   void close();
 
  private:
-  int fd_ = -1;
+  int fd_ = -1;  // set in the constructor, released in the destructor
+  std::atomic<bool> closed_{false};
   std::uint16_t port_ = 0;
 };
 

@@ -18,7 +18,9 @@ import oracle_lib as O
 import wire_client as W
 
 ROOT = pathlib.Path(__file__).resolve().parent.parent
-STUB = ROOT / "build" / "avec_stub_server"
+# AVEC_STUB_BIN: another build of the stub server (e.g. the ThreadSanitizer
+# one from `make tsan`)
+STUB = pathlib.Path(__import__("os").environ.get("AVEC_STUB_BIN", ROOT / "build" / "avec_stub_server"))
 REF_CLIENT = ROOT / "oracle" / "_ref" / "ref_client"
 
 
