@@ -225,7 +225,7 @@ int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, 
     if (planes < 1 || h < 1 || w < 1 || max_peaks < 1) avec::fail(AVEC_ERR_INVALID_ARGUMENT, "bad nms shape");
     avec::check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
     std::lock_guard<std::mutex> lk(ctx->post_m);
-    const size_t need_bytes = avec::nms_scratch_bytes(planes, h, w);
+    const size_t need_bytes = avec::nms_scratch_bytes(planes, h, w, max_peaks);
     ctx->scratch.ensure(need_bytes, ctx->device);
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     avec::launch_nms(d_in, planes, h, w, threshold, max_peaks, d_counts, d_peaks, ctx->scratch.p,

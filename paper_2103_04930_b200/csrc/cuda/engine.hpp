@@ -63,6 +63,6 @@ void launch_upsample(const float* d_in, int planes, int h, int w, int scale, flo
 void launch_nms(const float* d_in, int planes, int H, int W, float threshold, int max_peaks,
                 int* d_counts, float* d_peaks, void* d_scratch, size_t scratch_bytes,
                 cudaStream_t stream);
-size_t nms_scratch_bytes(int planes, int H, int W);
+size_t nms_scratch_bytes(int planes, int H, int W, int max_peaks);
 
 }  // namespace avec

@@ -219,14 +219,32 @@ __device__ __forceinline__ unsigned nms_tile_peaks(const float* tile, int W, int
     row[k][1] = c.x; row[k][2] = c.y; row[k][3] = c.z; row[k][4] = c.w;
     row[k][5] = 4 * x4 + 4 < W ? t[4] : NEG;
   }
+  // "strictly greater than all 8 neighbours" as one comparison with their
+  // maximum, built from shared pairwise maxima; max.NaN propagates a NaN
+  // neighbour so it still blocks the peak, as in the oracle's comparisons
+  auto mx = [](float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+  };
+  float h0[4], h2[4];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float* a = row[2 * k];
+    float pr[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) pr[i] = mx(a[i], a[i + 1]);
+    float* h = k ? h2 : h0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = mx(pr[i], a[i + 2]);
+  }
   unsigned m = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const float v = row[1][i + 1];
     mid[i] = v;
-    const bool pk = v > threshold && v > row[0][i] && v > row[0][i + 1] && v > row[0][i + 2] && v > row[1][i] &&
-                    v > row[1][i + 2] && v > row[2][i] && v > row[2][i + 1] && v > row[2][i + 2];
-    m |= pk ? (1u << i) : 0u;
+    const float nb = mx(mx(h0[i], h2[i]), mx(row[1][i], row[1][i + 2]));
+    m |= (v > threshold && v > nb) ? (1u << i) : 0u;
   }
   return m;
 }
@@ -448,6 +466,137 @@ __global__ void nms4_onepass_kernel(const float* __restrict__ in, int H, int W, 
   }
 }
 
+// Tile-compact NMS (W % 4 == 0, default). Pass 1 reads the heatmaps once:
+// every 8-row tile (one bulk async copy) finds its peaks and writes the
+// first `cap` of them, in raster order, to its own slot of a scratch list
+// together with its peak count -- no block ever waits for another. Pass 2
+// (one small block per plane) scans the tile counts and gathers the plane's
+// first max_peaks peaks in raster order, refining each from its 3x3
+// neighbourhood. Same peak test and refinement arithmetic as the two-pass
+// kernels (bit-exact against the oracle).
+struct NmsPeak {
+  int x, y;
+  float score;
+};
+
+__global__ void nms4_tiles_kernel(const float* __restrict__ in, int H, int W, float threshold, int cap,
+                                  int* __restrict__ tile_counts, NmsPeak* __restrict__ tile_peaks) {
+  extern __shared__ __align__(16) float tile[];
+  __shared__ int wbase[kNmsRows1][32];
+  __shared__ __align__(8) uint64_t bar;
+  const int tiles = gridDim.x, tt = blockIdx.x, pl = blockIdx.y;
+  const int y0 = tt * kNmsRows1;
+  const int rows = y0 + kNmsRows1 < H ? kNmsRows1 : H - y0;
+  const float* p = in + static_cast<size_t>(pl) * H * W;
+  const int ya = y0 > 0 ? y0 - 1 : 0, yb = y0 + rows < H ? y0 + rows + 1 : H;  // in-plane rows [ya, yb)
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = static_cast<uint32_t>(yb - ya) * W * 4;
+    ptx::mbar_arrive_expect_tx(&bar, bytes);
+    ptx::bulk_load(tile + (ya - (y0 - 1)) * W, p + static_cast<size_t>(ya) * W, bytes, &bar);
+  }
+  {
+    const float NEG = -__int_as_float(0x7f800000);
+    if (y0 == 0)
+      for (int i = threadIdx.x; i < W; i += blockDim.x) tile[i] = NEG;
+    if (y0 + rows == H)
+      for (int i = threadIdx.x; i < W; i += blockDim.x) tile[(rows + 1) * W + i] = NEG;
+  }
+  ptx::mbar_wait(&bar, 0);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int x4 = threadIdx.x;  // blockDim covers W / 4 columns
+  uint64_t masks = 0;
+  for (int r = 0; r < rows; ++r) {
+    float mid[4];
+    const unsigned m = nms_tile_peaks(tile, W, r, x4, threshold, mid);
+    masks |= static_cast<uint64_t>(m) << (4 * r);
+    int c = __popc(m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) wbase[r][wid] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // raster order = row-major over (row, warp)
+    int acc = 0;
+    for (int r = 0; r < rows; ++r)
+      for (int w = 0; w < nw; ++w) {
+        const int c = wbase[r][w];
+        wbase[r][w] = acc;
+        acc += c;
+      }
+    tile_counts[static_cast<size_t>(pl) * tiles + tt] = acc;
+  }
+  __syncthreads();
+  NmsPeak* out = tile_peaks + (static_cast<size_t>(pl) * tiles + tt) * cap;
+  for (int r = 0; r < rows; ++r) {
+    const unsigned m = static_cast<unsigned>(masks >> (4 * r)) & 15u;
+    if (!__any_sync(0xffffffffu, m)) continue;  // typical heatmaps: most warp rows have no peak
+    const int mine = __popc(m);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int idx = wbase[r][wid] + incl - mine;
+    for (int i = 0; i < 4 && idx < cap; ++i) {
+      if (!((m >> i) & 1u)) continue;
+      const int x = 4 * x4 + i;
+      out[idx] = NmsPeak{x, y0 + r, tile[(r + 1) * W + x]};
+      ++idx;
+    }
+  }
+}
+
+__global__ void nms_gather_kernel(const float* __restrict__ in, int H, int W, int tiles, int cap, int max_peaks,
+                                  const int* __restrict__ tile_counts, const NmsPeak* __restrict__ tile_peaks,
+                                  int* __restrict__ counts, float* __restrict__ peaks) {
+  extern __shared__ int base[];  // tiles + 1 exclusive prefix
+  const int pl = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int t = 0; t < tiles; ++t) {
+      base[t] = acc;
+      acc += tile_counts[static_cast<size_t>(pl) * tiles + t];
+    }
+    base[tiles] = acc;
+    counts[pl] = acc < max_peaks ? acc : max_peaks;
+  }
+  __syncthreads();
+  const int n = base[tiles] < max_peaks ? base[tiles] : max_peaks;
+  const float* p = in + static_cast<size_t>(pl) * H * W;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int lo = 0, hi = tiles;  // the tile holding peak i: base[lo] <= i < base[lo + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (base[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    const NmsPeak pk = tile_peaks[(static_cast<size_t>(pl) * tiles + lo) * cap + (i - base[lo])];
+    float sw = 0.0f, sx = 0.0f, sy = 0.0f;
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int yy = pk.y + dy, xx = pk.x + dx;
+        if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+        const float sv = __ldg(p + static_cast<size_t>(yy) * W + xx);
+        sw = __fadd_rn(sw, sv);
+        sx = __fadd_rn(sx, __fmul_rn(static_cast<float>(xx), sv));
+        sy = __fadd_rn(sy, __fmul_rn(static_cast<float>(yy), sv));
+      }
+    float* o = peaks + (static_cast<size_t>(pl) * max_peaks + i) * 5;
+    o[0] = static_cast<float>(pk.x);
+    o[1] = static_cast<float>(pk.y);
+    o[2] = __fdiv_rn(sx, sw);
+    o[3] = __fdiv_rn(sy, sw);
+    o[4] = pk.score;
+  }
+}
+
 // pass 1: per (plane, row) peak counts
 __global__ void nms_count_kernel(const float* __restrict__ in, int H, int W, float threshold,
                                  int* __restrict__ row_counts) {
@@ -563,14 +712,17 @@ void launch_upsample(const float* d_in, int planes, int h, int w, int scale, flo
   check_cuda(cudaGetLastError(), "upsample launch");
 }
 
-size_t nms_scratch_bytes(int planes, int H, int /*W*/) {
-  return 2 * static_cast<size_t>(planes) * H * sizeof(int);
+size_t nms_scratch_bytes(int planes, int H, int /*W*/, int max_peaks) {
+  // two-pass row counts/offsets, or the tile-compact path's counts + peak lists
+  const size_t tiles = (static_cast<size_t>(H) + kNmsRows1 - 1) / kNmsRows1;
+  const size_t compact = static_cast<size_t>(planes) * tiles * (sizeof(int) + sizeof(NmsPeak) * max_peaks) + 64;
+  return std::max(2 * static_cast<size_t>(planes) * H * sizeof(int), compact);
 }
 
 void launch_nms(const float* d_in, int planes, int H, int W, float threshold, int max_peaks,
                 int* d_counts, float* d_peaks, void* d_scratch, size_t scratch_bytes,
                 cudaStream_t stream) {
-  if (scratch_bytes < nms_scratch_bytes(planes, H, W)) fail(AVEC_ERR_INVALID_ARGUMENT, "nms scratch");
+  if (scratch_bytes < nms_scratch_bytes(planes, H, W, max_peaks)) fail(AVEC_ERR_INVALID_ARGUMENT, "nms scratch");
   if (H > 65535 || planes > 65535) fail(AVEC_ERR_UNSUPPORTED, "nms grid limits");
   int* row_counts = static_cast<int*>(d_scratch);
   int* row_offsets = row_counts + static_cast<size_t>(planes) * H;
@@ -591,6 +743,24 @@ void launch_nms(const float* d_in, int planes, int H, int W, float threshold, in
       const char* e = std::getenv("AVEC_NMS_TWOPASS");
       return e && e[0] == '1';
     }();
+    static const int mode = [] {  // 0 tile-compact (default), 1 one-pass look-back
+      const char* e = std::getenv("AVEC_NMS_LOOKBACK");
+      return e && e[0] == '1' ? 1 : 0;
+    }();
+    if (!two_pass && mode == 0 && (reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && max_peaks > 0) {
+      if (tile1_bytes > 48 * 1024)
+        check_cuda(cudaFuncSetAttribute(nms4_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(tile1_bytes)), "nms smem");
+      int* tile_counts = static_cast<int*>(d_scratch);
+      auto* tile_peaks = reinterpret_cast<NmsPeak*>(
+          reinterpret_cast<uintptr_t>(tile_counts + static_cast<size_t>(planes) * tiles1 + 15) & ~uintptr_t(15));
+      nms4_tiles_kernel<<<dim3(tiles1, planes), threads, tile1_bytes, stream>>>(d_in, H, W, threshold, max_peaks,
+                                                                                 tile_counts, tile_peaks);
+      nms_gather_kernel<<<planes, 128, (tiles1 + 1) * sizeof(int), stream>>>(d_in, H, W, tiles1, max_peaks, max_peaks,
+                                                                            tile_counts, tile_peaks, d_counts, d_peaks);
+      check_cuda(cudaGetLastError(), "nms launch");
+      return;
+    }
     if (!two_pass && (reinterpret_cast<uintptr_t>(d_in) & 15) == 0) {
       if (tile1_bytes > 48 * 1024)
         check_cuda(cudaFuncSetAttribute(nms4_onepass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
