@@ -21,7 +21,7 @@ HOST_SRCS := $(filter-out $(HOST_DIR)/%_main.cpp,$(wildcard $(HOST_DIR)/*.cpp))
 HOST_HDRS := $(wildcard $(HOST_DIR)/*.hpp) include/avec_cuda.h
 HOST_OBJS := $(patsubst $(HOST_DIR)/%.cpp,build/obj/host/%.o,$(HOST_SRCS))
 
-.PHONY: all product oracle probe clean tsan
+.PHONY: all product oracle probe clean tsan asan
 all: product oracle probe
 
 product: $(LIB)/libavec_cuda.so $(LIB)/libavec_host.so $(BIN)/avec-server $(BIN)/avec-loadgen
@@ -73,6 +73,14 @@ build/tsan/avec_stub_server: tests/native/stub_server.cpp $(HOST_SRCS) $(HOST_HD
 	$(TSAN_CXX) $(TSAN_FLAGS) -I$(HOST_DIR) -o $@ tests/native/stub_server.cpp $(HOST_SRCS) -L$(LIB) -lavec_cuda \
 	  -Wl,-rpath,'$$ORIGIN/../../$(LIB)' -l:libcrypto.a -lpthread
 tsan: build/tsan/avec_stub_server
+
+# AddressSanitizer + UBSan build of the same (AVEC_STUB_BIN=build/asan/avec_stub_server)
+ASAN_FLAGS := -std=c++20 -O1 -g -fsanitize=address,undefined -fno-omit-frame-pointer -fPIC -I/usr/local/cuda/include -Iinclude
+build/asan/avec_stub_server: tests/native/stub_server.cpp $(HOST_SRCS) $(HOST_HDRS) $(LIB)/libavec_cuda.so
+	@mkdir -p build/asan
+	$(TSAN_CXX) $(ASAN_FLAGS) -I$(HOST_DIR) -o $@ tests/native/stub_server.cpp $(HOST_SRCS) -L$(LIB) -lavec_cuda \
+	  -Wl,-rpath,'$$ORIGIN/../../$(LIB)' -l:libcrypto.a -lpthread
+asan: build/asan/avec_stub_server
 
 probe: build/tc_probe build/tc2_probe build/tma3d_probe
 build/tc_probe: tests/native/tc_probe.cu $(CUDA_DIR)/ptx.cuh
