@@ -222,6 +222,8 @@ void stream_begin(avec_stream* s, uint64_t handle, uint32_t n, uint32_t c, uint3
 
 void stream_feed(avec_stream* s, uint64_t landed) {
   if (!s->active) fail(AVEC_ERR_INVALID_ARGUMENT, "no pipelined cycle is active");
+  // callers are session / dispatcher threads whose current device may be any GPU
+  check_cuda(cudaSetDevice(s->ctx->device), "cudaSetDevice");
   if (landed > s->in_bytes) landed = s->in_bytes;
   issue_h2d(s, landed, landed == s->in_bytes);
   if (s->model.kind == AVEC_MODEL_POSENET) launch_groups(s);
@@ -229,6 +231,7 @@ void stream_feed(avec_stream* s, uint64_t landed) {
 
 double stream_finish(avec_stream* s) {
   if (!s->active) fail(AVEC_ERR_INVALID_ARGUMENT, "no pipelined cycle is active");
+  check_cuda(cudaSetDevice(s->ctx->device), "cudaSetDevice");
   double secs = 0;
   try {
     issue_h2d(s, s->in_bytes, true);
@@ -268,6 +271,7 @@ double stream_finish(avec_stream* s) {
 }
 
 void stream_abort(avec_stream* s) {
+  cudaSetDevice(s->ctx->device);
   if (s->active) drain(s);
 }
 

@@ -115,3 +115,38 @@ def test_session_policy_pins_and_serves(tmp_path):
         assert json.loads(r.stdout.strip().splitlines()[-1])["ok"]
     finally:
         srv.stop()
+
+
+@needs2
+def test_pipelined_sessions_on_two_gpus(tmp_path):
+    """Two concurrent reference clients on a 2-GPU server (session policy:
+    one session per GPU, so each GPU's pool pipelines its session's repeat
+    cycles): every reply equals the 1-GPU whole-batch forward bit for bit
+    (the C2 4-frame groups keep the 8-frame plan's kernels and K order)."""
+    from paper_2103_04930_b200 import B200Backend, Dims, Frame, make_model, netspec
+    spec = tmp_path / "coco.spec"
+    spec.write_bytes(netspec.spec())
+    w, h, nb, cycles = 656, 368, 8, 4
+    log = tmp_path / "events.jsonl"
+    srv = W.ServerProc([str(SERVER), "--policy", "session", "--devices", "0,1", "--slots", "1", "--log", str(log)])
+    try:
+        procs = [subprocess.Popen([str(REF_CLIENT), "--endpoint", srv.endpoint, "--structure", str(spec), "--divisor",
+                                   repr(netspec.COCO_DIVISOR), "--width", str(w), "--height", str(h), "--batch",
+                                   str(nb), "--frames", str(cycles), "--seed", str(7 + k), "--dump",
+                                   str(tmp_path / f"o{k}.bin"), "--name", "openpose_coco"],
+                                  stdout=subprocess.PIPE, text=True) for k in range(2)]
+        outs = [json.loads(p.communicate(timeout=600)[0].strip().splitlines()[-1]) for p in procs]
+        assert all(o["ok"] and o["byte_account_bad"] == 0 for o in outs)
+    finally:
+        srv.stop()
+    be = B200Backend(0, slots=1)
+    hd = be.register_model(make_model("openpose_coco", netspec.spec(), b"", netspec.COCO_DIVISOR))
+    for k in range(2):
+        got = np.fromfile(tmp_path / f"o{k}.bin", dtype=np.float32).reshape(cycles, -1)
+        for c in range(cycles):
+            frames = O.batched_frame(w, h, nb, seed=7 + k, first=c * nb)
+            want = be.forward(hd, Frame(Dims(1, 3 * nb, h, w), frames)).data
+            assert got[c].tobytes() == want.tobytes(), (k, c)
+    be.close()
+    events = [json.loads(l)["event"] for l in log.read_text().splitlines() if l.strip()]
+    assert events.count("cycle_pipelined") >= 2
