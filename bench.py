@@ -129,14 +129,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def run_reference_arm(steps: int, warmup: int, width=None, height=None, batch=None, clients=1) -> dict:
+def run_reference_arm(steps: int, warmup: int, width=None, height=None, batch=None, clients=1,
+                      divisor=None) -> dict:
     width, height = width or W, height or H
     batch = batch or CFG["global_batch"]
+    divisor = divisor or CFG["divisor"]
     exe = ROOT / "oracle" / "_ref" / "ref_arm"
     if not exe.exists():
         return {"ok": False, "error": f"{exe} not built"}
     out = subprocess.run([str(exe), "--width", str(width), "--height", str(height), "--batch", str(batch),
-                          "--steps", str(steps), "--warmup", str(warmup), "--clients", str(clients)],
+                          "--steps", str(steps), "--warmup", str(warmup), "--clients", str(clients),
+                          "--divisor", repr(divisor)],
                          capture_output=True, text=True, timeout=1800)
     try:
         return json.loads(out.stdout.strip().splitlines()[-1])
@@ -723,6 +726,23 @@ def ours_main(args, rank: int, world: int, local_rank: int) -> int:
             "clocks": clocks.summary(),
             "kernel_breakdown_ms_per_step": breakdown,
         }
+        if world == 1 and args.config == "c2":
+            # the reference's own server path (Server + MockPoseBackend on one
+            # host thread, reference Session clients, TCP loopback) on each
+            # config's shape, beside our number
+            legs = {"c1": dict(width=368, height=368, batch=1, steps=200, warmup=5),
+                    "c4": dict(width=W, height=H, batch=8, steps=8, warmup=1, clients=8),
+                    "c5": dict(width=CONFIGS["c5"]["width"], height=CONFIGS["c5"]["height"],
+                               batch=CONFIGS["c5"]["global_batch"], steps=2, warmup=1,
+                               divisor=CONFIGS["c5"]["divisor"])}
+            for key, kw in legs.items():
+                if isinstance(extras.get(key), dict):
+                    r = run_reference_arm(**kw)
+                    extras[key]["reference_cpu"] = {
+                        "ok": r.get("ok"), "fps": r.get("fps"), "unit": "frames/s", "cores": 1,
+                        "kind": "reference", "error": r.get("error"),
+                        "sample": f"reference Server+MockPoseBackend, {kw.get('clients', 1)} Session client(s) over "
+                                  f"TCP loopback, {kw['steps']} cycles of {kw['batch']}x{kw['width']}x{kw['height']}"}
         line.update(extras)
         print(json.dumps(line))
     if be is not None:
