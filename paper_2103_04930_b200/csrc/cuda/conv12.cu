@@ -8,23 +8,33 @@
 //             (x0-2) & ~3] (zero-filled outside the frame; a TMA inner
 //             coordinate must be 16-byte aligned — an unaligned one is an
 //             illegal instruction, tests/native/tma3d_probe.cu), conv1_1 weights once, conv1_2
-//             weights per tap (9 x 64x64 per tile, from L2)
+//             weights per (column tap s, K half) as [W(2,s); W(1,s); W(0,s)]
+//             (3 x 64 cout x 32 K, SW64; 72 KB per tile, from L2)
 //   epilogue  A: im2col of the 27 taps per window position (x - 0.5, 0 outside
-//                the frame) into a K = 32 SW64 im2col buffer
+//                the frame) into a K = 32 SW64 im2col buffer; taps 27 and 28
+//                are 1.0, against conv1_1's bias split hi + lo into its
+//                weights there (engine.cu upload), so acc1 includes the bias
 //   MMA       conv1_1: 4 windows x 2 MMAs (M128 N64 K16) -> acc1[4] in TMEM
-//   epilogue  B: acc1 -> bias, ReLU, 0 outside the image, bf16 -> overwrites
+//   epilogue  B: acc1 -> ReLU, 0 outside the image, bf16 -> overwrites
 //                the window (it is now conv1_2's A operand, SW128 K-major)
-//   MMA       conv1_2: 9 taps x 4 K16 x 2 rows (sub-tile 0 reads window r,
-//             sub-tile 1 window r+1, shifted by s rows) -> acc2[stage]
+//   MMA       conv1_2, per column tap s and K16 step: window w (shifted by s
+//             positions) feeds output row 0 with W(w,s) and output row 1 with
+//             W(w-1,s). The two middle windows do both in one N = 128 MMA
+//             against the adjacent [W(w,s); W(w-1,s)] rows (64 cycles, at the
+//             tensor rate), the outer two one N = 64 MMA each: 224 cycles per
+//             step instead of six N = 64 MMAs at the 48-cycle shared-memory
+//             operand floor (288; profiles/r01_tc_probe.json) -> acc2[stage]
 //   epilogue  C: 2x2 max of the raw sums, bias, ReLU, bf16 -> pooled row
 //             y0/2, columns x0/2 .. x0/2+62 through a 4D TMA map (the 127th/
 //             128th positions read past their window and are never stored)
 // Windows are double-buffered and the MMA warp issues conv1_1(t+1) before
 // conv1_2(t), so the im2col of tile t+2, the conv1_1 epilogue of tile t+1 and
-// the pooled epilogue of tile t-1 all overlap conv1_2 of tile t. Bit-identical to the
-// separate conv_first + pooled conv1_2 path (same bf16 operands, K order and
-// MMA shapes).
+// the pooled epilogue of tile t-1 all overlap conv1_2 of tile t. Same bf16
+// operands as the separate conv_first + pooled conv1_2 path; the fp32 sums run
+// in another tap order, so the two agree to bf16 rounding, not bit for bit.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 
 #include "conv_tc.cuh"
 #include "engine.hpp"
@@ -36,26 +46,43 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 352;  // weights, MMA, 8 epilogue warps (2 per TMEM lane quadrant), frame patches
-constexpr int kEpi = 256;
+// SUBS = epilogue warps per TMEM lane quadrant: 2 (default; 152 vs 156 us at
+// C2, 2.52-2.58 vs 2.62-2.65 ms at C5) or 4 (AVEC_C12_SUBS=4)
+template <int SUBS>
+struct C12Cfg {
+  static constexpr int kEpi = 128 * SUBS;
+  static constexpr int kThreads = 64 + kEpi + 32;  // weights, MMA, epilogue warps, frame patches
+  static constexpr int kPatchWarp = 2 + 4 * SUBS;
+  static constexpr int kWinPerSub = 4 / SUBS;      // windows per epilogue warp (im2col, conv1_1 epilogue)
+  static constexpr int kChPerSub = 64 / SUBS;      // pooled channels per epilogue warp
+};
 constexpr uint32_t kTmemCols = 512;
 constexpr int kTileCols = 126;  // output columns per tile (even: whole pooled columns)
 constexpr int kPatchCols = 132;
 constexpr int kPatchRows = 6;
 constexpr int kPatchBytes = 3 * kPatchRows * kPatchCols * 4;  // 9504
+// conv1_2 weight ring: a stage is one column tap s and one K chunk q,
+// [W(2,s); W(1,s); W(0,s)] x [64 cout][kWK K] bf16, swizzle span 2 kWK bytes.
+// K halves (SW64, 12 KB, 3 stages): 152 us at C2. K16 chunks (SW32, 6 KB, 7
+// stages, to hide more L2 latency) measured slower: 159 us.
+constexpr int kWK = 32;                  // K per stage
+constexpr int kWBlk = 64 * kWK * 2;      // one W(r,s) block, bytes
+constexpr int kW12Stage = 3 * kWBlk;
 constexpr int kW12Stages = 3;
 constexpr int kAcc2Col = 256;  // acc2[2 stages] at 256..383, 384..511 (2 rows x 64 each)
 
 struct Smem12 {
   static constexpr int win = 0;                          // 2 buffers x 4 windows x [128][64] bf16 SW128
   static constexpr int imc = win + 2 * 4 * 16384;        // 4 windows x [128][32] bf16 SW64 (im2col)
-  static constexpr int w12 = imc + 4 * 8192;             // kW12Stages x [64 cout][64 K]
-  static constexpr int w11 = w12 + kW12Stages * 8192;    // [64 cout][64 K] (K 27 used)
-  static constexpr int patch = w11 + 8192;               // 2 x [3][6][132] fp32
-  static constexpr int stg = patch + 2 * 9728;           // 4 warps x [16 px][64 ch] (pooled box)
-  static constexpr int bias = stg + 4 * 2048;            // b11, b12 (64 each)
+  static constexpr int w12 = imc + 4 * 8192;             // kW12Stages x kW12Stage
+  static constexpr int w11 = w12 + kW12Stages * kW12Stage;  // [64 cout][32 K] SW64 (K 29 used)
+  static constexpr int patch = w11 + 4096;               // [3][6][132] fp32 (one buffer: the
+                                                         // next patch has a whole tile to land)
+  static constexpr int stg = patch + 10240;              // 4 warps x [16 px][64 ch] (pooled box)
+  static constexpr int bias = stg + 4 * 2048;            // conv1_2 bias (64; room for 128)
   static constexpr int bars = bias + 2 * 64 * 4;
   static constexpr int total = bars + 256;
+  static_assert((2 + 2 + 1 + 2 * kW12Stages + 1 + 1 + 2 + 2 + 2 + 2) * 8 + 4 <= 256, "barrier block");
   static_assert(total + 1024 <= 232448, "smem budget");
 };
 
@@ -82,8 +109,12 @@ __device__ __forceinline__ void tile_of(const ConvParams& p, int t, int& n, int&
 // maps.act_big[0]: fp32 frames [N*3][H][W], box {132, 6, 3}; maps.wgt[0]:
 // conv1_2 weights, maps.wgt[1]: conv1_1 weights (box {64, 64}); maps.out_pool[0]
 // / [1]: pooled 4D stores with 16 / 15-column boxes. p.g[0] = conv1_2, p.g[1] = conv1_1.
-__global__ void __launch_bounds__(kThreads, 1)
+template <int SUBS>
+__global__ void __launch_bounds__(C12Cfg<SUBS>::kThreads, 1)
     conv12_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p) {
+  using Cfg = C12Cfg<SUBS>;
+  constexpr int kSubs = SUBS, kEpi = Cfg::kEpi, kPatchWarp = Cfg::kPatchWarp;
+  constexpr int kWinPerSub = Cfg::kWinPerSub, kChPerSub = Cfg::kChPerSub;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* win = smem + Smem12::win;
@@ -92,10 +123,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* w11 = smem + Smem12::w11;
   float* patch = reinterpret_cast<float*>(smem + Smem12::patch);
   uint8_t* stg = smem + Smem12::stg;
-  float* b11 = reinterpret_cast<float*>(smem + Smem12::bias);
-  float* b12 = b11 + 64;
+  float* b12 = reinterpret_cast<float*>(smem + Smem12::bias);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem12::bars);
-  uint64_t* patch_full = bars;             // [2]
+  uint64_t* patch_full = bars;             // [2] (only [0] used)
   uint64_t* patch_empty = patch_full + 2;  // [2] 128 arrivals
   uint64_t* w11_full = patch_empty + 2;
   uint64_t* w12_full = w11_full + 1;       // [kW12Stages]
@@ -137,20 +167,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ producer
     if (elect_one()) {
       const uint64_t keep = policy_evict_last();
-      mbar_arrive_expect_tx(w11_full, 8192);
+      mbar_arrive_expect_tx(w11_full, 4096);
       tma_load_2d(w11, &maps.wgt[1], w11_full, 0, 0);
       int ws = 0;
       uint32_t wph = 0;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-        for (int tap = 0; tap < 9; ++tap) {
-          mbar_wait(&w12_empty[ws], wph ^ 1);
-          mbar_arrive_expect_tx(&w12_full[ws], 8192);
-          tma_load_2d_hint(w12 + ws * 8192, &maps.wgt[0], &w12_full[ws], tap * 64, 0, keep);
-          if (++ws == kW12Stages) { ws = 0; wph ^= 1; }
-        }
+        for (int s = 0; s < 3; ++s)
+          for (int q = 0; q < 64 / kWK; ++q) {
+            mbar_wait(&w12_empty[ws], wph ^ 1);
+            mbar_arrive_expect_tx(&w12_full[ws], kW12Stage);
+            for (int r = 2; r >= 0; --r)  // K index (r*3 + s)*64 + cin
+              tma_load_2d_hint(w12 + ws * kW12Stage + (2 - r) * kWBlk, &maps.wgt[0], &w12_full[ws],
+                               (r * 3 + s) * 64 + kWK * q, 0, keep);
+            if (++ws == kW12Stages) { ws = 0; wph ^= 1; }
+          }
       }
     }
-  } else if (warp == 10) {
+  } else if (warp == kPatchWarp) {
     // ------------------------------------------------------------ frame patches
     // its own warp, so a patch lands as soon as its buffer frees (the im2col
     // of tile t+1 runs before conv1_2 of tile t and must not wait on HBM)
@@ -159,10 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
         int n, y0, x0;
         tile_of(p, t, n, y0, x0);
-        const int pb = it & 1;
-        mbar_wait(&patch_empty[pb], ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&patch_full[pb], kPatchBytes);
-        tma_load_3d(patch + pb * (9728 / 4), &maps.act_big[0], &patch_full[pb], (x0 - 2) & ~3, y0 - 2, n * 3);
+        mbar_wait(&patch_empty[0], (it & 1) ^ 1);
+        mbar_arrive_expect_tx(&patch_full[0], kPatchBytes);
+        tma_load_3d(patch, &maps.act_big[0], &patch_full[0], (x0 - 2) & ~3, y0 - 2, n * 3);
       }
     }
   } else if (warp == 1) {
@@ -171,13 +203,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // im2col of t+1 is written), then conv1_2(t) — the tensor pipe runs them
     // in issue order, so act11(t+1) overlaps conv1_2(t)
     if (elect_one()) {
-      const uint32_t idesc = idesc_bf16_f32(128, 64);
+      const uint32_t idesc = idesc_bf16_f32(128, 64), idesc2 = idesc_bf16_f32(128, 128);
       const uint32_t win_base = smem_u32(win), imc_base = smem_u32(imc);
       const uint32_t w12_base = smem_u32(w12), w11_base = smem_u32(w11);
       auto conv11 = [&](uint32_t ph) {
         mbar_wait(imc_full, ph);
         tc_fence_after();
-        const uint64_t bd11 = desc_sw128(w11_base);
+        const uint64_t bd11 = desc_sw64(w11_base);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint64_t ad = desc_sw64(imc_base + j * 8192);
@@ -200,19 +232,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t + int(gridDim.x) < p.total_tiles) conv11((it + 1) & 1);
         mbar_wait(&acc2_empty[b], bph ^ 1);
         tc_fence_after();
+        // acc2: output row 0 at columns d0 .. d0+63, row 1 at d0+64 .. d0+127
         const uint32_t d0 = tmem + kAcc2Col + b * 128;
-        for (int r = 0; r < 3; ++r)
-          for (int s = 0; s < 3; ++s) {
+        for (int s = 0; s < 3; ++s)
+          for (int q = 0; q < 64 / kWK; ++q) {
             mbar_wait(&w12_full[ws], wph);
             tc_fence_after();
-            // descriptors once per tap; a 32-byte K step adds 2 to each
-            const uint64_t bd = desc_sw128(w12_base + ws * 8192);
-            const uint64_t a0 = desc_sw128(wb + r * 16384 + s * 128), a1 = desc_sw128(wb + (r + 1) * 16384 + s * 128);
+            // the stage holds W(2,s), W(1,s), W(0,s) kWBlk bytes apart; a
+            // 32-byte K step adds 2 to a descriptor
+            const uint64_t b2 = kWK == 32 ? desc_sw64(w12_base + ws * kW12Stage) : desc_sw32(w12_base + ws * kW12Stage);
+            const uint64_t b1 = b2 + (kWBlk >> 4), b0 = b2 + 2 * (kWBlk >> 4);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint32_t accum = (r == 0 && s == 0 && kk == 0) ? 0u : 1u;
-              mma_bf16_ss(d0, a0 + 2 * kk, bd + 2 * kk, idesc, accum);
-              mma_bf16_ss(d0 + 64, a1 + 2 * kk, bd + 2 * kk, idesc, accum);
+            for (int kk = 0; kk < kWK / 16; ++kk) {
+              const uint32_t accum = (s == 0 && q == 0 && kk == 0) ? 0u : 1u;
+              const uint32_t ko = 2 * (q * (kWK / 16) + kk), kb = 2 * kk;
+              mma_bf16_ss(d0 + 64, desc_sw128(wb + 3 * 16384 + s * 128) + ko, b2 + kb, idesc, accum);  // row 1 += win3 W(2,s)
+              mma_bf16_ss(d0, desc_sw128(wb + s * 128) + ko, b0 + kb, idesc, accum);  // row 0 += win0 W(0,s)
+              mma_bf16_ss(d0, desc_sw128(wb + 16384 + s * 128) + ko, b1 + kb, idesc2, 1u);  // rows 0|1 += win1 [W(1,s); W(0,s)]
+              mma_bf16_ss(d0, desc_sw128(wb + 2 * 16384 + s * 128) + ko, b2 + kb, idesc2, 1u);  // rows 0|1 += win2 [W(2,s); W(1,s)]
             }
             mma_commit(&w12_empty[ws]);
             if (++ws == kW12Stages) { ws = 0; wph ^= 1; }
@@ -223,40 +260,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue group
-    // warps 2..9: quad = TMEM lane quadrant (warp % 4), sub = which half of
-    // the windows (im2col, conv1_1 epilogue) or channels (pooled) it handles
+    // warps 2 .. 1 + 4 kSubs: quad = TMEM lane quadrant (warp % 4), sub =
+    // which windows (im2col, conv1_1 epilogue) or channels (pooled) it handles;
+    // four warps per quadrant keep enough loads in flight (two left the MMA
+    // waiting on the conv1_1 epilogue)
     const uint32_t quad = warp & 3;
     const int sub = (int(warp) - 2) >> 2;
     const uint32_t lane = lane_id();
     const int px = int(quad) * 32 + int(lane);  // window position / TMEM lane of this thread
     const int ep = int(threadIdx.x) - 64;
     const uint32_t lane_base = (quad * 32) << 16;
-    if (ep < 64) {
-      const ConvGroupParams& g2 = p.g[0];
-      const ConvGroupParams& g1 = p.g[1];
-      b12[ep] = g2.bias[ep];
-      b11[ep] = g1.bias[ep];
-    }
+    if (ep < 64) b12[ep] = p.g[0].bias[ep];  // (conv1_1's bias rides in its weights)
     named_bar_sync(1, kEpi);
     // A: im2col of tile (t, it) into the SW64 im2col buffer (free once conv1_1
     // of the previous tile completed)
     auto im2col = [&](int t, int it) {
       int n, y0, x0;
       tile_of(p, t, n, y0, x0);
-      const int b = it & 1;
-      mbar_wait(&patch_full[b], (it >> 1) & 1);
-      const float* pp = patch + b * (9728 / 4);
+      mbar_wait(&patch_full[0], it & 1);
+      const float* pp = patch;
       const int C = x0 + px - 1;  // image column of this window position
       // the patch starts at column (x0 - 2) & ~3: TMA needs 16-byte aligned inner coordinates
       const float* ppx = pp + px + ((x0 - 2) & 3);
       uint8_t* wrow = imc + px * 64;
 #pragma unroll
-      for (int jw = 0; jw < 2; ++jw) {
-        const int j = 2 * sub + jw;
+      for (int jw = 0; jw < kWinPerSub; ++jw) {
+        const int j = kWinPerSub * sub + jw;
         const int R = y0 - 1 + j;  // conv1_1 output row of window j
         float xs[32];
+        xs[27] = xs[28] = 1.f;  // the bias taps
 #pragma unroll
-        for (int i = 27; i < 32; ++i) xs[i] = 0.f;
+        for (int i = 29; i < 32; ++i) xs[i] = 0.f;
 #pragma unroll
         for (int ci = 0; ci < 3; ++ci)
 #pragma unroll
@@ -281,10 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
       }
       fence_proxy_async_smem();
-      mbar_arrive(&patch_empty[b]);
+      mbar_arrive(&patch_empty[0]);
       mbar_arrive(imc_full);
     };
-    // B: conv1_1 accumulators -> bias, ReLU, zero outside the image, bf16 ->
+    // B: conv1_1 accumulators (bias included) -> ReLU, zero outside the image, bf16 ->
     // the tile's window buffer (conv1_2's A operand, SW128 K-major)
     auto act11 = [&](int t, int it) {
       int n, y0, x0;
@@ -294,8 +328,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int C = x0 + px - 1;
       uint8_t* wrow = win + b * 4 * 16384 + px * 128;
 #pragma unroll
-      for (int jw = 0; jw < 2; ++jw) {
-        const int j = 2 * sub + jw;
+      for (int jw = 0; jw < kWinPerSub; ++jw) {
+        const int j = kWinPerSub * sub + jw;
         const int R = y0 - 1 + j;
         const bool valid = R >= 0 && R < p.H && C >= 0 && C < p.W;
         uint32_t va[32], vb[32];
@@ -309,9 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
             const int c = q * 8 + 2 * jj;
-            const float2 bias = *reinterpret_cast<const float2*>(b11 + c);
-            w[jj] = valid ? pack2_relu(__uint_as_float(q < 4 ? va[c & 31] : vb[c & 31]) + bias.x,
-                                       __uint_as_float(q < 4 ? va[(c + 1) & 31] : vb[(c + 1) & 31]) + bias.y)
+            w[jj] = valid ? pack2_relu(__uint_as_float(q < 4 ? va[c & 31] : vb[c & 31]),
+                                       __uint_as_float(q < 4 ? va[(c + 1) & 31] : vb[(c + 1) & 31]))
                           : 0u;
           }
           *reinterpret_cast<uint4*>(row + ((q ^ (px & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -333,35 +366,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tb0 = tmem + lane_base + kAcc2Col + b * 128;
       uint8_t* buf = stg + quad * 2048;
       if (sub == 0 && lane == 0) bulk_wait_read<0>();
-      named_bar_sync(2 + quad, 64);  // the quad's previous store has read the staging box
+      named_bar_sync(2 + quad, 32 * kSubs);  // the quad's previous store has read the staging box
       {
-        const int hlf = sub;
-        uint32_t va[32], vb[32];
-        tmem_ld32(tb0 + 32 * hlf, va);
-        tmem_ld32(tb0 + 64 + 32 * hlf, vb);
+        constexpr int kH = kChPerSub / 2;
+        const int cb = kChPerSub * sub;
+        uint32_t va[kChPerSub], vb[kChPerSub];
+        if constexpr (kChPerSub == 16) {
+          tmem_ld16(tb0 + cb, va);
+          tmem_ld16(tb0 + 64 + cb, vb);
+        } else {
+          tmem_ld32(tb0 + cb, va);
+          tmem_ld32(tb0 + 64 + cb, vb);
+        }
         tmem_ld_wait();
         // vertical max in registers; the horizontal pair (lanes 2i, 2i+1)
-        // splits the 32 channels: the even lane finishes 0..15, the odd 16..31
+        // splits the channels: the even lane finishes the lower half, the odd the upper
         const bool odd = lane & 1;
-        float m[16];
+        float m[kH];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < kH; ++k) {
           const float lo = fmaxf(__uint_as_float(va[k]), __uint_as_float(vb[k]));
-          const float hi = fmaxf(__uint_as_float(va[16 + k]), __uint_as_float(vb[16 + k]));
+          const float hi = fmaxf(__uint_as_float(va[kH + k]), __uint_as_float(vb[kH + k]));
           const float other = __shfl_xor_sync(0xffffffffu, odd ? lo : hi, 1);
           m[k] = fmaxf(odd ? hi : lo, other);
         }
-        const int c0 = 32 * hlf + (odd ? 16 : 0);
-        uint32_t w[8];
+        const int c0 = cb + (odd ? kH : 0);
+        uint32_t w[kH / 2];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < kH / 2; ++k) {
           const float2 bias = *reinterpret_cast<const float2*>(b12 + c0 + 2 * k);
           w[k] = pvalid ? pack2_relu(m[2 * k] + bias.x, m[2 * k + 1] + bias.y) : 0u;
         }
         const uint32_t row = lane >> 1;
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const uint32_t qq = 4 * hlf + (odd ? 2 : 0) + q;
+        for (int q = 0; q < kH / 8; ++q) {
+          const uint32_t qq = c0 / 8 + q;
           *reinterpret_cast<uint4*>(buf + row * 128 + ((qq ^ (row & 7)) << 4)) =
               make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
         }
@@ -369,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&acc2_empty[b]);
       fence_proxy_async_smem();
-      named_bar_sync(2 + quad, 64);
+      named_bar_sync(2 + quad, 32 * kSubs);
       if (sub == 0 && lane == 0) {
         // warp 3's 16th pooled column is the next tile's first: 15-column box
         tma_store_4d(quad == 3 ? &maps.out_pool[1] : &maps.out_pool[0], buf, p.g[0].out_c_off,
@@ -401,15 +440,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 void conv12_configure() {
-  check_cuda(cudaFuncSetAttribute(conv12_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem12::total + 1024),
+  check_cuda(cudaFuncSetAttribute(conv12_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem12::total + 1024),
+             "conv12 smem attribute");
+  check_cuda(cudaFuncSetAttribute(conv12_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem12::total + 1024),
              "conv12 smem attribute");
 }
 
 int conv12_tile_cols() { return kTileCols; }
+int conv12_wgt_k() { return kWK; }
 
 void launch_conv12(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
   const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
-  conv12_kernel<<<grid, kThreads, Smem12::total + 1024, stream>>>(maps, p);
+  static const int subs = [] {
+    const char* e = std::getenv("AVEC_C12_SUBS");
+    return e && e[0] == '4' ? 4 : 2;
+  }();
+  if (subs == 2)
+    conv12_kernel<2><<<grid, C12Cfg<2>::kThreads, Smem12::total + 1024, stream>>>(maps, p);
+  else
+    conv12_kernel<4><<<grid, C12Cfg<4>::kThreads, Smem12::total + 1024, stream>>>(maps, p);
   check_cuda(cudaGetLastError(), "conv12 launch");
 }
 

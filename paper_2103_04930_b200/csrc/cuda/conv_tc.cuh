@@ -171,6 +171,7 @@ int conv_head_pair_max_chunks();  // input chunks the pair head keeps resident
 // conv1_1 + conv1_2 + pool1 (conv12.cu)
 void conv12_configure();
 int conv12_tile_cols();
+int conv12_wgt_k();  // K columns per conv1_2 weight box (the stage's swizzle span / 2)
 void launch_conv12(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream);
 void launch_conv_head(const HeadMaps& maps, const HeadParams& p, int sm_count, cudaStream_t stream);
 void launch_conv_first(const ConvMaps& maps, const ConvParams& p, const float* frames, int sm_count,

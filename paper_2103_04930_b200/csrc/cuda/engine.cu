@@ -89,16 +89,20 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2D bf16 [rows][cols] row-major, box {64 cols, box_rows}, 128-byte swizzle
-CUtensorMap make_map_2d(const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+// 2D bf16 [rows][cols] row-major, box {box_cols, box_rows}; the swizzle span
+// equals the box row (64 cols: 128 B, 32 cols: 64 B, 16 cols: 32 B)
+CUtensorMap make_map_2d(const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows, uint32_t box_cols = 64) {
   CUtensorMap m;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           box_cols == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
+                           : box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                            : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
   return m;
@@ -312,6 +316,16 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
       src += size_t(d.cout) * d.cin * k * k;
     }
     std::memcpy(host.data() + b_off[i], src, d.cout * 4);
+    if (i == 0) {
+      // conv12 folds conv1_1's bias into its MMA: im2col taps 27 and 28 are
+      // 1.0, weights there bias = hi + lo (two bf16 parts, 2^-17 relative);
+      // conv_first's im2col keeps them 0
+      uint16_t* w = reinterpret_cast<uint16_t*>(host.data() + w_off[i]);
+      for (int co = 0; co < d.cout; ++co) {
+        w[size_t(co) * 64 + 27] = bf16_bits(src[co]);
+        w[size_t(co) * 64 + 28] = bf16_bits(src[co] - bf16_value(src[co]));
+      }
+    }
     src += d.cout;
     if (d.act == kActPrelu) {
       std::memcpy(host.data() + b_off[i] + size_t(L.cout_pad) * 4, src, d.cout * 4);
@@ -480,8 +494,8 @@ struct PlanBuilder {
     g1.act = A.def.act;
     g1.cout = 64;
     op.maps.act_big[0] = make_map_frames(plan.in.p, uint64_t(p.W), uint64_t(p.H), uint64_t(plan.n) * 3);
-    op.maps.wgt[0] = make_map_2d(B.w, 9 * 64, B.cout_pad, 64);
-    op.maps.wgt[1] = make_map_2d(A.w, 64, A.cout_pad, 64);
+    op.maps.wgt[0] = make_map_2d(B.w, 9 * 64, B.cout_pad, 64, conv12_wgt_k());  // [64 cout][K chunk]
+    op.maps.wgt[1] = make_map_2d(A.w, 64, A.cout_pad, 64, 32);  // [64 cout][32 K] SW64
     const Geometry& g1g = plan.geo[1];
     op.maps.out_pool[0] = make_map_4d_store(plan.bufs[pooled]->p, 64, g1g.Wp(), g1g.Hp(), plan.n, 16);
     op.maps.out_pool[1] = make_map_4d_store(plan.bufs[pooled]->p, 64, g1g.Wp(), g1g.Hp(), plan.n, 15);

@@ -306,6 +306,14 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t smem_addr) {
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
+// The 32-byte swizzled K-major layout: rows of 32 B (16 bf16), 8-row groups
+// 256 B apart, layout = 6 (SWIZZLE_32B); 16-byte chunk c of row r sits at
+// chunk c ^ ((r >> 2) & 1).
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t smem_addr) {
+  return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)16 << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
+
 // Instruction descriptor, kind::f16: bf16 x bf16 -> f32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4)            // c_format F32

@@ -280,12 +280,14 @@ be.close()
 """
 
 
-def test_conv12_bit_identical_to_unfused(net, tmp_path):
-    """The fused conv1_1 + conv1_2 + pool1 kernel uses the same bf16 operands,
-    K order and MMA shapes as conv_first + the pooled conv1_2, so pool1 and the
-    whole forward are bit-identical to the unfused path (run in a subprocess
-    with AVEC_CONV12=0). Width 400 gives four 126-column tiles whose frame
-    patches start at both 16-byte alignments ((x0 - 2) & 3 = 2 and 0)."""
+def test_conv12_matches_unfused(net, tmp_path):
+    """The fused conv1_1 + conv1_2 + pool1 kernel against conv_first + the
+    pooled conv1_2 (run in a subprocess with AVEC_CONV12=0). The fused kernel
+    adds conv1_1's bias inside the MMA and sums conv1_2's taps in another order
+    (N = 128 MMAs over two output rows, conv12.cu), so pool1 agrees to a bf16
+    step and the whole forward within the end-to-end tolerance.
+    Width 400 gives four 126-column tiles whose frame patches start at both
+    16-byte alignments ((x0 - 2) & 3 = 2 and 0)."""
     import os
     import pathlib
     import subprocess
@@ -303,5 +305,13 @@ def test_conv12_bit_identical_to_unfused(net, tmp_path):
     subprocess.run([sys.executable, "-c", _UNFUSED_SCRIPT, root, str(dst), str(w), str(hgt), str(nb)],
                    env=env, check=True, timeout=600)
     ref = np.load(dst)
-    assert pooled.tobytes() == ref["pooled"].tobytes()
-    assert out.tobytes() == ref["out"].tobytes()
+    rp = ref["pooled"].astype(np.float64)
+    fp = pooled.astype(np.float64)
+    # each path is within the per-layer bound of the oracle (test_layer_parity);
+    # against each other they may differ by a bf16 step near the layer's max
+    # (2^-8 relative), and conv1_1's output rounding the other way carries
+    # into conv1_2
+    assert np.max(np.abs(fp - rp)) <= 2.0 ** -8 * np.max(np.abs(rp)), float(np.max(np.abs(fp - rp)))
+    assert np.mean(fp != rp) < 0.02
+    ro, fo = ref["out"].astype(np.float64), out.astype(np.float64)
+    assert np.max(np.abs(fo - ro)) <= 2e-2 * np.max(np.abs(ro))
