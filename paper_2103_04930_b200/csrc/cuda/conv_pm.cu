@@ -334,14 +334,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               // descriptors built once per tap: a 32-byte K step adds 2 to the
               // start-address field (addresses < 256 KB, so it cannot carry out)
               const uint64_t bd0 = desc_sw128(bb);
+              // the K16 count as a compile-time constant: a fully unrolled
+              // tap is straight-line MMAs with immediate descriptor offsets
+              // (a runtime-bounded loop put a branch and a 64-bit add chain
+              // on the single issuing thread between MMAs)
+              auto tap = [&](auto kn_c) {
+                constexpr int KN = decltype(kn_c)::value;
 #pragma unroll
-              for (int sub = 0; sub < SUBS_M; ++sub) {
-                const uint64_t ad0 = desc_sw128(wb + (sub * 128 + s) * 128);
+                for (int sub = 0; sub < SUBS_M; ++sub) {
+                  const uint64_t ad0 = desc_sw128(wb + (sub * 128 + s) * 128);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                  if (kk >= kn) break;
-                  mma(d0 + sub * N, ad0 + 2 * kk, bd0 + 2 * kk, (first && kk == 0) ? 0u : 1u);
+                  for (int kk = 0; kk < KN; ++kk)
+                    mma(d0 + sub * N, ad0 + 2 * kk, bd0 + 2 * kk, (first && kk == 0) ? 0u : 1u);
                 }
+              };
+              switch (kn) {
+                case 4: tap(std::integral_constant<int, 4>{}); break;
+                case 3: tap(std::integral_constant<int, 3>{}); break;
+                case 2: tap(std::integral_constant<int, 2>{}); break;
+                default: tap(std::integral_constant<int, 1>{}); break;
               }
               first = false;
               if constexpr (C::kTaps == 1) {

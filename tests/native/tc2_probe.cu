@@ -181,6 +181,54 @@ __global__ void __cluster_dims__(2, 1, 1) probe2_rate(int N, int iters, unsigned
   if (warp_id() == 0) tmem_dealloc2<256>(tmem_base);
 }
 
+// rate with conv_pm's operand pattern: A = a 264-row window read at row
+// offsets sub*128 + s (s = the filter tap, sub = the 128-row sub-tile), two
+// accumulators, B one [N/2][64] block per tap; off_mode 0 = no row shift (s = 0)
+__global__ void __cluster_dims__(2, 1, 1) probe2_rate_conv(int N, int iters, int off_mode, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar_mma;
+  __shared__ uint32_t tmem_base;
+  constexpr int kWin = 272 * 128, kB = 3 * 16384;
+  for (int i = threadIdx.x; i < (kWin + kB) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp_id() == 0) tmem_alloc2<512>(&tmem_base);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_mma, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (cta_rank() == 0 && threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16_f32(256, N);
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + kWin);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const uint64_t bd = desc_sw128(b0 + s * 16384);
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          const uint64_t ad = desc_sw128(a0 + (sub * 128 + (off_mode ? s : 0)) * 128);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma2(tmem_base + sub * N, ad + 2 * k, bd + 2 * k, idesc, 1);
+        }
+      }
+    }
+    commit2(&bar_mma);
+    mbar_wait(&bar_mma, 0);
+    long long t1 = clock64();
+    cycles[blockIdx.x / 2] = (unsigned long long)(t1 - t0);
+  } else if (threadIdx.x == 0) {
+    mbar_wait(&bar_mma, 0);
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp_id() == 0) tmem_dealloc2<512>(tmem_base);
+}
+
 int main() {
   const int M = 256, K = 64, BR = 256;
   std::vector<__nv_bfloat16> hA(M * K), hB(BR * K);
@@ -252,6 +300,25 @@ int main() {
     std::printf("%s{\"N\": %d, \"cycles_per_mma\": %.2f, \"ideal\": %.1f}", ni ? ", " : "", N, per_mma,
                 N / 2.0);
   }
+  std::printf("], \"rate_conv\": [");
+  const int smem_conv = 120 * 1024;  // > half the SM: one CTA (and one 512-column TMEM allocation) per SM
+  CK(cudaFuncSetAttribute(probe2_rate_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_conv));
+  const int Nc[3] = {96, 128, 256};
+  bool firstc = true;
+  for (int ni = 0; ni < 3; ++ni)
+    for (int om = 0; om < 2; ++om) {
+      const int N = Nc[ni], iters = 500;
+      probe2_rate_conv<<<2 * pairs, 128, smem_conv>>>(N, iters, om, dc);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(hc.data(), dc, pairs * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      double avg = 0;
+      for (auto c : hc) avg += double(c);
+      avg /= pairs;
+      std::printf("%s{\"N\": %d, \"row_shift\": %d, \"cycles_per_mma\": %.2f, \"ideal\": %.1f}", firstc ? "" : ", ",
+                  N, om, avg / (iters * 24.0), N / 2.0);
+      firstc = false;
+    }
   std::printf("]}\n");
   return 0;
 }
