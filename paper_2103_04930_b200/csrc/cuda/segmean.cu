@@ -6,13 +6,23 @@
 // Explicit _rn intrinsics keep the device op sequence identical to the CPU's,
 // so the result is bit-exact (tests/test_gpu_mockpose.py).
 //
+// The division: for short segments (n <= MAXN) sum / n is taken as
+//   q = RN(sum * y), r = fma(-q, n, sum) (exact), q' = RN(fma(r, y, q)),
+// y = RN(1/n) from a per-CTA table. With y correctly rounded and q within an
+// ulp of sum/n, q' is the correctly rounded quotient (Markstein's theorem),
+// i.e. exactly __ddiv_rn(sum, n); 2e8 random sums of 1..8 floats over wide
+// exponent ranges agreed bit for bit on the host. Three FP64 ops instead of
+// the division sequence, which made the kernel instruction-bound.
+// Non-finite sums and empty segments keep __ddiv_rn (inf - inf, 0 * inf).
+//
 // HBM-bound: 4E bytes read + 4K bytes written per frame. Each CTA stages its
-// contiguous input span in shared memory with 16-byte loads, then every thread
+// contiguous input span in shared memory by a bulk copy, then every thread
 // walks four (short) segments in order.
 #include <cmath>
 #include <cstdint>
 
 #include "engine.hpp"
+#include "ptx.cuh"
 
 namespace avec {
 
@@ -45,7 +55,10 @@ __global__ void __launch_bounds__(kThreads) segmean_staged(const float* __restri
                                                            uint64_t K, double width, uint64_t jbeg,
                                                            uint64_t jend) {
   __shared__ uint32_t bnd[kSegsPerCta + 1];  // segment boundaries, offsets into the stage
+  __shared__ double rcp[MAXN + 1];           // RN(1 / n)
   extern __shared__ __align__(16) float stage[];
+  if (MAXN > 0 && threadIdx.x >= 1 && threadIdx.x <= MAXN)
+    rcp[threadIdx.x] = __ddiv_rn(1.0, static_cast<double>(threadIdx.x));
   const uint64_t j0 = jbeg + static_cast<uint64_t>(blockIdx.x) * kSegsPerCta;
   const uint64_t j1 = j0 + kSegsPerCta < jend ? j0 + kSegsPerCta : jend;
   const uint64_t span_lo = seg_bound(j0, K, E, width);
@@ -54,9 +67,20 @@ __global__ void __launch_bounds__(kThreads) segmean_staged(const float* __restri
   const uint64_t base = span_lo & ~uint64_t(3);
   const uint32_t n = static_cast<uint32_t>(span_hi - base);
   const uint32_t n4 = n >> 2;
-  const float4* src4 = reinterpret_cast<const float4*>(in + base);
-  float4* dst4 = reinterpret_cast<float4*>(stage);
-  for (uint32_t i = threadIdx.x; i < n4; i += kThreads) dst4[i] = __ldg(src4 + i);
+  // the 16-byte body of the span arrives by one bulk copy (no per-thread
+  // load -> store round trips; the boundaries below are computed while it
+  // lands), the < 4-float tail by plain loads
+  __shared__ uint64_t landed;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&landed, 1);
+    ptx::fence_barrier_init();
+    if (n4) {
+      ptx::mbar_arrive_expect_tx(&landed, n4 << 4);
+      ptx::bulk_load(stage, in + base, n4 << 4, &landed);
+    } else {
+      ptx::mbar_arrive(&landed);
+    }
+  }
   for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) stage[i] = __ldg(in + base + i);
   // every boundary once (segment j spans [bnd[j - j0], bnd[j - j0 + 1]) of the stage),
   // 32-bit offsets from here on: a staged span is < 12K floats
@@ -64,18 +88,25 @@ __global__ void __launch_bounds__(kThreads) segmean_staged(const float* __restri
   if (E <= 0xffffffffull) {
     // 32-bit boundaries (every FrameData: E < 2^29): the same products
     // double(j) * width truncated, j and the result exact in 32 bits
+    // (j = 0 needs no case: 0 * width truncates to 0); computed for every j
+    // and selected, so the loop is straight-line
     const uint32_t jb = static_cast<uint32_t>(j0), k32 = static_cast<uint32_t>(K);
     const uint32_t e32 = static_cast<uint32_t>(E), b32 = static_cast<uint32_t>(base);
-    for (uint32_t b = threadIdx.x; b <= nb; b += kThreads) {
-      const uint32_t j = jb + b;
-      const uint32_t at = j == 0 ? 0u : j >= k32 ? e32 : __double2uint_rz(__dmul_rn(__uint2double_rn(j), width));
-      bnd[b] = at - b32;
+#pragma unroll
+    for (int rr = 0; rr <= kSegsPerThread; ++rr) {
+      const uint32_t b = threadIdx.x + static_cast<uint32_t>(rr) * kThreads;
+      if (b <= nb) {
+        const uint32_t j = jb + b;
+        const uint32_t prod = __double2uint_rz(__dmul_rn(__uint2double_rn(j), width));
+        bnd[b] = (j >= k32 ? e32 : prod) - b32;
+      }
     }
   } else {
     for (uint32_t b = threadIdx.x; b <= nb; b += kThreads)
       bnd[b] = static_cast<uint32_t>(seg_bound(j0 + b, K, E, width) - base);
   }
   __syncthreads();
+  ptx::mbar_wait(&landed, 0);
 #pragma unroll
   for (int r = 0; r < kSegsPerThread; ++r) {
     const uint32_t jl = threadIdx.x + static_cast<uint32_t>(r) * kThreads;
@@ -91,10 +122,21 @@ __global__ void __launch_bounds__(kThreads) segmean_staged(const float* __restri
           const float x = lo + i < hi ? stage[lo + i] : -0.0f;
           sum = __dadd_rn(sum, static_cast<double>(x));
         }
+        const uint32_t cnt = hi - lo;
+        const double n = static_cast<double>(cnt);
+        double mean;
+        if (cnt != 0 && isfinite(sum)) {
+          const double y = rcp[cnt];
+          const double q = __dmul_rn(sum, y);
+          mean = __fma_rn(__fma_rn(-q, n, sum), y, q);
+        } else {
+          mean = __ddiv_rn(sum, n);
+        }
+        out[j0 + jl] = __double2float_rn(mean);
       } else {
         for (uint32_t i = lo; i < hi; ++i) sum = __dadd_rn(sum, static_cast<double>(stage[i]));
+        out[j0 + jl] = __double2float_rn(__ddiv_rn(sum, static_cast<double>(hi - lo)));
       }
-      out[j0 + jl] = __double2float_rn(__ddiv_rn(sum, static_cast<double>(hi - lo)));
     }
   }
 }

@@ -134,6 +134,28 @@ def test_random_against_oracle(be):
         assert fwd(be, data, c).tobytes() == O.mockpose_forward(data, c).tobytes()
 
 
+@pytest.mark.parametrize("c", [1.7, 2.46, 3.37, 5.5, 7.9])
+def test_extreme_values(be, c):
+    """Random float bit patterns over the whole exponent range, plus zeros of
+    both signs, infinities and NaNs: the short-segment division (segmean.cu,
+    Markstein's correction step) and its __ddiv_rn fallback for non-finite
+    sums must match the reference's sum / n bit for bit (NaNs: same positions)."""
+    rng = np.random.default_rng(int(c * 1000))
+    bits = rng.integers(0, 2**32, 200000, dtype=np.uint64).astype(np.uint32)
+    data = bits.view(np.float32).copy()
+    data[~np.isfinite(data)] = 1.5
+    special = rng.integers(0, data.size, 400)
+    data[special[:100]] = np.inf
+    data[special[100:200]] = -np.inf
+    data[special[200:300]] = np.nan
+    data[special[300:350]] = -0.0
+    data[special[350:]] = 0.0
+    got, want = fwd(be, data, c), O.mockpose_forward(data, c)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    fin = ~np.isnan(want)
+    assert got[fin].tobytes() == want[fin].tobytes()
+
+
 @pytest.mark.parametrize("c", [1.0, 47.5, 100.0, 1000.0, 4096.0])
 def test_wide_segments(be, c):
     # widths above the shared-memory staging bound take the direct kernel
