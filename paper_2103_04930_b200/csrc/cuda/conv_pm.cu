@@ -60,8 +60,11 @@ struct PmCfg {
 #define AVEC_PM_ROWW128 0
 #endif
   // AVEC_PM_ROWW128: N = 128 tiles trade their third window stage for row-wide
-  // weight stages (5 instead of 3)
-  static constexpr int kWinStages = POOL ? 6 : N == 64 ? 4 : N == 256 ? 2
+  // weight stages (5 instead of 3). N = 96 (BODY_25's dense blocks) keeps a
+  // fourth window in flight (3 row-wide weight stages instead of 5): its
+  // short-K chunks consume a window in ~600 cycles, less than a window load's
+  // latency; C5 dense-block convs 95-107 -> 88-98 us (profiles/r02_layers_c5.txt)
+  static constexpr int kWinStages = POOL ? 6 : N == 64 ? 4 : N == 256 ? 2 : N == 96 ? 4
                                   : (N == 128 && AVEC_PM_ROWW128) ? 2 : 3 + AVEC_PM_WIN_EXTRA;
   static constexpr int kWgtBytes = (N / NCTA) * 128;  // this CTA's N/NCTA rows x 64 bf16
   static constexpr int kAccCols = SUBS_M * N;
