@@ -19,6 +19,11 @@
 // several co-resident CTAs per SM.
 // Results are bit-identical to the im2col + 1x1 path it replaces (same bf16
 // operands, same K order, same MMA shape).
+//
+// TF32 (a net whose spec says "input tf32"): the A row is the 27 taps as fp32
+// rounded to tf32 (cvt.rna) plus 5 zeros, 32 floats = one 128-byte SW128 row,
+// the weights [64 cout][32] tf32, and K = 32 runs as four kind::tf32 M128 N64
+// K8 MMAs; same tile, staging and epilogue.
 #include <cuda_bf16.h>
 
 #include "conv_tc.cuh"
@@ -50,6 +55,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+template <bool TF32>
 __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
     conv_first_kernel(const __grid_constant__ ConvMaps maps, const __grid_constant__ ConvParams p,
                       const float* __restrict__ frames) {
@@ -77,7 +83,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
     sslope[tid] = g.act == 1 ? 0.f : (g.act == 2 && tid < g.cout) ? g.slope[tid] : 1.f;
   }
   // K channels 32..63 of the A tile are always zero: write them once
-  {
+  if (!TF32) {
     uint8_t* row = sa + tid * 128;
 #pragma unroll
     for (int q = 4; q < 8; ++q) *reinterpret_cast<uint4*>(row + ((q ^ (tid & 7)) << 4)) = make_uint4(0, 0, 0, 0);
@@ -129,7 +135,18 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
     const int ww = o - hh * p.Wp;
     const bool valid = hh < p.H && ww < p.W;
     // ---- im2col row of this pixel: taps k = ci*9 + r*3 + s
-    {
+    if constexpr (TF32) {
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 27; ++i) v[i] = to_tf32(x[i]);
+#pragma unroll
+      for (int i = 27; i < 32; ++i) v[i] = 0.f;
+      uint8_t* row = sa + tid * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(row + ((q ^ (tid & 7)) << 4)) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
       uint32_t packed[16];
 #pragma unroll
       for (int i = 0; i < 13; ++i) packed[i] = pack2(x[2 * i], x[2 * i + 1]);
@@ -147,11 +164,18 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
     if (tid == 0) {
       tc_fence_after();
       if (first) mbar_wait(w_full, 0);
-      const uint32_t idesc = idesc_bf16_f32(128, 64);
       const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sw);
+      if constexpr (TF32) {
+        const uint32_t idesc = idesc_tf32_f32(128, 64);
 #pragma unroll
-      for (int kk = 0; kk < 2; ++kk)  // K = 32 covers the 27 taps
-        mma_bf16_ss(tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), idesc, kk ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk)  // K = 32 fp32 = the 128-byte row, 8 per MMA
+          mma_tf32_ss(tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), idesc, kk ? 1u : 0u);
+      } else {
+        const uint32_t idesc = idesc_bf16_f32(128, 64);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)  // K = 32 covers the 27 taps
+          mma_bf16_ss(tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), idesc, kk ? 1u : 0u);
+      }
       mma_commit(mma_done);
     }
     first = false;
@@ -205,7 +229,10 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSm)
 }  // namespace
 
 void conv_first_configure() {
-  check_cuda(cudaFuncSetAttribute(conv_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  check_cuda(cudaFuncSetAttribute(conv_first_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  FirstSmem::total + 1024),
+             "conv_first smem attribute");
+  check_cuda(cudaFuncSetAttribute(conv_first_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   FirstSmem::total + 1024),
              "conv_first smem attribute");
 }
@@ -214,7 +241,10 @@ void launch_conv_first(const ConvMaps& maps, const ConvParams& p, const float* f
                        cudaStream_t stream) {
   const int cap = sm_count * kFCtasPerSm;
   const int grid = p.total_tiles < cap ? p.total_tiles : cap;
-  conv_first_kernel<<<grid, kFThreads, FirstSmem::total + 1024, stream>>>(maps, p, frames);
+  if (p.tf32)
+    conv_first_kernel<true><<<grid, kFThreads, FirstSmem::total + 1024, stream>>>(maps, p, frames);
+  else
+    conv_first_kernel<false><<<grid, kFThreads, FirstSmem::total + 1024, stream>>>(maps, p, frames);
   check_cuda(cudaGetLastError(), "conv_first launch");
 }
 

@@ -102,6 +102,7 @@ struct ConvParams {
   // ([tile][split][tile_px][128]) and conv_tc_reduce_kernel sums them in split
   // order (deterministic) and applies the epilogue. 1 = off.
   int splits;
+  int tf32;            // conv_first: tf32 operands (kind::tf32) instead of bf16
   float* ws;
   ConvGroupParams g[kConvMaxGroups];
 };

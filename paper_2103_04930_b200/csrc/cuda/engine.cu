@@ -63,6 +63,15 @@ uint16_t bf16_bits(float x) {
   u += 0x7fffu + ((u >> 16) & 1u);
   return uint16_t(u >> 16);
 }
+// fp32 -> tf32 bit pattern, round to nearest, ties away from zero (= cvt.rna.tf32.f32)
+float tf32_value(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
 float bf16_value(float x) {
   uint32_t u = uint32_t(bf16_bits(x)) << 16;
   float r;
@@ -105,6 +114,20 @@ CUtensorMap make_map_2d(const void* base, uint64_t cols, uint64_t rows, uint32_t
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+// 2D fp32 [rows][cols] row-major, box {32 cols = 128 B, box_rows}, 128-byte swizzle
+CUtensorMap make_map_2d_f32(const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(AVEC_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed: " + std::to_string(int(r)));
   return m;
 }
 
@@ -286,6 +309,8 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
     w_off[i] = take(size_t(L.cout_pad) * L.exec_k * L.exec_k * L.cin_pad * 2);
     b_off[i] = take(size_t(L.cout_pad) * 4 * 2);  // bias, then PReLU slopes
   }
+  // "input tf32": the first layer's weights again, as tf32 [cout_pad][32]
+  const size_t tf32_off = f.input_tf32 ? take(size_t(net->layers[0].cout_pad) * 32 * 4) : 0;
   std::vector<uint8_t> host(total, 0);
   const float* src = weights;
   for (size_t i = 0; i < f.convs.size(); ++i) {
@@ -298,6 +323,11 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
       for (int co = 0; co < d.cout; ++co)
         for (int t = 0; t < 27; ++t)  // t = ci*9 + r*3 + s, the im2col channel order
           w[size_t(co) * 64 + t] = bf16_bits(src[size_t(co) * 27 + t]);
+      if (f.input_tf32) {
+        float* wt = reinterpret_cast<float*>(host.data() + tf32_off);
+        for (int co = 0; co < d.cout; ++co)
+          for (int t = 0; t < 27; ++t) wt[size_t(co) * 32 + t] = tf32_value(src[size_t(co) * 27 + t]);
+      }
       src += size_t(d.cout) * 27;
     } else {
       // Caffe input channel ci -> internal channel of the layer's input window
@@ -349,6 +379,7 @@ std::shared_ptr<PoseNet> upload_posenet(int device, PoseFamily fam, const float*
     net->layers[i].bias = reinterpret_cast<float*>(base + b_off[i]);
     net->layers[i].slope = reinterpret_cast<float*>(base + b_off[i]) + net->layers[i].cout_pad;
   }
+  if (f.input_tf32) net->layers[0].w_tf32 = reinterpret_cast<float*>(base + tf32_off);
   return net;
 }
 
@@ -438,7 +469,12 @@ struct PlanBuilder {
     gp.out = plan.bufs[out.buf]->p;
     gp.out_c_off = out.c_off;
     gp.out_c_stride = out.c_stride;
-    op.maps.wgt[0] = make_map_2d(L.w, 64, L.cout_pad, 64);
+    if (L.w_tf32) {  // "input tf32": kind::tf32 MMAs on fp32 taps and weights
+      p.tf32 = 1;
+      op.maps.wgt[0] = make_map_2d_f32(L.w_tf32, 32, L.cout_pad, 64);
+    } else {
+      op.maps.wgt[0] = make_map_2d(L.w, 64, L.cout_pad, 64);
+    }
     op.maps.out[0] = make_map_3d_store(plan.bufs[out.buf]->p, plan.buf_c[out.buf], uint64_t(gi.Hp()) * gi.Wp(),
                                        plan.n);
     TensorView in;
@@ -458,7 +494,9 @@ struct PlanBuilder {
     const ConvLayerDev& A = net.layers[l1];
     const ConvLayerDev& B = net.layers[l2];
     const Geometry& g0 = plan.geo[0];
-    if (!on || A.def.cin != 3 || A.def.k != 3 || A.def.cout != 64 || A.def.act != kActRelu || B.exec_k != 3 ||
+    // ("input tf32" nets take the conv_first path: conv12 is bf16-only)
+    if (!on || net.fam.input_tf32 || A.def.cin != 3 || A.def.k != 3 || A.def.cout != 64 || A.def.act != kActRelu ||
+        B.exec_k != 3 ||
         B.def.cin != 64 || B.def.cout != 64 || B.def.act != kActRelu || g0.H % 2 || g0.W % 4 ||
         plan.buf_c[pooled] != 64)
       return false;
@@ -1514,10 +1552,12 @@ void posenet_layer_rows(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, 
         std::fill(o, o + size_t(Wl) * cdim, 0.f);
         continue;
       }
-      if (v.buf == -2) {  // the frames as the first layer sees them: bf16(x - 0.5)
+      if (v.buf == -2) {  // the frames as the first layer sees them: bf16 (or tf32) of x - 0.5
         for (int x = 0; x < Wl; ++x)
-          for (int ch = 0; ch < 3; ++ch)
-            o[x * 3 + ch] = bf16_value(in[((size_t(b) * 3 + ch) * Hl + y) * Wl + x] - 0.5f);
+          for (int ch = 0; ch < 3; ++ch) {
+            const float xv = in[((size_t(b) * 3 + ch) * Hl + y) * Wl + x] - 0.5f;
+            o[x * 3 + ch] = f.input_tf32 ? tf32_value(xv) : bf16_value(xv);
+          }
       } else if (v.buf == -1) {
         if (out_all.empty()) {
           out_all.resize(plan->out_elems);
@@ -1576,13 +1616,14 @@ void posenet_layer_io(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, ui
     const int lv = v.buf >= 0 ? v.level : d.level;
     const Geometry& g = plan->geo[lv];
     const int Hl = int(h) >> lv, Wl = int(w) >> lv;
-    if (v.buf == -2) {  // network input as the first layer sees it: bf16(x - 0.5), NHWC
+    if (v.buf == -2) {  // network input as the first layer sees it: bf16 (or tf32) of x - 0.5, NHWC
       for (int b = 0; b < n_img; ++b)
         for (int y = 0; y < Hl; ++y)
           for (int x = 0; x < Wl; ++x)
-            for (int ch = 0; ch < 3; ++ch)
-              dst[((size_t(b) * Hl + y) * Wl + x) * 3 + ch] =
-                  bf16_value(in[((size_t(b) * 3 + ch) * Hl + y) * Wl + x] - 0.5f);
+            for (int ch = 0; ch < 3; ++ch) {
+              const float xv = in[((size_t(b) * 3 + ch) * Hl + y) * Wl + x] - 0.5f;
+              dst[((size_t(b) * Hl + y) * Wl + x) * 3 + ch] = f.input_tf32 ? tf32_value(xv) : bf16_value(xv);
+            }
       return;
     }
     if (v.buf == -1) {  // fp32 NCHW plan output -> NHWC channel range

@@ -49,6 +49,7 @@ struct ConvLayerDev {
   int exec_k = 0;  // filter size as executed (the first layer: 1, K = its 27 taps, conv_first.cu)
   int cin_pad = 0, cout_pad = 0;
   void* w = nullptr;       // bf16 [cout_pad][k*k][cin_pad]
+  float* w_tf32 = nullptr; // the first layer of an "input tf32" net: [cout_pad][32] tf32 (27 taps, zeros)
   float* bias = nullptr;   // [cout_pad]
   float* slope = nullptr;  // [cout_pad] PReLU slopes (zeros unless act == prelu)
 };

@@ -156,6 +156,11 @@ PoseFamily parse_avecnet(const uint8_t* s, size_t n) {
     } else if (key == "stages") {
       ls >> f.stages;
       if (f.stages < 2 || f.stages > 6) fail(AVEC_ERR_INVALID_MODEL, "stages must be 2..6");
+    } else if (key == "input") {
+      std::string dt;
+      ls >> dt;
+      if (dt != "bf16" && dt != "tf32") fail(AVEC_ERR_INVALID_MODEL, "input must be bf16 or tf32");
+      f.input_tf32 = dt == "tf32";
     } else if (key == "init") {
       std::string kind;
       ls >> kind >> f.init_seed;

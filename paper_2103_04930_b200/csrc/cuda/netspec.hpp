@@ -41,6 +41,9 @@ struct PoseFamily {
   int trunk_channels = 128;
   std::vector<ConvDef> convs;  // weights-blob order
   uint64_t init_seed = 1;
+  // "input tf32": conv1_1 takes the fp32 frames as tf32 operands (10-bit
+  // mantissa) instead of bf16 (7-bit); every later layer stays bf16
+  bool input_tf32 = false;
   int out_channels() const { return heat_channels + paf_channels; }
   uint64_t weight_floats() const;
   bool body25() const { return family == "openpose_body25"; }

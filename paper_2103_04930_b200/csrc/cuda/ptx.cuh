@@ -314,6 +314,33 @@ __device__ __forceinline__ uint64_t desc_sw32(uint32_t smem_addr) {
          ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
 }
 
+// Instruction descriptor, kind::tf32: tf32 x tf32 -> f32, both K-major (K = 8
+// per MMA; a 32-byte K step is still +2 in a descriptor).
+__host__ __device__ constexpr uint32_t idesc_tf32_f32(uint32_t M, uint32_t N) {
+  return (1u << 4)            // c_format F32
+         | (2u << 7)          // a_format TF32
+         | (2u << 10)         // b_format TF32
+         | ((N >> 3) << 17)   // n_dim
+         | ((M >> 4) << 24);  // m_dim
+}
+
+__device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// fp32 -> tf32 (round to nearest, ties away from zero), as an fp32 bit pattern
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 // Instruction descriptor, kind::f16: bf16 x bf16 -> f32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4)            // c_format F32

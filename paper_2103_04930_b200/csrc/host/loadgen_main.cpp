@@ -36,6 +36,7 @@ std::vector<float> gen_batch(std::uint64_t seed, std::uint32_t first, std::uint3
 
 int main(int argc, char** argv) {
   std::string endpoint = "127.0.0.1:7000", model = "posenet";
+  std::string input_dtype = "bf16";  // pose nets: "tf32" = the tf32 first layer (netspec "input tf32")
   unsigned clients = 1, steps = 20, warmup = 3, batch = 8, width = 656, height = 368;
   unsigned long elems_override = 0;  // raw FrameData size (memcpy sweep), Resolution = width x (E/width)
   // client 0's timed cycles as a reference-format run record (record.hpp)
@@ -50,6 +51,7 @@ int main(int argc, char** argv) {
     else if (a == "--width") width = std::stoul(v);
     else if (a == "--height") height = std::stoul(v);
     else if (a == "--model") model = v;
+    else if (a == "--input") input_dtype = v;
     else if (a == "--elems") elems_override = std::stoul(v);
     else if (a == "--record-csv") record_csv = v;
     else if (a == "--record-md") record_md = v;
@@ -62,11 +64,16 @@ int main(int argc, char** argv) {
   }
   using namespace avec;
   wire::ModelDescriptor md;
+  if (input_dtype != "bf16" && input_dtype != "tf32") {
+    std::fprintf(stderr, "--input must be bf16 or tf32\n");
+    return 2;
+  }
+  const std::string input_line = input_dtype == "tf32" ? "input tf32\n" : "";
   if (model == "posenet") {
-    std::string s = "avecnet 1\nfamily openpose_coco\ninit he_uniform 1\n";
+    std::string s = "avecnet 1\nfamily openpose_coco\n" + input_line + "init he_uniform 1\n";
     md = wire::make_model("openpose_coco", {s.begin(), s.end()}, {}, 192.0 / 57.0);
   } else if (model == "posenet-body25") {
-    std::string s = "avecnet 1\nfamily openpose_body25\ninit he_uniform 1\n";
+    std::string s = "avecnet 1\nfamily openpose_body25\n" + input_line + "init he_uniform 1\n";
     md = wire::make_model("openpose_body25", {s.begin(), s.end()}, {}, 192.0 / 78.0);
   } else {
     // the reference's model: opaque structure -> segment means; "mockpose-c1"

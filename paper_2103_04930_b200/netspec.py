@@ -43,10 +43,16 @@ class ConvDef:
         return self.act
 
 
-def spec(family: str = "openpose_coco", stages: int = 6, seed: int = 1) -> bytes:
+def spec(family: str = "openpose_coco", stages: int = 6, seed: int = 1, input_dtype: str = "bf16") -> bytes:
+    """avecnet structure bytes. input_dtype "tf32": conv1_1 consumes the fp32
+    frames as tf32 tensor-core operands instead of bf16 (conv_first.cu)."""
     lines = ["avecnet 1", f"family {family}"]
     if stages != 6:
         lines.append(f"stages {stages}")
+    if input_dtype != "bf16":
+        if input_dtype != "tf32":
+            raise ValueError("input_dtype must be bf16 or tf32")
+        lines.append("input tf32")
     lines.append(f"init he_uniform {seed}")
     return ("\n".join(lines) + "\n").encode()
 

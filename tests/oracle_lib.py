@@ -100,6 +100,16 @@ def synth_blobs(seed: int, structure_bytes: int, weights_bytes: int):
     return s.tobytes(), w.tobytes()
 
 
+def tf32_round(a: np.ndarray) -> np.ndarray:
+    """fp32 -> tf32 (10-bit mantissa), round to nearest, ties away from zero:
+    cvt.rna.tf32.f32, which conv_first.cu applies to the frames of an
+    "input tf32" net (and the upload to its first-layer weights)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    fin = (u & 0x7F800000) != 0x7F800000
+    r = np.where(fin, (u + 0x1000) & 0xFFFFE000, u).astype(np.uint32)
+    return r.view(np.float32).reshape(np.shape(a))
+
+
 def bf16_round(a: np.ndarray) -> np.ndarray:
     """Vectorised RNE fp32 -> bf16 -> fp32 (same rule as oracle_bf16_round)."""
     a = np.ascontiguousarray(a, np.float32)

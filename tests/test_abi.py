@@ -63,6 +63,17 @@ def test_invalid_spec_is_invalid_model():
     assert e.value.name == "invalid_model"
 
 
+def test_input_precision_spec_key():
+    """`input tf32` selects the tf32 first layer (test_gpu_tf32.py); it does not
+    change the weights blob; anything but bf16 / tf32 is an invalid model."""
+    from paper_2103_04930_b200 import AvecError, netspec, synth_posenet_weights
+    s32 = netspec.spec(input_dtype="tf32")
+    assert b"input tf32" in s32 and b"input" not in netspec.spec()
+    assert (synth_posenet_weights(s32) == synth_posenet_weights(netspec.spec())).all()
+    with pytest.raises(AvecError):
+        synth_posenet_weights(b"avecnet 1\nfamily openpose_coco\ninput fp8\n")
+
+
 def test_host_library_exports_frame_groups():
     """The split policy's partition is exported from the C++ host library
     (b200_backend.hpp) and is what sharding.py binds."""

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--json", default="")
+    ap.add_argument("--input", default="bf16", choices=["bf16", "tf32"], help="first-layer operand precision")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -29,7 +30,7 @@ def main():
     }[a.config]
     B = a.batch or B
     be = B200Backend(0, slots=1)
-    h = be.register_model(make_model(fam, netspec.spec(fam), b"", div))
+    h = be.register_model(make_model(fam, netspec.spec(fam, input_dtype=a.input), b"", div))
     dims = Dims(1, 3 * B, H, W)
     x = torch.from_numpy(np.random.default_rng(7).random(dims.elem_count(), dtype=np.float32)).cuda()
     prof = be.profile(h, dims, x.data_ptr(), reps=a.reps)
