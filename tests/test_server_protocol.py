@@ -10,7 +10,6 @@ import json
 import pathlib
 import struct
 import subprocess
-
 import time
 
 import numpy as np
