@@ -553,6 +553,162 @@ __global__ void nms4_tiles_kernel(const float* __restrict__ in, int H, int W, fl
   }
 }
 
+// NMS pass 1 (W % 8 == 0, W <= 2048; the default): same per-tile peak lists
+// as nms4_tiles_kernel. The tile's R + 2 rows land in shared memory by one
+// bulk copy (all bytes in flight at once, no registers held for them); then
+// each thread owns 8 columns and walks the rows top to bottom, reading every
+// row ONCE (two conflict-free 16-byte loads), taking the neighbour columns
+// from the adjacent lanes by shuffle (the warp's edge lanes read one scalar),
+// and forming each row's horizontal 3-max and left/right max once for the
+// rows above and below. nms4_tiles_kernel read every row three times with
+// 4-way-conflicting scalar neighbour loads (~40 instructions per pixel,
+// issue-bound). Same peak test (strictly greater than the max.NaN of the 8
+// neighbours; max is associative and commutative, so the regrouping cannot
+// change a comparison) and the same raster-ordered lists for nms_gather_kernel.
+constexpr int kNms8Rows = 8;  // measured per tile height (C2 planes): 4: 54.7 us, 6: 48.0, 8: 47.8, 12: 52.8, 16: 58.2
+
+// One tile per block (a persistent, double-buffered variant in which each
+// block prefetched its next tile measured slower, 67 us: fewer resident
+// warps for the compute).
+template <int R>
+__global__ void __launch_bounds__(256) nms8_tiles_kernel(const float* __restrict__ in, int H, int W, float threshold,
+                                                         int cap, int tiles, int* __restrict__ tile_counts,
+                                                         NmsPeak* __restrict__ tile_peaks) {
+  extern __shared__ __align__(16) float tile[];  // rows y0-1 .. y0+R (-inf outside the plane)
+  __shared__ int wbase[R][8];
+  __shared__ uint8_t pmask[R][256];
+  __shared__ __align__(8) uint64_t bar;
+  const float NEG = -__int_as_float(0x7f800000);
+  const int x8 = threadIdx.x, c0 = 8 * x8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool col_ok = c0 < W;
+  const int t = blockIdx.x;  // = plane * tiles + tile index
+  const int pl = t / tiles, y0 = (t - pl * tiles) * R;
+  const int rows = y0 + R < H ? R : H - y0;
+  const int ya = y0 > 0 ? y0 - 1 : 0, yb = y0 + rows < H ? y0 + rows + 1 : H;  // in-plane rows [ya, yb)
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_barrier_init();
+    const uint32_t bytes = static_cast<uint32_t>(yb - ya) * W * 4;
+    ptx::mbar_arrive_expect_tx(&bar, bytes);
+    ptx::bulk_load(tile + (ya - (y0 - 1)) * W, in + static_cast<size_t>(pl) * H * W + static_cast<size_t>(ya) * W,
+                   bytes, &bar);
+  }
+  if (y0 == 0)
+    for (int i = threadIdx.x; i < W; i += blockDim.x) tile[i] = NEG;
+  if (y0 + rows == H)
+    for (int i = threadIdx.x; i < W; i += blockDim.x) tile[(rows + 1) * W + i] = NEG;
+  __syncthreads();  // (also orders the barrier's init before the other threads' waits)
+  ptx::mbar_wait(&bar, 0);
+  auto mx = [](float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+  };
+  struct Row {
+    float4 a, b;
+    float el, er;  // lane 0: column c0 - 1; lane 31: column c0 + 8
+  };
+  {
+    auto load = [&](int k) {  // tile row k = image row y0 - 1 + k
+      Row r;
+      const float* rp = tile + k * W + c0;
+      const float4 n4 = make_float4(NEG, NEG, NEG, NEG);
+      r.a = col_ok ? reinterpret_cast<const float4*>(rp)[0] : n4;
+      r.b = col_ok ? reinterpret_cast<const float4*>(rp)[1] : n4;
+      r.el = (lane == 0 && col_ok && c0 > 0) ? rp[-1] : NEG;
+      r.er = (lane == 31 && c0 + 8 < W) ? rp[8] : NEG;
+      return r;
+    };
+    // hm: max of the 3 columns around each of mine; lr: max of left and right
+    auto horiz = [&](const Row& r, float (&v)[8], float (&lr)[8], float (&hm)[8]) {
+      float left = __shfl_up_sync(0xffffffffu, r.b.w, 1);
+      float right = __shfl_down_sync(0xffffffffu, r.a.x, 1);
+      if (lane == 0) left = r.el;
+      if (lane == 31) right = r.er;
+      const float e[10] = {left, r.a.x, r.a.y, r.a.z, r.a.w, r.b.x, r.b.y, r.b.z, r.b.w, right};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = e[i + 1];
+        lr[i] = mx(e[i], e[i + 2]);
+        hm[i] = mx(lr[i], e[i + 1]);
+      }
+    };
+    float v_cur[8], lr_cur[8], hm_cur[8], hm_prev[8];
+    {
+      float vd[8], lrd[8];
+      const Row r0 = load(0), r1 = load(1);
+      horiz(r0, vd, lrd, hm_prev);
+      horiz(r1, v_cur, lr_cur, hm_cur);
+    }
+    Row nxt = load(2);
+    for (int r = 0; r < rows; ++r) {
+      float v_n[8], lr_n[8], hm_n[8];
+      horiz(nxt, v_n, lr_n, hm_n);  // row y0 + r + 1
+      if (r + 3 <= rows + 1) nxt = load(r + 3);
+      unsigned m = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float nb = mx(mx(hm_prev[i], hm_n[i]), lr_cur[i]);
+        m |= (v_cur[i] > threshold && v_cur[i] > nb) ? (1u << i) : 0u;
+      }
+      if (!col_ok) m = 0;
+      pmask[r][threadIdx.x] = static_cast<uint8_t>(m);
+      const int c = __reduce_add_sync(0xffffffffu, __popc(m));
+      if (lane == 0) wbase[r][wid] = c;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        hm_prev[i] = hm_cur[i];
+        hm_cur[i] = hm_n[i];
+        lr_cur[i] = lr_n[i];
+        v_cur[i] = v_n[i];
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {
+      // exclusive prefix over (row, warp) in raster order: lane l sums a run
+      // of the rows * nw counts, then one warp scan
+      const int n = rows * nw, per = (n + 31) / 32, beg = lane * per;
+      int run = 0;
+      for (int e = beg; e < beg + per && e < n; ++e) run += wbase[e / nw][e % nw];
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int q = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += q;
+      }
+      int acc = incl - run;
+      for (int e = beg; e < beg + per && e < n; ++e) {
+        const int c = wbase[e / nw][e % nw];
+        wbase[e / nw][e % nw] = acc;
+        acc += c;
+      }
+      if (lane == 31) tile_counts[t] = incl;  // t = pl * tiles + tile index
+    }
+    __syncthreads();
+    NmsPeak* out = tile_peaks + static_cast<size_t>(t) * cap;
+    for (int r = 0; r < rows; ++r) {
+      if (wbase[r][0] >= cap) break;  // the tile's list is full (uniform: shared offsets only grow)
+      const unsigned m = pmask[r][threadIdx.x];
+      if (!__any_sync(0xffffffffu, m)) continue;  // typical heatmaps: most warp rows have no peak
+      const int mine = __popc(m);
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int q = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += q;
+      }
+      int idx = wbase[r][wid] + incl - mine;
+      for (int i = 0; i < 8 && idx < cap; ++i) {
+        if (!((m >> i) & 1u)) continue;
+        const int x = c0 + i;
+        out[idx] = NmsPeak{x, y0 + r, tile[(r + 1) * W + x]};
+        ++idx;
+      }
+    }
+  }
+}
+
 __global__ void nms_gather_kernel(const float* __restrict__ in, int H, int W, int tiles, int cap, int max_peaks,
                                   const int* __restrict__ tile_counts, const NmsPeak* __restrict__ tile_peaks,
                                   int* __restrict__ counts, float* __restrict__ peaks) {
@@ -714,7 +870,8 @@ void launch_upsample(const float* d_in, int planes, int h, int w, int scale, flo
 
 size_t nms_scratch_bytes(int planes, int H, int /*W*/, int max_peaks) {
   // two-pass row counts/offsets, or the tile-compact path's counts + peak lists
-  const size_t tiles = (static_cast<size_t>(H) + kNmsRows1 - 1) / kNmsRows1;
+  const int rmin = kNmsRows1 < kNms8Rows ? kNmsRows1 : kNms8Rows;  // the smaller tile height of the two paths
+  const size_t tiles = (static_cast<size_t>(H) + rmin - 1) / rmin;
   const size_t compact = static_cast<size_t>(planes) * tiles * (sizeof(int) + sizeof(NmsPeak) * max_peaks) + 64;
   return std::max(2 * static_cast<size_t>(planes) * H * sizeof(int), compact);
 }
@@ -747,6 +904,33 @@ void launch_nms(const float* d_in, int planes, int H, int W, float threshold, in
       const char* e = std::getenv("AVEC_NMS_LOOKBACK");
       return e && e[0] == '1' ? 1 : 0;
     }();
+    static const bool staged = [] {  // AVEC_NMS_STAGED=1: the shared-memory tile pass 1
+      const char* e = std::getenv("AVEC_NMS_STAGED");
+      return e && e[0] == '1';
+    }();
+    if (!two_pass && mode == 0 && !staged && W % 8 == 0 && W <= 2048 &&
+        (reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && max_peaks > 0) {
+      const int tiles_s = (H + kNms8Rows - 1) / kNms8Rows;
+      const int threads8 = ((W / 8) + 31) / 32 * 32;
+      int* tile_counts = static_cast<int*>(d_scratch);
+      auto* tile_peaks = reinterpret_cast<NmsPeak*>(
+          reinterpret_cast<uintptr_t>(tile_counts + static_cast<size_t>(planes) * tiles_s + 15) & ~uintptr_t(15));
+      const size_t tile8_bytes = static_cast<size_t>(kNms8Rows + 2) * W * sizeof(float);
+      static bool configured = false;
+      if (!configured) {  // up to W = 2048 (+ ~2.3 KB of static tables)
+        check_cuda(cudaFuncSetAttribute(nms8_tiles_kernel<kNms8Rows>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (kNms8Rows + 2) * 2048 * 4), "nms smem");
+        configured = true;
+      }
+      const int total = tiles_s * planes;
+      nms8_tiles_kernel<kNms8Rows><<<total, threads8, tile8_bytes, stream>>>(d_in, H, W, threshold, max_peaks, tiles_s,
+                                                                           tile_counts, tile_peaks);
+      nms_gather_kernel<<<planes, 128, (tiles_s + 1) * sizeof(int), stream>>>(d_in, H, W, tiles_s, max_peaks,
+                                                                             max_peaks, tile_counts, tile_peaks,
+                                                                             d_counts, d_peaks);
+      check_cuda(cudaGetLastError(), "nms launch");
+      return;
+    }
     if (!two_pass && mode == 0 && (reinterpret_cast<uintptr_t>(d_in) & 15) == 0 && max_peaks > 0) {
       if (tile1_bytes > 48 * 1024)
         check_cuda(cudaFuncSetAttribute(nms4_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
