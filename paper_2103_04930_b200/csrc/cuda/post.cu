@@ -642,26 +642,33 @@ __global__ void __launch_bounds__(256) nms8_tiles_kernel(const float* __restrict
       horiz(r1, v_cur, lr_cur, hm_cur);
     }
     Row nxt = load(2);
-    for (int r = 0; r < rows; ++r) {
-      float v_n[8], lr_n[8], hm_n[8];
-      horiz(nxt, v_n, lr_n, hm_n);  // row y0 + r + 1
-      if (r + 3 <= rows + 1) nxt = load(r + 3);
-      unsigned m = 0;
+    // unrolled over the tile's R rows (a short last tile skips the rest), so
+    // the row-to-row rotation of the 32 per-thread values is register renaming
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float nb = mx(mx(hm_prev[i], hm_n[i]), lr_cur[i]);
-        m |= (v_cur[i] > threshold && v_cur[i] > nb) ? (1u << i) : 0u;
-      }
-      if (!col_ok) m = 0;
-      pmask[r][threadIdx.x] = static_cast<uint8_t>(m);
-      const int c = __reduce_add_sync(0xffffffffu, __popc(m));
-      if (lane == 0) wbase[r][wid] = c;
+    for (int r = 0; r < R; ++r) {
+      if (r < rows) {
+        float v_n[8], lr_n[8], hm_n[8];
+        horiz(nxt, v_n, lr_n, hm_n);  // row y0 + r + 1
+        if (r + 3 <= rows + 1) nxt = load(r + 3);
+        unsigned m = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        hm_prev[i] = hm_cur[i];
-        hm_cur[i] = hm_n[i];
-        lr_cur[i] = lr_n[i];
-        v_cur[i] = v_n[i];
+        for (int i = 0; i < 8; ++i) {
+          // v > threshold and v > every neighbour, as one comparison with
+          // max.NaN(neighbours, threshold): a NaN anywhere still fails it
+          const float lim = mx(mx(mx(hm_prev[i], hm_n[i]), lr_cur[i]), threshold);
+          m |= v_cur[i] > lim ? (1u << i) : 0u;
+        }
+        if (!col_ok) m = 0;
+        pmask[r][threadIdx.x] = static_cast<uint8_t>(m);
+        const int c = __reduce_add_sync(0xffffffffu, __popc(m));
+        if (lane == 0) wbase[r][wid] = c;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          hm_prev[i] = hm_cur[i];
+          hm_cur[i] = hm_n[i];
+          lr_cur[i] = lr_n[i];
+          v_cur[i] = v_n[i];
+        }
       }
     }
     __syncthreads();
