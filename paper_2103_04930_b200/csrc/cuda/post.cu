@@ -565,7 +565,7 @@ __global__ void nms4_tiles_kernel(const float* __restrict__ in, int H, int W, fl
 // issue-bound). Same peak test (strictly greater than the max.NaN of the 8
 // neighbours; max is associative and commutative, so the regrouping cannot
 // change a comparison) and the same raster-ordered lists for nms_gather_kernel.
-constexpr int kNms8Rows = 8;  // measured per tile height (C2 planes): 4: 54.7 us, 6: 48.0, 8: 47.8, 12: 52.8, 16: 58.2
+constexpr int kNms8Rows = 5;  // tile height, measured on C2 planes (stress / sparse threshold, us): 4: 44.4 / 41.9, 5: 39.9 / 38.3, 6: 40.5 / 38.5, 8: 42.3 / 39.0, 12: 47.6 / 44.5, 16: 49.6 / 46.9
 
 // One tile per block (a persistent, double-buffered variant in which each
 // block prefetched its next tile measured slower, 67 us: fewer resident
@@ -642,33 +642,32 @@ __global__ void __launch_bounds__(256) nms8_tiles_kernel(const float* __restrict
       horiz(r1, v_cur, lr_cur, hm_cur);
     }
     Row nxt = load(2);
-    // unrolled over the tile's R rows (a short last tile skips the rest), so
-    // the row-to-row rotation of the 32 per-thread values is register renaming
+    // unrolled over all R rows with no branch (a short last tile computes the
+    // rows past its end from stale shared memory and masks them), so the
+    // row-to-row rotation of the per-thread values is register renaming
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      if (r < rows) {
-        float v_n[8], lr_n[8], hm_n[8];
-        horiz(nxt, v_n, lr_n, hm_n);  // row y0 + r + 1
-        if (r + 3 <= rows + 1) nxt = load(r + 3);
-        unsigned m = 0;
+      float v_n[8], lr_n[8], hm_n[8];
+      horiz(nxt, v_n, lr_n, hm_n);  // row y0 + r + 1
+      if (r + 3 <= R + 1) nxt = load(r + 3);
+      unsigned m = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          // v > threshold and v > every neighbour, as one comparison with
-          // max.NaN(neighbours, threshold): a NaN anywhere still fails it
-          const float lim = mx(mx(mx(hm_prev[i], hm_n[i]), lr_cur[i]), threshold);
-          m |= v_cur[i] > lim ? (1u << i) : 0u;
-        }
-        if (!col_ok) m = 0;
-        pmask[r][threadIdx.x] = static_cast<uint8_t>(m);
-        const int c = __reduce_add_sync(0xffffffffu, __popc(m));
-        if (lane == 0) wbase[r][wid] = c;
+      for (int i = 0; i < 8; ++i) {
+        // v > threshold and v > every neighbour, as one comparison with
+        // max.NaN(neighbours, threshold): a NaN anywhere still fails it
+        const float lim = mx(mx(mx(hm_prev[i], hm_n[i]), lr_cur[i]), threshold);
+        m |= v_cur[i] > lim ? (1u << i) : 0u;
+      }
+      if (!col_ok || r >= rows) m = 0;
+      pmask[r][threadIdx.x] = static_cast<uint8_t>(m);
+      const int c = __reduce_add_sync(0xffffffffu, __popc(m));
+      if (lane == 0) wbase[r][wid] = c;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          hm_prev[i] = hm_cur[i];
-          hm_cur[i] = hm_n[i];
-          lr_cur[i] = lr_n[i];
-          v_cur[i] = v_n[i];
-        }
+      for (int i = 0; i < 8; ++i) {
+        hm_prev[i] = hm_cur[i];
+        hm_cur[i] = hm_n[i];
+        lr_cur[i] = lr_n[i];
+        v_cur[i] = v_n[i];
       }
     }
     __syncthreads();
@@ -721,19 +720,34 @@ __global__ void nms_gather_kernel(const float* __restrict__ in, int H, int W, in
                                   int* __restrict__ counts, float* __restrict__ peaks) {
   extern __shared__ int base[];  // tiles + 1 exclusive prefix
   const int pl = blockIdx.x;
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int t = 0; t < tiles; ++t) {
-      base[t] = acc;
-      acc += tile_counts[static_cast<size_t>(pl) * tiles + t];
+  if (threadIdx.x < 32) {
+    // warp 0: lane l loads and sums a contiguous run of the tile counts
+    // (all loads in flight at once), then one warp scan
+    const int lane = threadIdx.x, per = (tiles + 31) / 32, beg = lane * per;
+    const int* tc = tile_counts + static_cast<size_t>(pl) * tiles;
+    int run = 0;
+    for (int t = beg; t < beg + per && t < tiles; ++t) run += tc[t];
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int q = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += q;
     }
-    base[tiles] = acc;
-    counts[pl] = acc < max_peaks ? acc : max_peaks;
+    int acc = incl - run;
+    for (int t = beg; t < beg + per && t < tiles; ++t) {
+      base[t] = acc;
+      acc += tc[t];
+    }
+    if (lane == 31) {
+      base[tiles] = incl;
+      if (blockIdx.y == 0) counts[pl] = incl < max_peaks ? incl : max_peaks;
+    }
   }
   __syncthreads();
   const int n = base[tiles] < max_peaks ? base[tiles] : max_peaks;
   const float* p = in + static_cast<size_t>(pl) * H * W;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  // blockIdx.y: this block's slice of the plane's first max_peaks peaks
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < n; i += gridDim.y * blockDim.x) {
     int lo = 0, hi = tiles;  // the tile holding peak i: base[lo] <= i < base[lo + 1]
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -932,9 +946,9 @@ void launch_nms(const float* d_in, int planes, int H, int W, float threshold, in
       const int total = tiles_s * planes;
       nms8_tiles_kernel<kNms8Rows><<<total, threads8, tile8_bytes, stream>>>(d_in, H, W, threshold, max_peaks, tiles_s,
                                                                            tile_counts, tile_peaks);
-      nms_gather_kernel<<<planes, 128, (tiles_s + 1) * sizeof(int), stream>>>(d_in, H, W, tiles_s, max_peaks,
-                                                                             max_peaks, tile_counts, tile_peaks,
-                                                                             d_counts, d_peaks);
+      // a block per (plane, 64 peaks): the refinement's 9 loads per peak in flight on many SMs
+      nms_gather_kernel<<<dim3(planes, (max_peaks + 63) / 64), 64, (tiles_s + 1) * sizeof(int), stream>>>(
+          d_in, H, W, tiles_s, max_peaks, max_peaks, tile_counts, tile_peaks, d_counts, d_peaks);
       check_cuda(cudaGetLastError(), "nms launch");
       return;
     }
@@ -947,8 +961,8 @@ void launch_nms(const float* d_in, int planes, int H, int W, float threshold, in
           reinterpret_cast<uintptr_t>(tile_counts + static_cast<size_t>(planes) * tiles1 + 15) & ~uintptr_t(15));
       nms4_tiles_kernel<<<dim3(tiles1, planes), threads, tile1_bytes, stream>>>(d_in, H, W, threshold, max_peaks,
                                                                                  tile_counts, tile_peaks);
-      nms_gather_kernel<<<planes, 128, (tiles1 + 1) * sizeof(int), stream>>>(d_in, H, W, tiles1, max_peaks, max_peaks,
-                                                                            tile_counts, tile_peaks, d_counts, d_peaks);
+      nms_gather_kernel<<<dim3(planes, (max_peaks + 63) / 64), 64, (tiles1 + 1) * sizeof(int), stream>>>(
+          d_in, H, W, tiles1, max_peaks, max_peaks, tile_counts, tile_peaks, d_counts, d_peaks);
       check_cuda(cudaGetLastError(), "nms launch");
       return;
     }
