@@ -69,35 +69,82 @@ __device__ __forceinline__ float src_coord_pow2(int o, float inv_scale, int n, i
   return __fsub_rn(f, static_cast<float>(a));
 }
 
-// one thread per 8 consecutive outputs of a row (two float4 stores). Their
-// source columns span at most 3 consecutive inputs per source row, loaded
-// once and selected per output.
-// x8 interior groups (1 <= g < w - 1): outputs 8g+j sit at f = g - 1 + (j + 4.5) / 8
-// (j < 4: between source columns g-1, g; j >= 4: between g, g+1). Every step
-// of src_coord is exact in fp32 there, so lx is the constant (j + 4.5) / 8 mod 1
-// and the result equals the general kernel's bit for bit.
-__global__ void upsample8_interior_kernel(const float* __restrict__ in, int h, int w, float* __restrict__ out) {
+// x8 upsample. Interior 8-output groups (1 <= g < w - 1): outputs 8g+j sit
+// at f = g - 1 + (j + 4.5) / 8 (j < 4: between source columns g-1, g; j >= 4:
+// between g, g+1). Every step of src_coord is exact in fp32 there, so lx is
+// the constant (j + 4.5) / 8 mod 1 and the result equals the general
+// kernel's bit for bit; the groups at the row ends (clamped columns) take the
+// general coordinates in the block's last warp.
+// A thread computes one float4 of outputs (4 columns: they all lie between
+// the same two source columns) for the 4 output rows of a quad (oy = 4q ..
+// 4q+3 share one pair of source rows: rows 8k..8k+3 sit between source rows
+// k-1 and k, rows 8k+4..8k+7 between k and k+1, clamped alike at the
+// borders). The 4 source values and 8 horizontal lerps are done once per
+// quad, the vertical lerp per row, with the same op sequence per output as
+// the general kernel (bit for bit). Consecutive lanes store consecutive 16-byte
+// chunks, so each store instruction writes whole sectors: the previous
+// 8-columns-per-thread layout wrote 32-byte strided halves and moved twice the
+// bytes through L1 -> L2 (the write path at 83%; with a separate row-end
+// kernel 106 + 10 us at C2, now 79 us).
+__global__ void upsample8_kernel(const float* __restrict__ in, int h, int w, float* __restrict__ out) {
   const int wo = w * 8, ho = h * 8;
-  const int g = 1 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= w - 1) return;
-  const int oy = blockIdx.y;
+  const int n_in = 2 * (w - 2);  // interior float4s per output row (threads 0 .. n_in-1)
+  const int oy0 = blockIdx.y * 4;
   const int pl = blockIdx.z;
   const float* src = in + static_cast<size_t>(pl) * h * w;
-  int y0, y1;
-  const float ly = src_coord_pow2(oy, 0.125f, h, y0, y1);
-  const float* r0 = src + static_cast<size_t>(y0) * w + (g - 1);
-  const float* r1 = src + static_cast<size_t>(y1) * w + (g - 1);
-  const float a0 = __ldg(r0), a1 = __ldg(r0 + 1), a2 = __ldg(r0 + 2);
-  const float b0 = __ldg(r1), b1 = __ldg(r1 + 1), b2 = __ldg(r1 + 2);
+  const int tid = threadIdx.x;
+  if (tid >= blockDim.x - 32) {
+    // the block's last warp: the row ends (the 8-output groups 0 and w-1,
+    // clamped source columns) of its 4 rows on the general per-column
+    // coordinates, one float4 of one row per lane, so no interior warp waits
+    const int l = tid - (blockDim.x - 32);
+    if (l >= 16) return;
+    const int oy = oy0 + (l >> 2), k = l & 3;
+    const int f = k < 2 ? k : 2 * w - 4 + k;
+    int y0, y1;
+    const float ly = src_coord_pow2(oy, 0.125f, h, y0, y1);
+    const float* r0 = src + static_cast<size_t>(y0) * w;
+    const float* r1 = src + static_cast<size_t>(y1) * w;
+    float r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int x0, x1;
+      const float lx = src_coord_pow2(4 * f + j, 0.125f, w, x0, x1);
+      r[j] = lerp2(lerp2(__ldg(r0 + x0), __ldg(r0 + x1), lx), lerp2(__ldg(r1 + x0), __ldg(r1 + x1), lx), ly);
+    }
+    reinterpret_cast<float4*>(out + (static_cast<size_t>(pl) * ho + oy) * wo)[f] = make_float4(r[0], r[1], r[2], r[3]);
+    return;
+  }
+  if (tid >= n_in) return;
+  const int f = 2 + tid;  // float4 index of the output row
+  const int g = f >> 1, half = f & 1;
   constexpr float kLx[8] = {0.5625f, 0.6875f, 0.8125f, 0.9375f, 0.0625f, 0.1875f, 0.3125f, 0.4375f};
-  float r[8];
+  const int c = g - 1 + half;  // left source column of these 4 outputs
+  int py0 = -1, py1 = -1;
+  float top[4], bot[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) r[j] = lerp2(lerp2(a0, a1, kLx[j]), lerp2(b0, b1, kLx[j]), ly);
+  for (int dy = 0; dy < 4; ++dy) {
+    const int oy = oy0 + dy;
+    int y0, y1;
+    const float ly = src_coord_pow2(oy, 0.125f, h, y0, y1);
+    if (y0 != py0 || y1 != py1) {  // once per quad (the rows share their source rows)
+      const float* r0 = src + static_cast<size_t>(y0) * w + c;
+      const float* r1 = src + static_cast<size_t>(y1) * w + c;
+      const float a0 = __ldg(r0), a1 = __ldg(r0 + 1);
+      const float b0 = __ldg(r1), b1 = __ldg(r1 + 1);
 #pragma unroll
-  for (int j = 4; j < 8; ++j) r[j] = lerp2(lerp2(a1, a2, kLx[j]), lerp2(b1, b2, kLx[j]), ly);
-  float4* o4 = reinterpret_cast<float4*>(out + (static_cast<size_t>(pl) * ho + oy) * wo) + 2 * g;
-  o4[0] = make_float4(r[0], r[1], r[2], r[3]);
-  o4[1] = make_float4(r[4], r[5], r[6], r[7]);
+      for (int j = 0; j < 4; ++j) {
+        const float lx = kLx[half * 4 + j];
+        top[j] = lerp2(a0, a1, lx);
+        bot[j] = lerp2(b0, b1, lx);
+      }
+      py0 = y0;
+      py1 = y1;
+    }
+    reinterpret_cast<float4*>(out + (static_cast<size_t>(pl) * ho + oy) * wo)[f] =
+        make_float4(lerp2(top[0], bot[0], ly), lerp2(top[1], bot[1], ly), lerp2(top[2], bot[2], ly),
+                    lerp2(top[3], bot[3], ly));
+  }
 }
 
 // one 8-output group: the general path of the pow2 kernels
@@ -138,17 +185,6 @@ __global__ void upsample_pow2_kernel(const float* __restrict__ in, int planes, i
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= w * scale / 8) return;
   upsample_group(in, h, w, scale, inv_scale, out, blockIdx.z, blockIdx.y, g);
-}
-
-// the two border groups (0 and w - 1) of every x8 output row, one per thread
-__global__ void upsample8_border_kernel(const float* __restrict__ in, int planes, int h, int w,
-                                        float* __restrict__ out) {
-  const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned ho = static_cast<unsigned>(h) * 8;
-  if (idx >= 2u * ho * static_cast<unsigned>(planes)) return;
-  const unsigned rest = idx >> 1;
-  const int oy = static_cast<int>(rest % ho), pl = static_cast<int>(rest / ho);
-  upsample_group(in, h, w, 8, 0.125f, out, pl, oy, (idx & 1u) ? w - 1 : 0);
 }
 
 // Peak test for the pixel this lane owns in row y; neighbours come from the
@@ -868,12 +904,12 @@ void launch_upsample(const float* d_in, int planes, int h, int w, int scale, flo
   if (pow2 && h * scale <= 65535 && planes <= 65535) {  // 8 outputs per thread: <= 3 source columns each side
     const int wg = w * scale / 8;
     const float inv = 1.0f / static_cast<float>(scale);
-    if (scale == 8 && w >= 3) {  // interior groups on the fast kernel, the two border groups apart
-      const int n = w - 2;
-      const int tpb = n >= 128 ? 128 : (n + 31) / 32 * 32;
-      upsample8_interior_kernel<<<dim3((n + tpb - 1) / tpb, h * 8, planes), tpb, 0, stream>>>(d_in, h, w, d_out);
-      const unsigned nb = 2u * static_cast<unsigned>(h) * 8u * static_cast<unsigned>(planes);
-      upsample8_border_kernel<<<(nb + 255) / 256, 256, 0, stream>>>(d_in, planes, h, w, d_out);
+    if (scale == 8 && w >= 3 && w <= 498) {
+      // a block per 4 output rows: a float4 x 4 rows per thread for the
+      // interior, then one warp for the row ends (general coordinates)
+      const int n = 2 * (w - 2);
+      const int tpb = (n + 31) / 32 * 32 + 32;
+      upsample8_kernel<<<dim3(1, h * 2, planes), tpb, 0, stream>>>(d_in, h, w, d_out);
     } else {
       const int tpb = wg >= 128 ? 128 : (wg + 31) / 32 * 32;
       upsample_pow2_kernel<<<dim3((wg + tpb - 1) / tpb, h * scale, planes), tpb, 0, stream>>>(
