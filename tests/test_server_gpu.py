@@ -84,6 +84,26 @@ def test_posenet_over_the_wire_equals_c_abi(server, tmp_path):
     be.close()
 
 
+def test_tf32_posenet_over_the_wire_equals_c_abi(server, tmp_path):
+    """An `input tf32` net uploaded by the unmodified reference client (the
+    spec rides in the model structure) replies what the C-ABI computes."""
+    from paper_2103_04930_b200 import B200Backend, Dims, Frame, make_model, netspec
+    s32 = netspec.spec(input_dtype="tf32")
+    spec = tmp_path / "spec32.txt"
+    spec.write_bytes(s32)
+    h, w, b = 64, 96, 2
+    rc, out = ref_client(server.endpoint, "--structure", str(spec), "--divisor", repr(netspec.COCO_DIVISOR),
+                         "--width", str(w), "--height", str(h), "--batch", str(b), "--frames", "1",
+                         "--dump", str(tmp_path / "heat32.bin"), "--name", "openpose_coco_tf32")
+    assert rc == 0 and out["ok"] and out["byte_account_bad"] == 0
+    wire_out = np.fromfile(tmp_path / "heat32.bin", dtype=np.float32)
+    be = B200Backend(0)
+    hd = be.register_model(make_model("openpose_coco_tf32", s32, b"", netspec.COCO_DIVISOR))
+    local = be.forward(hd, Frame(Dims(1, 3 * b, h, w), O.batched_frame(w, h, b, seed=7))).data
+    assert wire_out.tobytes() == local.tobytes()
+    be.close()
+
+
 def test_c1_reference_client_posenet_368(server, tmp_path):
     """BASELINE configs[0] (C1): the unmodified reference client drives the COCO
     pose net through our server, one 368x368 frame, batch 1. The wire reply is
