@@ -61,28 +61,31 @@ constexpr int kTileCols = 126;  // output columns per tile (even: whole pooled c
 constexpr int kPatchCols = 132;
 constexpr int kPatchRows = 6;
 constexpr int kPatchBytes = 3 * kPatchRows * kPatchCols * 4;  // 9504
-// conv1_2 weight ring: a stage is one column tap s and one K chunk q,
-// [W(2,s); W(1,s); W(0,s)] x [64 cout][kWK K] bf16, swizzle span 2 kWK bytes.
-// K halves (SW64, 12 KB, 3 stages): 152 us at C2. K16 chunks (SW32, 6 KB, 7
-// stages, to hide more L2 latency) measured slower: 159 us.
-constexpr int kWK = 32;                  // K per stage
-constexpr int kWBlk = 64 * kWK * 2;      // one W(r,s) block, bytes
-constexpr int kW12Stage = 3 * kWBlk;
-constexpr int kW12Stages = 3;
+// conv1_2's weights stay resident for the CTA's lifetime (72 KB): per column
+// tap s, [W(2,s); W(1,s); W(0,s)] x [64 cout][64 K] bf16 SW128, 8 KB each. A
+// ring of 3 x 12 KB stages reloaded 72 KB per tile from L2 and left the MMA
+// warp waiting on weights (16% of its samples); the 6-slot window ring below
+// is what frees the room.
+constexpr int kWBlk = 64 * 64 * 2;       // one W(r,s) block, bytes
+constexpr int kW12Tap = 3 * kWBlk;       // the three filter rows of one column tap
+// conv1_1 output windows: a ring of 6 slots instead of 2 x 4 buffers. conv1_2
+// reads a tile's windows in order (window-outer MMAs), so a tile's first two
+// slots free early and the next tile's conv1_1 epilogue reuses them.
+constexpr int kWinSlots = 6;
 constexpr int kAcc2Col = 256;  // acc2[2 stages] at 256..383, 384..511 (2 rows x 64 each)
 
 struct Smem12 {
-  static constexpr int win = 0;                          // 2 buffers x 4 windows x [128][64] bf16 SW128
-  static constexpr int imc = win + 2 * 4 * 16384;        // 4 windows x [128][32] bf16 SW64 (im2col)
-  static constexpr int w12 = imc + 4 * 8192;             // kW12Stages x kW12Stage
-  static constexpr int w11 = w12 + kW12Stages * kW12Stage;  // [64 cout][32 K] SW64 (K 29 used)
+  static constexpr int win = 0;                          // kWinSlots x [128][64] bf16 SW128
+  static constexpr int imc = win + kWinSlots * 16384;    // 4 windows x [128][32] bf16 SW64 (im2col)
+  static constexpr int w12 = imc + 4 * 8192;             // 3 x kW12Tap, resident
+  static constexpr int w11 = w12 + 3 * kW12Tap;          // [64 cout][32 K] SW64 (K 29 used)
   static constexpr int patch = w11 + 4096;               // [3][6][132] fp32 (one buffer: the
                                                          // next patch has a whole tile to land)
   static constexpr int stg = patch + 10240;              // 4 warps x [16 px][64 ch] (pooled box)
   static constexpr int bias = stg + 4 * 2048;            // conv1_2 bias (64; room for 128)
   static constexpr int bars = bias + 2 * 64 * 4;
   static constexpr int total = bars + 256;
-  static_assert((2 + 2 + 1 + 2 * kW12Stages + 1 + 1 + 2 + 2 + 2 + 2) * 8 + 4 <= 256, "barrier block");
+  static_assert((2 + 2 + 1 + 1 + 1 + 1 + 2 + kWinSlots + 2 + 2) * 8 + 4 <= 256, "barrier block");
   static_assert(total + 1024 <= 232448, "smem budget");
 };
 
@@ -128,13 +131,12 @@ __global__ void __launch_bounds__(C12Cfg<SUBS>::kThreads, 1)
   uint64_t* patch_full = bars;             // [2] (only [0] used)
   uint64_t* patch_empty = patch_full + 2;  // [2] 128 arrivals
   uint64_t* w11_full = patch_empty + 2;
-  uint64_t* w12_full = w11_full + 1;       // [kW12Stages]
-  uint64_t* w12_empty = w12_full + kW12Stages;
-  uint64_t* imc_full = w12_empty + kW12Stages;  // 128 arrivals: im2col written
+  uint64_t* w12_full = w11_full + 1;            // the resident conv1_2 weights landed
+  uint64_t* imc_full = w12_full + 1;            // 128 arrivals: im2col written
   uint64_t* a1_full = imc_full + 1;             // conv1_1 MMAs done (acc1 ready, im2col free)
-  uint64_t* win_full = a1_full + 1;             // [2] 128 arrivals: conv1_1 output written, acc1 drained
-  uint64_t* win_empty = win_full + 2;           // [2] conv1_2 MMAs done with the windows
-  uint64_t* acc2_full = win_empty + 2;          // [2]
+  uint64_t* win_full = a1_full + 1;             // [2] by tile parity: its 4 windows written, acc1 drained
+  uint64_t* slot_empty = win_full + 2;          // [kWinSlots] conv1_2 MMAs done with a window slot
+  uint64_t* acc2_full = slot_empty + kWinSlots; // [2]
   uint64_t* acc2_empty = acc2_full + 2;         // [2] 128 arrivals
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc2_empty + 2);
 
@@ -144,17 +146,14 @@ __global__ void __launch_bounds__(C12Cfg<SUBS>::kThreads, 1)
       mbar_init(&patch_full[i], 1);
       mbar_init(&patch_empty[i], kEpi);
       mbar_init(&win_full[i], kEpi);
-      mbar_init(&win_empty[i], 1);
       mbar_init(&acc2_full[i], 1);
       mbar_init(&acc2_empty[i], kEpi);
     }
+    for (int i = 0; i < kWinSlots; ++i) mbar_init(&slot_empty[i], 1);
     mbar_init(w11_full, 1);
+    mbar_init(w12_full, 1);
     mbar_init(imc_full, kEpi);
     mbar_init(a1_full, 1);
-    for (int i = 0; i < kW12Stages; ++i) {
-      mbar_init(&w12_full[i], 1);
-      mbar_init(&w12_empty[i], 1);
-    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -166,22 +165,12 @@ __global__ void __launch_bounds__(C12Cfg<SUBS>::kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (elect_one()) {
-      const uint64_t keep = policy_evict_last();
       mbar_arrive_expect_tx(w11_full, 4096);
       tma_load_2d(w11, &maps.wgt[1], w11_full, 0, 0);
-      int ws = 0;
-      uint32_t wph = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-        for (int s = 0; s < 3; ++s)
-          for (int q = 0; q < 64 / kWK; ++q) {
-            mbar_wait(&w12_empty[ws], wph ^ 1);
-            mbar_arrive_expect_tx(&w12_full[ws], kW12Stage);
-            for (int r = 2; r >= 0; --r)  // K index (r*3 + s)*64 + cin
-              tma_load_2d_hint(w12 + ws * kW12Stage + (2 - r) * kWBlk, &maps.wgt[0], &w12_full[ws],
-                               (r * 3 + s) * 64 + kWK * q, 0, keep);
-            if (++ws == kW12Stages) { ws = 0; wph ^= 1; }
-          }
-      }
+      mbar_arrive_expect_tx(w12_full, 3 * kW12Tap);
+      for (int s = 0; s < 3; ++s)
+        for (int r = 2; r >= 0; --r)  // K index (r*3 + s)*64 + cin
+          tma_load_2d(w12 + s * kW12Tap + (2 - r) * kWBlk, &maps.wgt[0], w12_full, (r * 3 + s) * 64, 0);
     }
   } else if (warp == kPatchWarp) {
     // ------------------------------------------------------------ frame patches
@@ -219,42 +208,53 @@ __global__ void __launch_bounds__(C12Cfg<SUBS>::kThreads, 1)
         }
         mma_commit(a1_full);
       };
-      int ws = 0;
-      uint32_t wph = 0;
       mbar_wait(w11_full, 0);
       if (int(blockIdx.x) < p.total_tiles) conv11(0);
+      mbar_wait(w12_full, 0);
       int it = 0;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
-        const int b = it & 1;  // window buffer, also the acc2 stage
+        const int b = it & 1;  // acc2 stage, window-written barrier
         const uint32_t bph = (it >> 1) & 1;
-        const uint32_t wb = win_base + b * 4 * 16384;
         mbar_wait(&win_full[b], bph);
         if (t + int(gridDim.x) < p.total_tiles) conv11((it + 1) & 1);
         mbar_wait(&acc2_empty[b], bph ^ 1);
         tc_fence_after();
-        // acc2: output row 0 at columns d0 .. d0+63, row 1 at d0+64 .. d0+127
+        // acc2: output row 0 at columns d0 .. d0+63, row 1 at d0+64 .. d0+127.
+        // Window w (shifted by s positions) feeds row 0 with W(w,s) and row 1
+        // with W(w-1,s); the middle two in one N = 128 MMA against the
+        // adjacent [W(w,s); W(w-1,s)] rows, the outer two N = 64. Windows 0
+        // and 1 first (interleaved per K step), then 2 and 3: the first pair's
+        // slots are released half-way through the tile.
         const uint32_t d0 = tmem + kAcc2Col + b * 128;
-        for (int s = 0; s < 3; ++s)
-          for (int q = 0; q < 64 / kWK; ++q) {
-            mbar_wait(&w12_full[ws], wph);
-            tc_fence_after();
-            // the stage holds W(2,s), W(1,s), W(0,s) kWBlk bytes apart; a
-            // 32-byte K step adds 2 to a descriptor
-            const uint64_t b2 = kWK == 32 ? desc_sw64(w12_base + ws * kW12Stage) : desc_sw32(w12_base + ws * kW12Stage);
-            const uint64_t b1 = b2 + (kWBlk >> 4), b0 = b2 + 2 * (kWBlk >> 4);
+#pragma unroll 1
+        for (int hp = 0; hp < 2; ++hp) {  // windows (0, 1), then (2, 3), interleaved per K step
+          const int slot_a = (4 * it + 2 * hp) % kWinSlots, slot_b = (4 * it + 2 * hp + 1) % kWinSlots;
+          const uint32_t wa = win_base + slot_a * 16384, wb2 = win_base + slot_b * 16384;
 #pragma unroll
-            for (int kk = 0; kk < kWK / 16; ++kk) {
-              const uint32_t accum = (s == 0 && q == 0 && kk == 0) ? 0u : 1u;
-              const uint32_t ko = 2 * (q * (kWK / 16) + kk), kb = 2 * kk;
-              mma_bf16_ss(d0 + 64, desc_sw128(wb + 3 * 16384 + s * 128) + ko, b2 + kb, idesc, accum);  // row 1 += win3 W(2,s)
-              mma_bf16_ss(d0, desc_sw128(wb + s * 128) + ko, b0 + kb, idesc, accum);  // row 0 += win0 W(0,s)
-              mma_bf16_ss(d0, desc_sw128(wb + 16384 + s * 128) + ko, b1 + kb, idesc2, 1u);  // rows 0|1 += win1 [W(1,s); W(0,s)]
-              mma_bf16_ss(d0, desc_sw128(wb + 2 * 16384 + s * 128) + ko, b2 + kb, idesc2, 1u);  // rows 0|1 += win2 [W(2,s); W(1,s)]
+          for (int s = 0; s < 3; ++s) {
+            // W(2,s) at +0, W(1,s) at +8 KB, W(0,s) at +16 KB (512 descriptor units each)
+            const uint64_t b2 = desc_sw128(w12_base + s * kW12Tap), b1 = b2 + 512, b0 = b2 + 1024;
+            const uint64_t a0 = desc_sw128(wa + s * 128), a1 = desc_sw128(wb2 + s * 128);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {  // a 32-byte K step adds 2 to a descriptor
+              const uint64_t kb = 2 * kk;
+              if (hp == 0) {
+                mma_bf16_ss(d0, a0 + kb, b0 + kb, idesc, (s == 0 && kk == 0) ? 0u : 1u);  // row 0 += win0 W(0,s)
+                if (s == 0 && kk == 0) {
+                  mma_bf16_ss(d0, a1, b1, idesc, 1u);       // row 0 += win1 W(1,0)
+                  mma_bf16_ss(d0 + 64, a1, b0, idesc, 0u);  // row 1 = win1 W(0,0): its first term
+                } else {
+                  mma_bf16_ss(d0, a1 + kb, b1 + kb, idesc2, 1u);  // rows 0|1 += win1 [W(1,s); W(0,s)]
+                }
+              } else {
+                mma_bf16_ss(d0, a0 + kb, b2 + kb, idesc2, 1u);       // rows 0|1 += win2 [W(2,s); W(1,s)]
+                mma_bf16_ss(d0 + 64, a1 + kb, b2 + kb, idesc, 1u);   // row 1 += win3 W(2,s)
+              }
             }
-            mma_commit(&w12_empty[ws]);
-            if (++ws == kW12Stages) { ws = 0; wph ^= 1; }
           }
-        mma_commit(&win_empty[b]);
+          mma_commit(&slot_empty[slot_a]);
+          mma_commit(&slot_empty[slot_b]);
+        }
         mma_commit(&acc2_full[b]);
       }
     }
@@ -324,19 +324,22 @@ __global__ void __launch_bounds__(C12Cfg<SUBS>::kThreads, 1)
       int n, y0, x0;
       tile_of(p, t, n, y0, x0);
       const int b = it & 1;
-      mbar_wait(&win_empty[b], ((it >> 1) & 1) ^ 1);  // conv1_2 two tiles back is done with the buffer
       const int C = x0 + px - 1;
-      uint8_t* wrow = win + b * 4 * 16384 + px * 128;
 #pragma unroll
       for (int jw = 0; jw < kWinPerSub; ++jw) {
         const int j = kWinPerSub * sub + jw;
+        // window j of this tile is use u of ring slot u % kWinSlots: wait
+        // until conv1_2 released the slot's previous use
+        const int u = 4 * it + j;
+        const int slot = u % kWinSlots;
+        mbar_wait(&slot_empty[slot], ((u / kWinSlots) & 1) ^ 1);
+        uint8_t* row = win + slot * 16384 + px * 128;
         const int R = y0 - 1 + j;
         const bool valid = R >= 0 && R < p.H && C >= 0 && C < p.W;
         uint32_t va[32], vb[32];
         tmem_ld32(tmem + lane_base + j * 64, va);
         tmem_ld32(tmem + lane_base + j * 64 + 32, vb);
         tmem_ld_wait();
-        uint8_t* row = wrow + j * 16384;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           uint32_t w[4];
@@ -447,7 +450,7 @@ void conv12_configure() {
 }
 
 int conv12_tile_cols() { return kTileCols; }
-int conv12_wgt_k() { return kWK; }
+int conv12_wgt_k() { return 64; }  // resident W(r,s) blocks: [64 cout][64 K] SW128
 
 void launch_conv12(const ConvMaps& maps, const ConvParams& p, int sm_count, cudaStream_t stream) {
   const int grid = p.total_tiles < sm_count ? p.total_tiles : sm_count;
