@@ -7,29 +7,32 @@
 //   producer  TMA of the fp32 frame patch [3 ch][rows y0-2..y0+3][132 cols from
 //             (x0-2) & ~3] (zero-filled outside the frame; a TMA inner
 //             coordinate must be 16-byte aligned — an unaligned one is an
-//             illegal instruction, tests/native/tma3d_probe.cu), conv1_1 weights once, conv1_2
-//             weights per (column tap s, K half) as [W(2,s); W(1,s); W(0,s)]
-//             (3 x 64 cout x 32 K, SW64; 72 KB per tile, from L2)
+//             illegal instruction, tests/native/tma3d_probe.cu); conv1_1's
+//             and conv1_2's weights once per CTA (conv1_2's 72 KB stay
+//             resident as [W(2,s); W(1,s); W(0,s)] per column tap s)
 //   epilogue  A: im2col of the 27 taps per window position (x - 0.5, 0 outside
 //                the frame) into a K = 32 SW64 im2col buffer; taps 27 and 28
 //                are 1.0, against conv1_1's bias split hi + lo into its
 //                weights there (engine.cu upload), so acc1 includes the bias
 //   MMA       conv1_1: 4 windows x 2 MMAs (M128 N64 K16) -> acc1[4] in TMEM
-//   epilogue  B: acc1 -> ReLU, 0 outside the image, bf16 -> overwrites
-//                the window (it is now conv1_2's A operand, SW128 K-major)
-//   MMA       conv1_2, per column tap s and K16 step: window w (shifted by s
-//             positions) feeds output row 0 with W(w,s) and output row 1 with
-//             W(w-1,s). The two middle windows do both in one N = 128 MMA
-//             against the adjacent [W(w,s); W(w-1,s)] rows (64 cycles, at the
-//             tensor rate), the outer two one N = 64 MMA each: 224 cycles per
-//             step instead of six N = 64 MMAs at the 48-cycle shared-memory
-//             operand floor (288; profiles/r01_tc_probe.json) -> acc2[stage]
+//   epilogue  B: acc1 -> ReLU, 0 outside the image, bf16 -> the tile's four
+//                window slots of a 6-slot ring (conv1_2's A operand, SW128
+//                K-major), each once conv1_2 released the slot's last use
+//   MMA       conv1_2: window w (shifted by s positions) feeds output row 0
+//             with W(w,s) and output row 1 with W(w-1,s). The two middle
+//             windows do both in one N = 128 MMA against the adjacent
+//             [W(w,s); W(w-1,s)] rows (64 cycles, at the tensor rate), the
+//             outer two one N = 64 MMA each: 224 cycles per K16 step instead of
+//             six N = 64 MMAs at the 48-cycle shared-memory operand floor (288;
+//             profiles/r01_tc_probe.json) -> acc2[stage]. Windows (0, 1) run
+//             first, interleaved per K step, then (2, 3), so the first pair's
+//             slots are released half-way through the tile
 //   epilogue  C: 2x2 max of the raw sums, bias, ReLU, bf16 -> pooled row
 //             y0/2, columns x0/2 .. x0/2+62 through a 4D TMA map (the 127th/
 //             128th positions read past their window and are never stored)
-// Windows are double-buffered and the MMA warp issues conv1_1(t+1) before
-// conv1_2(t), so the im2col of tile t+2, the conv1_1 epilogue of tile t+1 and
-// the pooled epilogue of tile t-1 all overlap conv1_2 of tile t. Same bf16
+// The MMA warp issues conv1_1(t+1) before conv1_2(t), so the im2col of tile
+// t+2, the conv1_1 epilogue of tile t+1 (into the slots conv1_2(t) released
+// first) and the pooled epilogue of tile t-1 all overlap conv1_2 of tile t. Same bf16
 // operands as the separate conv_first + pooled conv1_2 path; the fp32 sums run
 // in another tap order, so the two agree to bf16 rounding, not bit for bit.
 #include <cuda_bf16.h>
