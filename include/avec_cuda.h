@@ -124,6 +124,12 @@ int avec_upsample_device(avec_ctx* ctx, const float* d_in, int planes, int h, in
                          float* d_out, void* cuda_stream);
 int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, float threshold,
                     int max_peaks, int* d_counts, float* d_peaks, void* cuda_stream);
+/* Both on the same planes in one pass: d_out = the x`scale` upsample of d_in
+ * ([planes][h*scale][w*scale], as avec_upsample_device) and the peaks of d_out
+ * (as avec_nms_device), bit for bit; the upsampled planes are written once and
+ * not read back. scale must be 8 (the pose net's output stride). */
+int avec_upsample_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, int scale, float threshold,
+                             int max_peaks, float* d_out, int* d_counts, float* d_peaks, void* cuda_stream);
 
 /* Bottom-up person assembly (OpenPose parsing; SURVEY.md §8 f rank 4, not in
  * the reference). Peaks come from avec_nms_device on the part heatmaps

@@ -30,7 +30,7 @@ EXPORTS = [
     "avec_last_error", "avec_version", "avec_device_count", "avec_ctx_create",
     "avec_ctx_destroy", "avec_ctx_label", "avec_model_register", "avec_model_kind",
     "avec_output_elems", "avec_forward", "avec_forward_device", "avec_upsample_device",
-    "avec_nms_device", "avec_posenet_layer_io", "avec_posenet_layer_rows", "avec_posenet_layer_out_level", "avec_posenet_layer_fusion", "avec_posenet_layer_info",
+    "avec_nms_device", "avec_upsample_nms_device", "avec_posenet_layer_io", "avec_posenet_layer_rows", "avec_posenet_layer_out_level", "avec_posenet_layer_fusion", "avec_posenet_layer_info",
     "avec_posenet_num_layers", "avec_posenet_profile", "avec_posenet_synth_weights", "avec_host_alloc", "avec_host_free",
     "avec_paf_candidates_device", "avec_assemble_people", "avec_coco_limbs",
     "avec_stream_create", "avec_stream_destroy", "avec_stream_prepare", "avec_stream_begin", "avec_stream_feed", "avec_stream_finish",
@@ -71,6 +71,7 @@ def load() -> ctypes.CDLL:
         "avec_forward_device": (i, [vp, u64, u32, u32, u32, u32, vp, vp, vp]),
         "avec_upsample_device": (i, [vp, vp, i, i, i, i, vp, vp]),
         "avec_nms_device": (i, [vp, vp, i, i, i, c.c_float, i, vp, vp, vp]),
+        "avec_upsample_nms_device": (i, [vp, vp, i, i, i, i, c.c_float, i, vp, vp, vp, vp]),
         "avec_posenet_layer_io": (i, [vp, u64, u32, u32, u32, u32, vp, i, vp, u64, vp, u64]),
         "avec_posenet_layer_rows": (i, [vp, u64, u32, u32, u32, u32, vp, i, i, vp, vp, i, vp, vp]),
         "avec_posenet_layer_out_level": (i, [vp, u64, u32, u32, u32, u32, i, c.POINTER(i)]),

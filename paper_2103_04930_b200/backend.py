@@ -276,6 +276,13 @@ class B200Backend:
                                                       lp.ctypes.data, lf.ctypes.data, lp.shape[0], threshold, d_cand,
                                                       ctypes.c_void_p(stream) if stream else None))
 
+    def upsample_nms_device(self, d_in: int, planes: int, h: int, w: int, scale: int, threshold: float,
+                            max_peaks: int, d_out: int, d_counts: int, d_peaks: int, stream: int = 0) -> None:
+        """upsample_device + nms_device of its output in one pass (avec_upsample_nms_device)."""
+        _lib.check(self._L.avec_upsample_nms_device(self._ctx, d_in, planes, h, w, scale, threshold, max_peaks,
+                                                    d_out, d_counts, d_peaks,
+                                                    ctypes.c_void_p(stream) if stream else None))
+
     def nms_device(self, d_in: int, planes: int, h: int, w: int, threshold: float, max_peaks: int,
                    d_counts: int, d_peaks: int, stream: int = 0) -> None:
         _lib.check(self._L.avec_nms_device(self._ctx, d_in, planes, h, w, threshold, max_peaks,

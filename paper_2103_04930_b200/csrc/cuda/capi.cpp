@@ -235,6 +235,26 @@ int avec_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, 
   });
 }
 
+int avec_upsample_nms_device(avec_ctx* ctx, const float* d_in, int planes, int h, int w, int scale, float threshold,
+                             int max_peaks, float* d_out, int* d_counts, float* d_peaks, void* cuda_stream) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(d_in, "d_in");
+    need(d_out, "d_out");
+    need(d_counts, "d_counts");
+    need(d_peaks, "d_peaks");
+    if (planes < 1 || h < 1 || w < 1 || max_peaks < 1) avec::fail(AVEC_ERR_INVALID_ARGUMENT, "bad upsample+nms shape");
+    if (scale != 8) avec::fail(AVEC_ERR_UNSUPPORTED, "the fused upsample+nms is x8 (the pose net's stride)");
+    avec::check_cuda(cudaSetDevice(ctx->device), "cudaSetDevice");
+    std::lock_guard<std::mutex> lk(ctx->post_m);
+    ctx->scratch.ensure(avec::nms_scratch_bytes(planes, 8 * h, 8 * w, max_peaks), ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    avec::launch_upsample_nms(d_in, planes, h, w, threshold, max_peaks, d_out, d_counts, d_peaks, ctx->scratch.p,
+                              ctx->scratch.bytes, st);
+    avec::check_cuda(cudaStreamSynchronize(st), "upsample+nms sync");  // scratch is shared per context
+  });
+}
+
 int avec_paf_candidates_device(avec_ctx* ctx, const float* d_paf, int H, int W, const int* d_counts,
                                const float* d_peaks, int max_peaks, const int* limb_parts, const int* limb_paf,
                                int n_limbs, float paf_threshold, float* d_cand, void* cuda_stream) {

@@ -65,4 +65,11 @@ void launch_nms(const float* d_in, int planes, int H, int W, float threshold, in
                 cudaStream_t stream);
 size_t nms_scratch_bytes(int planes, int H, int W, int max_peaks);
 
+// x8 upsample of [planes][h][w] into d_out [planes][8h][8w] and the NMS of
+// the result (launch_upsample + launch_nms, same outputs bit for bit), fused
+// so the upsampled planes are written once and not read back; scratch as
+// nms_scratch_bytes(planes, 8h, 8w, max_peaks)
+void launch_upsample_nms(const float* d_in, int planes, int h, int w, float threshold, int max_peaks, float* d_out,
+                         int* d_counts, float* d_peaks, void* d_scratch, size_t scratch_bytes, cudaStream_t stream);
+
 }  // namespace avec

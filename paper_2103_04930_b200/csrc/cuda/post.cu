@@ -810,6 +810,211 @@ __global__ void nms_gather_kernel(const float* __restrict__ in, int H, int W, in
   }
 }
 
+// Fused x8 upsample + NMS pass 1 (avec_upsample_nms_device): the heatmap
+// planes NMS reads are the ones upsample just wrote, so the pair re-read them
+// from HBM (C2: 139 MB written, then 139 MB read back). Here a block owns one
+// source-row period of a plane, output rows 8k .. 8k+7 (all of which lie
+// between source rows k-1, k, k+1), and thread g owns the 8-output group of
+// source column g. It computes output rows 8k-1 .. 8k+8 in registers with the
+// op sequence of upsample8_kernel (bit for bit: interior groups at the
+// constant lx of kLx, the two row-end groups at the clamped coordinates the
+// general src_coord_pow2 yields for them, written out below), stores rows
+// 8k .. 8k+7, and runs nms8_tiles_kernel's comparisons on the values as they
+// are produced: the plane is written once and never read back (only the few
+// peak values are, from L2). Same per-tile raster lists for nms_gather_kernel
+// (tiles = h per plane). Instruction-bound rather than HBM-bound (~11 ops per
+// output pixel: vertical lerp, 3x3 maxima, test); staging the stores through
+// shared memory for whole-sector store instructions measured slower (56-58
+// vs 52-54 us on C2's 144 planes).
+// Row-end groups, from src_coord_pow2(8g + j, 1/8, w): g = 0, j < 4 clamps to
+// f = 0 (columns 0, 1 at lx = 0), j >= 4 sits at 0 + (j - 3.5)/8; g = w - 1,
+// j < 4 sits between w - 2 and w - 1 at kLx[j], j >= 4 at column w - 1 with
+// x1 clamped to w - 1. So every group is "left half between columns (L0, L1)
+// at lxL[j], right half between (R0, R1) at kLx[4 + j]", with (L0, L1, R0, R1)
+// = (g-1, g, g, g+1) inside, (0, 1, 0, 1) at g = 0, (w-2, w-1, w-1, w-1) at w-1.
+__global__ void __launch_bounds__(256, 3) ups8_nms_kernel(const float* __restrict__ in, int h, int w, float threshold,
+                                                       int cap, float* __restrict__ out, int* __restrict__ tile_counts,
+                                                       NmsPeak* __restrict__ tile_peaks) {
+  constexpr int R = 8;
+  __shared__ int wbase[R * 8];                  // per (row, warp) counts, then offsets, raster order r * nw + warp
+  __shared__ uint8_t pmask[R][256];
+  constexpr float kLx[8] = {0.5625f, 0.6875f, 0.8125f, 0.9375f, 0.0625f, 0.1875f, 0.3125f, 0.4375f};
+  const float NEG = -__int_as_float(0x7f800000);
+  const int H = 8 * h, W = 8 * w;
+  const int g = threadIdx.x, c0 = 8 * g;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool col_ok = g < w;
+  const int t = blockIdx.x;  // = plane * h + k
+  const int pl = t / h, k = t - pl * h, y0 = 8 * k;
+  const float* src = in + static_cast<size_t>(pl) * h * w;
+  float* dst = out + static_cast<size_t>(pl) * H * W;
+  const int gc = col_ok ? g : w - 1;  // idle lanes load in-range columns (their values are never used)
+  const int L0 = gc > 0 ? gc - 1 : 0, L1 = gc > 0 ? gc : 1, R0 = gc, R1 = gc + 1 < w ? gc + 1 : w - 1;
+  // Source rows: output rows 8k-1 .. 8k+3 lie between the pair src_coord_pow2
+  // gives row 8k (k-1, k; (0, 1) at k = 0, where row -1 is outside), rows
+  // 8k+4 .. 8k+8 between the pair of row 8k+4 (k, k+1; clamped at k = h-1,
+  // where row 8k+8 is outside). Both pairs' source values load up front.
+  int ya0, ya1, yb0, yb1;
+  src_coord_pow2(y0, 0.125f, h, ya0, ya1);
+  src_coord_pow2(y0 + 4, 0.125f, h, yb0, yb1);
+  float A[8], B[8];  // (L0, L1, R0, R1) of the pair's top row, then of its bottom row
+  {
+    const float* a0 = src + static_cast<size_t>(ya0) * w;
+    const float* a1 = src + static_cast<size_t>(ya1) * w;
+    const float* b0 = src + static_cast<size_t>(yb0) * w;
+    const float* b1 = src + static_cast<size_t>(yb1) * w;
+    A[0] = __ldg(a0 + L0), A[1] = __ldg(a0 + L1), A[2] = __ldg(a0 + R0), A[3] = __ldg(a0 + R1);
+    A[4] = __ldg(a1 + L0), A[5] = __ldg(a1 + L1), A[6] = __ldg(a1 + R0), A[7] = __ldg(a1 + R1);
+    B[0] = __ldg(b0 + L0), B[1] = __ldg(b0 + L1), B[2] = __ldg(b0 + R0), B[3] = __ldg(b0 + R1);
+    B[4] = __ldg(b1 + L0), B[5] = __ldg(b1 + L1), B[6] = __ldg(b1 + R0), B[7] = __ldg(b1 + R1);
+  }
+  float lxL[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) lxL[j] = gc > 0 ? kLx[j] : 0.0f;
+  auto mx = [](float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+  };
+  // horizontal lerps of the current pair (tp: its top row, bt: its bottom row)
+  float tp[8], bt[8], tEl, bEl, tEr, bEr;
+  auto hsetup = [&](const float (&S)[8]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      tp[j] = lerp2(S[0], S[1], lxL[j]);
+      bt[j] = lerp2(S[4], S[5], lxL[j]);
+      tp[4 + j] = lerp2(S[2], S[3], kLx[4 + j]);
+      bt[4 + j] = lerp2(S[6], S[7], kLx[4 + j]);
+    }
+    // column c0 - 1 = group g - 1's last output (between g - 1 and g at kLx[7]);
+    // column c0 + 8 = group g + 1's first (between g and g + 1 at kLx[0])
+    tEl = lerp2(S[0], S[1], kLx[7]);
+    bEl = lerp2(S[4], S[5], kLx[7]);
+    tEr = lerp2(S[2], S[3], kLx[0]);
+    bEr = lerp2(S[6], S[7], kLx[0]);
+  };
+  struct Row {
+    float v[8];
+    float el, er;  // columns c0 - 1 and c0 + 8 (-inf outside the plane)
+  };
+  // output row y0 + rr (rr = -1 .. 8): its values, and its store for rr = 0 .. 7
+  auto make = [&](int rr) {
+    Row r;
+    const int oy = y0 + rr;
+    if (oy < 0 || oy >= H) {  // block-uniform: the halo row above the first / below the last tile
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r.v[j] = NEG;
+      r.el = r.er = NEG;
+      return r;
+    }
+    int ys0, ys1;
+    const float ly = src_coord_pow2(oy, 0.125f, h, ys0, ys1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r.v[j] = lerp2(tp[j], bt[j], ly);
+    r.el = col_ok && g > 0 ? lerp2(tEl, bEl, ly) : NEG;
+    r.er = g + 1 < w ? lerp2(tEr, bEr, ly) : NEG;
+    if (rr >= 0 && rr < R && col_ok) {  // two float4 per lane (a warp's stores are one contiguous 1 KB span)
+      float4* d = reinterpret_cast<float4*>(dst + static_cast<size_t>(oy) * W + c0);
+      d[0] = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+      d[1] = make_float4(r.v[4], r.v[5], r.v[6], r.v[7]);
+    }
+    return r;
+  };
+  // hm: max of the 3 columns around each of mine; lr: max of left and right.
+  // Lanes past the plane (g >= w) hold values of column w - 1 that no one
+  // may see: the plane's last group takes its right neighbour from r.er.
+  auto horiz = [&](const Row& r, float (&v)[8], float (&lr)[8], float (&hm)[8]) {
+    float left = __shfl_up_sync(0xffffffffu, r.v[7], 1);
+    float right = __shfl_down_sync(0xffffffffu, r.v[0], 1);
+    if (lane == 0) left = r.el;
+    if (lane == 31 || g + 1 >= w) right = r.er;
+    const float e[10] = {left, r.v[0], r.v[1], r.v[2], r.v[3], r.v[4], r.v[5], r.v[6], r.v[7], right};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i] = e[i + 1];
+      lr[i] = mx(e[i], e[i + 2]);
+      hm[i] = mx(lr[i], e[i + 1]);
+    }
+  };
+  float v_cur[8], lr_cur[8], hm_cur[8], hm_prev[8];
+  hsetup(A);
+  {
+    float vd[8], lrd[8];
+    horiz(make(-1), vd, lrd, hm_prev);
+    horiz(make(0), v_cur, lr_cur, hm_cur);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r + 1 == 4) hsetup(B);  // rows 8k+4 .. 8k+8
+    float v_n[8], lr_n[8], hm_n[8];
+    horiz(make(r + 1), v_n, lr_n, hm_n);
+    unsigned m = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      // nms8_tiles_kernel's test: v > max.NaN(8 neighbours, threshold)
+      const float lim = mx(mx(mx(hm_prev[i], hm_n[i]), lr_cur[i]), threshold);
+      m |= v_cur[i] > lim ? (1u << i) : 0u;
+    }
+    if (!col_ok) m = 0;
+    pmask[r][threadIdx.x] = static_cast<uint8_t>(m);
+    const int c = __reduce_add_sync(0xffffffffu, __popc(m));
+    if (lane == 0) wbase[r * nw + wid] = c;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      hm_prev[i] = hm_cur[i];
+      hm_cur[i] = hm_n[i];
+      lr_cur[i] = lr_n[i];
+      v_cur[i] = v_n[i];
+    }
+  }
+  __syncthreads();  // also makes this block's stores of its rows visible to the peak writes below
+  if (wid == 0) {
+    const int n = R * nw;  // <= 64: lanes l and l + 32
+    const int c_a = lane < n ? wbase[lane] : 0, c_b = lane + 32 < n ? wbase[lane + 32] : 0;
+    int incl = c_a;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int q = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += q;
+    }
+    const int tot_a = __shfl_sync(0xffffffffu, incl, 31);
+    int incl_b = c_b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int q = __shfl_up_sync(0xffffffffu, incl_b, o);
+      if (lane >= o) incl_b += q;
+    }
+    if (lane < n) wbase[lane] = incl - c_a;
+    if (lane + 32 < n) wbase[lane + 32] = tot_a + incl_b - c_b;
+    if (lane == 31) tile_counts[t] = tot_a + incl_b;
+  }
+  __syncthreads();
+  NmsPeak* outp = tile_peaks + static_cast<size_t>(t) * cap;
+  for (int r = 0; r < R; ++r) {
+    if (wbase[r * nw] >= cap) break;  // the tile's list is full (uniform: offsets only grow)
+    const unsigned m = pmask[r][threadIdx.x];
+    if (!__any_sync(0xffffffffu, m)) continue;
+    const int mine = __popc(m);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int q = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += q;
+    }
+    int idx = wbase[r * nw + wid] + incl - mine;
+    const float* vrow = dst + static_cast<size_t>(y0 + r) * W + c0;  // written above by this block
+    float pv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pv[i] = (m >> i) & 1u ? vrow[i] : 0.0f;  // all loads in flight at once
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (!((m >> i) & 1u) || idx >= cap) continue;
+      outp[idx] = NmsPeak{c0 + i, y0 + r, pv[i]};
+      ++idx;
+    }
+  }
+}
+
 // pass 1: per (plane, row) peak counts
 __global__ void nms_count_kernel(const float* __restrict__ in, int H, int W, float threshold,
                                  int* __restrict__ row_counts) {
@@ -1028,6 +1233,31 @@ void launch_nms(const float* d_in, int planes, int H, int W, float threshold, in
   nms_write_kernel<<<grid, 256, 0, stream>>>(d_in, H, W, threshold, max_peaks, row_offsets,
                                               d_peaks);
   check_cuda(cudaGetLastError(), "nms launch");
+}
+
+void launch_upsample_nms(const float* d_in, int planes, int h, int w, float threshold, int max_peaks, float* d_out,
+                         int* d_counts, float* d_peaks, void* d_scratch, size_t scratch_bytes, cudaStream_t stream) {
+  static const bool split = [] {  // AVEC_UPSNMS_SPLIT=1: the two separate launches (A/B)
+    const char* e = std::getenv("AVEC_UPSNMS_SPLIT");
+    return e && e[0] == '1';
+  }();
+  const size_t tiles = static_cast<size_t>(planes) * h;
+  const size_t need = tiles * sizeof(int) + 16 + tiles * max_peaks * sizeof(NmsPeak);
+  if (!split && w >= 3 && w <= 256 && tiles <= 0x7fffffff && planes <= 65535 && max_peaks > 0 &&
+      (reinterpret_cast<uintptr_t>(d_out) & 15) == 0 && need <= scratch_bytes) {
+    int* tile_counts = static_cast<int*>(d_scratch);
+    auto* tile_peaks = reinterpret_cast<NmsPeak*>(reinterpret_cast<uintptr_t>(tile_counts + tiles + 15) & ~uintptr_t(15));
+    const int threads = (w + 31) / 32 * 32;
+    // registers capped for 3 blocks of 256 threads per SM (80, no spills): 50 vs 54 us uncapped (94)
+    ups8_nms_kernel<<<static_cast<unsigned>(tiles), threads, 0, stream>>>(d_in, h, w, threshold, max_peaks, d_out,
+                                                                         tile_counts, tile_peaks);
+    nms_gather_kernel<<<dim3(planes, (max_peaks + 63) / 64), 64, (h + 1) * sizeof(int), stream>>>(
+        d_out, 8 * h, 8 * w, h, max_peaks, max_peaks, tile_counts, tile_peaks, d_counts, d_peaks);
+    check_cuda(cudaGetLastError(), "upsample+nms launch");
+    return;
+  }
+  launch_upsample(d_in, planes, h, w, 8, d_out, stream);
+  launch_nms(d_out, planes, 8 * h, 8 * w, threshold, max_peaks, d_counts, d_peaks, d_scratch, scratch_bytes, stream);
 }
 
 }  // namespace avec

@@ -5,6 +5,7 @@ the streaming layers"):
     (32x1312x736) FrameData, device-resident;
   * x8 bilinear upsample of the C2 net output (8 x 57 planes of 46x82);
   * 3x3 peak NMS on the 8 x 18 upsampled body-part heatmaps;
+  * the fused x8 upsample + NMS on those 144 planes (checked identical to the pair);
   * the pose net's remaining max-pool (one C2 forward).
 
     ncu --set full -k regex:'segmean|upsample|nms|maxpool' python tools/profile_streaming.py
@@ -52,6 +53,37 @@ def main():
         be.nms_device(heat.data_ptr(), heat.shape[0], 368, 656, thr, maxp, cnt.data_ptr(), pk.data_ptr())
         torch.cuda.synchronize()
         print("ok", q, int(cnt.sum()))
+    # the fused pair on the same 144 heatmap planes (upsample written once,
+    # not read back), against the two launches it replaces
+    src = out.view(8, 57, 46, 82)[:, :18].contiguous()
+    up2 = torch.empty((144, 368, 656), dtype=torch.float32, device="cuda")
+    cnt2 = torch.zeros_like(cnt)
+    pk2 = torch.zeros_like(pk)
+    for q in (0.5, 0.999):
+        thr = float(torch.quantile(sample, q))
+        be.upsample_nms_device(src.data_ptr(), 144, 46, 82, 8, thr, maxp, up2.data_ptr(), cnt2.data_ptr(),
+                               pk2.data_ptr())
+        be.nms_device(heat.data_ptr(), 144, 368, 656, thr, maxp, cnt.data_ptr(), pk.data_ptr())
+        torch.cuda.synchronize()
+        same = torch.equal(up2, heat) and torch.equal(cnt2, cnt) and torch.equal(pk2, pk)
+        print("fused ok", q, int(cnt2.sum()), "identical" if same else "DIFFERENT")
+    if "--time" in sys.argv:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        thr = float(torch.quantile(sample, 0.5))
+        for name, fn in (("split", lambda: (be.upsample_device(src.data_ptr(), 144, 46, 82, 8, up2.data_ptr()),
+                                            be.nms_device(up2.data_ptr(), 144, 368, 656, thr, maxp,
+                                                          cnt2.data_ptr(), pk2.data_ptr()))),
+                         ("fused", lambda: be.upsample_nms_device(src.data_ptr(), 144, 46, 82, 8, thr, maxp,
+                                                                  up2.data_ptr(), cnt2.data_ptr(), pk2.data_ptr()))):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            ev[0].record()
+            for _ in range(20):
+                fn()
+            ev[1].record()
+            torch.cuda.synchronize()
+            print(name, "%.1f us per call (incl. the per-call host sync)" % (ev[0].elapsed_time(ev[1]) * 1e3 / 20))
     be.close()
 
 
