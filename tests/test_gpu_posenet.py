@@ -199,6 +199,18 @@ def test_upsample_and_nms_bitexact(net):
         assert pk[p, :n, 2:4].tobytes() == ref.tobytes()
         assert pk[p, :n, 4].tobytes() == sc.tobytes()
     assert total > 0
+    # the fused entry on the net's own heatmap planes: same planes and peaks
+    src = np.ascontiguousarray(planes.reshape(NB, 57, H // 8, W // 8)[:, :18]).reshape(-1, H // 8, W // 8)
+    d_src = torch.from_numpy(src).cuda()
+    d_up2 = torch.empty_like(d_heat)
+    d_cnt2 = torch.zeros_like(d_cnt)
+    d_pk2 = torch.zeros_like(d_pk)
+    torch.cuda.synchronize()
+    be.upsample_nms_device(d_src.data_ptr(), src.shape[0], H // 8, W // 8, 8, thr, maxp, d_up2.data_ptr(),
+                           d_cnt2.data_ptr(), d_pk2.data_ptr())
+    assert d_up2.cpu().numpy().tobytes() == heat.tobytes()
+    assert np.array_equal(d_cnt2.cpu().numpy(), cnt)
+    assert d_pk2.cpu().numpy().tobytes() == pk.tobytes()
 
 
 def test_nms_synthetic_peaks_and_edges(net):
