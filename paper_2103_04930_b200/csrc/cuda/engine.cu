@@ -1296,6 +1296,72 @@ void overlapped_segment_means(Slot* s, const float* in, float* out, uint64_t E, 
   check_cuda(cudaEventSynchronize(s->ev1), "overlapped sync");
 }
 
+// A pose-net cycle between pinned host buffers as two frame groups (frames
+// are independent; batch folded into channels, server.cpp:297-301): group
+// g's H2D (copy_in), its graph (slot stream, behind its H2D's event) and its
+// output's D2H (copy_out, behind the graph) chain by events, so group 1's
+// input crosses PCIe while group 0 computes and group 0's output returns
+// while group 1 computes: one synchronous cycle no longer pays its copies
+// in series. The group plan's buffers are shared by the groups, so each group
+// enters and leaves them by a device copy from/to the slot's staging (in
+// stream order on the slot stream). Only for large cycles (>= 64 MB of
+// frames): halving the batch costs the group plans' efficiency, which C5's
+// copies repay and C2's do not (bench.py, same box: C5 32x1312x736 e2e
+// 994 -> 1032 frames/s, one thread 854 -> 921; C2 8x656x368 e2e 2808 ->
+// 2643). AVEC_FWD_PIPE=0 turns it off (A/B).
+constexpr uint64_t kPipeMin = uint64_t(64) << 20;
+
+bool pipelined_forward_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("AVEC_FWD_PIPE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool pipelined_posenet(avec_ctx* ctx, Slot* s, const Model& m, int n_img, int h, int w, const float* in, float* out,
+                       uint64_t E, uint64_t K) {
+  const int gf = (n_img + 1) / 2;  // frames of group 0; group 1 takes the rest
+  s->d_in.ensure(E * 4, ctx->device);
+  s->d_out.ensure(K * 4, ctx->device);
+  while (s->chunk_ev.size() < 4) {
+    cudaEvent_t e = nullptr;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    s->chunk_ev.push_back(e);
+  }
+  const uint64_t fin = E / n_img, fout = K / n_img;  // elements per frame in / out
+  Plan* plans[2] = {get_plan(ctx, s, m, gf, h, w), nullptr};  // built (captured) before anything is queued
+  plans[1] = n_img - gf == gf ? plans[0] : get_plan(ctx, s, m, n_img - gf, h, w);
+  // both group plans must be resident at once (a one-plan cache, AVEC_PLANS_PER_SLOT=1, evicts the first)
+  if (!s->plans.count(std::make_tuple(m.id, gf, h, w))) return false;
+  check_cuda(cudaStreamSynchronize(s->stream), "slot idle");  // earlier users of the staging are done
+  check_cuda(cudaEventRecord(s->ev0, s->copy_in), "ev0");
+  for (int g = 0; g < 2; ++g) {
+    const int f0 = g ? gf : 0, nf = g ? n_img - gf : gf;
+    Plan* plan = plans[g];
+    float* din = s->d_in.as<float>() + uint64_t(f0) * fin;
+    float* dout = s->d_out.as<float>() + uint64_t(f0) * fout;
+    check_cuda(cudaMemcpyAsync(din, in + uint64_t(f0) * fin, uint64_t(nf) * fin * 4, cudaMemcpyHostToDevice,
+                               s->copy_in),
+               "group H2D");
+    check_cuda(cudaEventRecord(s->chunk_ev[2 * g], s->copy_in), "group event");
+    check_cuda(cudaStreamWaitEvent(s->stream, s->chunk_ev[2 * g], 0), "wait group H2D");
+    check_cuda(cudaMemcpyAsync(plan->in.p, din, uint64_t(nf) * fin * 4, cudaMemcpyDeviceToDevice, s->stream),
+               "group in");
+    check_cuda(cudaGraphLaunch(plan->graph, s->stream), "group graph");
+    check_cuda(cudaMemcpyAsync(dout, plan->out.p, uint64_t(nf) * fout * 4, cudaMemcpyDeviceToDevice, s->stream),
+               "group out");
+    check_cuda(cudaEventRecord(s->chunk_ev[2 * g + 1], s->stream), "group event");
+    check_cuda(cudaStreamWaitEvent(s->copy_out, s->chunk_ev[2 * g + 1], 0), "wait group graph");
+    check_cuda(cudaMemcpyAsync(out + uint64_t(f0) * fout, dout, uint64_t(nf) * fout * 4, cudaMemcpyDeviceToHost,
+                               s->copy_out),
+               "group D2H");
+  }
+  check_cuda(cudaEventRecord(s->ev1, s->copy_out), "ev1");
+  check_cuda(cudaEventSynchronize(s->ev1), "pipelined forward sync");
+  return true;
+}
+
 }  // namespace
 
 double forward_host(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint32_t h, uint32_t w,
@@ -1314,11 +1380,14 @@ double forward_host(avec_ctx* ctx, uint64_t handle, uint32_t n, uint32_t c, uint
   if (m.kind == AVEC_MODEL_POSENET) {
     int n_img = 0;
     posenet_shape(m, n, c, h, w, n_img);
-    Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
-    check_cuda(cudaEventRecord(s->ev0, s->stream), "ev0");
-    stage_h2d(s, plan->in.p, in, E * 4);
-    check_cuda(cudaGraphLaunch(plan->graph, s->stream), "graph launch");
-    stage_d2h(s, out, plan->out.p, K * 4);
+    if (!(n_img >= 2 && E * 4 >= kPipeMin && is_pinned(in) && is_pinned(out) && pipelined_forward_enabled() &&
+          pipelined_posenet(ctx, s, m, n_img, int(h), int(w), in, out, E, K))) {
+      Plan* plan = get_plan(ctx, s, m, n_img, int(h), int(w));
+      check_cuda(cudaEventRecord(s->ev0, s->stream), "ev0");
+      stage_h2d(s, plan->in.p, in, E * 4);
+      check_cuda(cudaGraphLaunch(plan->graph, s->stream), "graph launch");
+      stage_d2h(s, out, plan->out.p, K * 4);
+    }
   } else if (E * 4 >= kOverlapMin && is_pinned(in) && is_pinned(out)) {
     s->d_in.ensure(E * 4, ctx->device);
     s->d_out.ensure(K * 4, ctx->device);

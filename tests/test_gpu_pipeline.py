@@ -140,3 +140,32 @@ def test_server_pipelines_repeat_cycles(tmp_path):
     # the first cycle, so the second cycle may still run whole
     events = [json.loads(l)["event"] for l in log.read_text().splitlines() if l.strip()]
     assert cycles - 2 <= events.count("cycle_pipelined") <= cycles - 1
+
+
+@pytest.mark.parametrize("nb", [8, 7])
+def test_forward_pinned_is_two_frame_groups(be, nb):
+    """avec_forward between pinned host buffers runs a multi-frame pose-net
+    cycle as two frame groups whose copies overlap the other group's compute
+    (engine.cu pipelined_posenet, cycles of >= 64 MB of frames): its output
+    is the two groups' forwards, bit for bit (8 frames: 4 + 4; 7 frames:
+    4 + 3, two plan sizes)."""
+    from paper_2103_04930_b200 import Dims, Frame, PinnedBuffer, make_model, netspec
+    w, h = 1312, 736  # 8 frames: 92.7 MB
+    hd = be.register_model(make_model("openpose_coco", netspec.spec(), b"", netspec.COCO_DIVISOR))
+    dims = Dims(1, 3 * nb, h, w)
+    frames = O.batched_frame(w, h, nb, seed=11)
+    K = be.output_elems(hd, dims)
+    pin_in, pin_out = PinnedBuffer(frames.size), PinnedBuffer(K)
+    pin_in.array[:] = frames
+    for _ in range(2):  # the second cycle reuses the slot's staging and group plans
+        pin_out.array[:] = np.nan
+        be.forward(hd, Frame(dims, pin_in.array), out=pin_out.array)
+        got = pin_out.array.copy()
+        per_frame = K // nb
+        g0 = (nb + 1) // 2
+        for f0, n in ((0, g0), (g0, nb - g0)):
+            sub = frames.reshape(nb, -1)[f0:f0 + n].ravel()
+            want = be.forward(hd, Frame(Dims(1, 3 * n, h, w), sub)).data
+            assert got[f0 * per_frame:(f0 + n) * per_frame].tobytes() == want.tobytes(), f0
+    pin_in.free()
+    pin_out.free()
